@@ -1,0 +1,107 @@
+/* oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, sequential CPU oracle of the BF-AMG-GMRES linear-solve hot path of
+ * arXiv 1611.00127 with the
+ * readings of SURVEY.md section 8(c) (c.2 step by step, c.4 determinism contract).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * leg may load this library.  It shares no code, header or constant generator
+ * with the CUDA path (paper_1611_00127_b200/), and the CUDA path never loads it.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared (no FMA contraction, IEEE binary64,
+ * round to nearest: c.4 item 1).
+ */
+#ifndef BF_ORACLE_H
+#define BF_ORACLE_H
+#include <stdint.h>
+
+typedef struct {
+  int32_t nrows, ncols;
+  int64_t nnz;
+  int64_t *rp;   /* [nrows+1] */
+  int32_t *ci;   /* [nnz] strictly ascending per row */
+  double  *v;    /* [nnz] */
+} or_csr;
+
+typedef struct {
+  double   theta;          /* strength threshold (Q24), 0.25 */
+  int32_t  max_levels;     /* 25 (Q28) */
+  int32_t  max_coarse;     /* 64 (Q28) */
+  int32_t  smoother;       /* 0 l1-Jacobi, 1 Chebyshev (Q27) */
+  int32_t  nu_pre, nu_post;/* 1, 1 */
+  int32_t  cheb_degree;    /* 2 */
+  double   cheb_lo;        /* 0.3 */
+  uint64_t seed;           /* PMIS hash seed (Q25) */
+  int32_t  orth;           /* 0 CGS2, 1 CGS1 (Q30) */
+  int32_t  schur_as_printed; /* 0: A_sp (Q21); 1: literal P:L239 (A_pp) */
+  int32_t  interp_norm;    /* 1: weights normalised to P 1 = 1 (R8, default); 0: Q26 denominators */
+} or_options;
+
+#define OR_MAX_LEVELS 64
+
+typedef struct {
+  int32_t nlev;
+  or_csr A[OR_MAX_LEVELS];        /* A_0 .. A_{L} */
+  or_csr P[OR_MAX_LEVELS];        /* P_l : n_l x n_{l+1}, l < L */
+  or_csr R[OR_MAX_LEVELS];        /* R_l = P_l^T */
+  int8_t *cf[OR_MAX_LEVELS];      /* 1 = C, 0 = F (levels l < L) */
+  uint8_t *strong[OR_MAX_LEVELS]; /* per-nnz strength flags of A_l (l < L) */
+  double *dl1[OR_MAX_LEVELS];     /* l1 diagonal of every level */
+  double *lu;                     /* dense LU of A_L (row-major n_L x n_L) or NULL */
+  int32_t *piv;                   /* pivot rows */
+  or_options opt;
+} or_amg;
+
+typedef struct {
+  int32_t n;                      /* cells */
+  int32_t var_order;
+  /* the input Jacobian (BSR2 in canonical row-major (p,s) order) */
+  int64_t *brp; int32_t *bci; double *bv;
+  or_csr App, Aps, Asp, Ass, S;   /* field split and S~ */
+  double *dss;                    /* diag(A_ss) */
+  or_amg hss, hS;                 /* hierarchies for A_ss and S~ */
+  or_options opt;
+} or_bf;
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+const char *or_last_error(void);
+void or_default_options(or_options *o);
+uint32_t or_h32(uint64_t seed, int32_t level, int64_t i);
+
+void or_bsr_spmv(int32_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                 const double *x, double *y);
+void or_csr_spmv(const or_csr *A, const double *x, double *y);
+
+int  or_split(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
+              int32_t block_order, int32_t var_order,
+              or_csr *App, or_csr *Aps, or_csr *Asp, or_csr *Ass, double *dss);
+int  or_schur(const or_csr *App, const or_csr *Aps, const or_csr *Asp, const double *dss,
+              int32_t as_printed, or_csr *S);
+void or_strength(const or_csr *A, double theta, uint8_t *strong);
+void or_pmis(const or_csr *A, const uint8_t *strong, const uint32_t *h32, int8_t *cf);
+int  or_interp(const or_csr *A, const uint8_t *strong, const int8_t *cf, int32_t norm, or_csr *P);
+void or_transpose(const or_csr *P, or_csr *R);
+void or_matmul(const or_csr *A, const or_csr *B, or_csr *C);
+void or_l1diag(const or_csr *A, double *d);
+/* one smoothing pass (kind 0: l1-Jacobi, 1: Chebyshev of `degree` on [lo,1]) with diagonal d */
+void or_smooth(const or_csr *A, const double *d, const double *b, double *x, int32_t kind,
+               int32_t degree, double lo);
+int  or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h);
+void or_amg_free(or_amg *h);
+void or_vcycle(const or_amg *h, const double *b, double *x);
+void or_csr_free(or_csr *A);
+
+int  or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
+                 int32_t block_order, int32_t var_order, const or_options *o, or_bf **out);
+void or_bf_free(or_bf *b);
+void or_bf_apply(const or_bf *b, const double *v, double *z);
+void or_bf_spmv(const or_bf *b, const double *x, double *y);
+int  or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t restart,
+              int32_t maxit, int32_t *iters, double *res_hist, int32_t *converged,
+              double *final_relres);
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,442 @@
+"""Pins of the CPU oracle (oracle/) against what the paper and the mathematics fix
+(SURVEY.md c.5).  These tests never touch the CUDA path."""
+import os
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import oracle
+from oracle import CSR
+from workload import make_system, seeded_vector, Problem, CapillaryModel, jacobian, DAY
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def lap1d(n):
+    return sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1]).tocsr()
+
+
+def lap(n, d):
+    T = lap1d(n)
+    I = sp.identity(n)
+    if d == 2:
+        return (sp.kron(I, T) + sp.kron(T, I)).tocsr()
+    return (sp.kron(sp.kron(I, I), T) + sp.kron(sp.kron(I, T), I) + sp.kron(sp.kron(T, I), I)).tocsr()
+
+
+def tiny_system(dims=(4, 4, 1), config=1, gravity=True):
+    return make_system(config, gravity=gravity, dims=dims)
+
+
+def bsr_from_dense_blocks(App, Aps, Asp, Ass):
+    """Build a BSR2 (full cell adjacency = union of block patterns) from 4 dense n x n blocks."""
+    from workload import BSR2
+    n = App.shape[0]
+    pat = (App != 0) | (Aps != 0) | (Asp != 0) | (Ass != 0) | np.eye(n, dtype=bool)
+    rp = [0]
+    ci, vals = [], []
+    for r in range(n):
+        for c in np.nonzero(pat[r])[0]:
+            ci.append(c)
+            vals.append([[App[r, c], Aps[r, c]], [Asp[r, c], Ass[r, c]]])
+        rp.append(len(ci))
+    return BSR2(n, np.array(rp, np.int32), np.array(ci, np.int32), np.array(vals, np.float64))
+
+
+# ---------------------------------------------------------------------------- split / S~
+def test_split_restrictions_and_roundtrip():
+    """R_p R_p^T = I, R_s R_s^T = I, R_p^T R_p + R_s^T R_s = I, and the four
+    blocks re-interleave to J (exact zeros dropped except the diagonal, Q23)."""
+    prob, J, rhs = tiny_system((5, 4, 1))
+    n = J.n
+    Rp = sp.csr_matrix((np.ones(n), (np.arange(n), 2 * np.arange(n))), shape=(n, 2 * n))
+    Rs = sp.csr_matrix((np.ones(n), (np.arange(n), 2 * np.arange(n) + 1)), shape=(n, 2 * n))
+    assert (Rp @ Rp.T != sp.identity(n)).nnz == 0 and (Rs @ Rs.T != sp.identity(n)).nnz == 0
+    assert ((Rp.T @ Rp + Rs.T @ Rs) != sp.identity(2 * n)).nnz == 0
+    s = oracle.split(J)
+    D = J.to_dense()
+    B = {k: s[k].to_dense() for k in ("App", "Aps", "Asp", "Ass")}
+    assert np.array_equal(B["App"], (Rp @ D @ Rp.T)) and np.array_equal(B["Aps"], Rp @ D @ Rs.T)
+    assert np.array_equal(B["Asp"], Rs @ D @ Rp.T) and np.array_equal(B["Ass"], Rs @ D @ Rs.T)
+    for k in B:   # pattern: nonzeros plus the diagonal
+        A = s[k]
+        rows = np.repeat(np.arange(n), np.diff(A.rp))
+        assert np.all((A.v != 0) | (A.ci == rows))
+        assert np.count_nonzero(B[k] - np.diag(np.diag(B[k]))) == np.count_nonzero((A.v != 0) & (A.ci != rows))
+    assert np.array_equal(s["dss"], np.diag(B["Ass"]))
+    # block_order = 1 (column-major blocks) gives the same split
+    s2 = oracle.split(J, block_order=1)
+    for k in ("App", "Aps", "Asp", "Ass"):
+        assert np.array_equal(s2[k].to_dense(), B[k])
+
+
+def test_split_zero_diag_error():
+    prob, J, rhs = tiny_system((3, 3, 1))
+    J.vals[J.row_ptr[4] + 2, 1, 1] = 0.0          # diag block of cell 4 (row 4: -y,-x,diag,...)
+    assert J.col_idx[J.row_ptr[4] + 2] == 4
+    with pytest.raises(RuntimeError, match="cell 4"):
+        oracle.split(J)
+
+
+def test_schur_toy_and_special_cases():
+    # toy [2],[1],[1],[4] -> 1.75
+    J = bsr_from_dense_blocks(np.array([[2.0]]), np.array([[1.0]]), np.array([[1.0]]), np.array([[4.0]]))
+    s = oracle.split(J)
+    S = oracle.schur(s["App"], s["Aps"], s["Asp"], s["dss"])
+    assert S.to_dense()[0, 0] == 1.75
+    rng = np.random.default_rng(3)
+    n = 9
+    App = -rng.uniform(0, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.4) + 6 * np.eye(n)
+    Asp = -rng.uniform(0, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.4) + 5 * np.eye(n)
+    Ass = -rng.uniform(0, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.4) + 7 * np.eye(n)
+    # A_ps = 0 -> S~ = A_pp exactly
+    s = oracle.split(bsr_from_dense_blocks(App, np.zeros((n, n)), Asp, Ass))
+    assert np.array_equal(oracle.schur(s["App"], s["Aps"], s["Asp"], s["dss"]).to_dense(), App)
+    # A_ss diagonal -> S~ = exact Schur complement
+    Aps = rng.uniform(0, 1, (n, n)) * (rng.uniform(size=(n, n)) < 0.4) - 3 * np.eye(n)
+    Dss = np.diag(np.diag(Ass))
+    s = oracle.split(bsr_from_dense_blocks(App, Aps, Asp, Dss))
+    S = oracle.schur(s["App"], s["Aps"], s["Asp"], s["dss"]).to_dense()
+    Sex = App - Aps @ np.linalg.solve(Dss, Asp)
+    assert np.max(np.abs(S - Sex)) <= 1e-13 * np.max(np.abs(Sex))
+
+
+def test_schur_vs_dense_on_generated_jacobian():
+    """S~ = A_pp - A_ps diag(A_ss)^-1 A_sp (Q21) against dense numpy; the literal
+    printed form (A_pp in the last slot) is available and differs."""
+    for dims in ((4, 4, 1), (3, 3, 3)):
+        prob, J, rhs = tiny_system(dims, config=2)
+        D = J.to_dense()
+        App, Aps, Asp, Ass = D[0::2, 0::2], D[0::2, 1::2], D[1::2, 0::2], D[1::2, 1::2]
+        s = oracle.split(J)
+        S = oracle.schur(s["App"], s["Aps"], s["Asp"], s["dss"])
+        Sd = App - Aps @ np.diag(1 / np.diag(Ass)) @ Asp
+        scale = np.abs(App).max() + np.abs(Aps @ np.diag(1 / np.diag(Ass)) @ Asp).max()
+        assert np.max(np.abs(S.to_dense() - Sd)) <= 1e-14 * scale
+        # pattern = pattern(A_pp) U pattern(A_ps * A_sp)
+        pat = (s["App"].to_dense() != 0) | np.eye(J.n, dtype=bool) | \
+              ((np.abs(s["Aps"].to_dense()) > 0).astype(int) @ (np.abs(s["Asp"].to_dense()) > 0).astype(int) > 0)
+        got = np.zeros((J.n, J.n), bool)
+        rows = np.repeat(np.arange(J.n), np.diff(S.rp))
+        got[rows, S.ci] = True
+        assert np.array_equal(got, pat)
+        Sp = oracle.schur(s["App"], s["Aps"], s["Asp"], s["dss"], as_printed=1).to_dense()
+        assert np.allclose(Sp, App - Aps @ np.diag(1 / np.diag(Ass)) @ App, rtol=1e-13, atol=1e-14 * scale)
+
+
+def test_block_lu_identity():
+    """BJ oracle check 2: J = [[I, A_ps A_ss^-1],[0,I]] diag(S, A_ss) [[I,0],[A_ss^-1 A_sp, I]]
+     with the oracle's field split, to 1e-12 relative."""
+    for dims in ((3, 3, 1), (4, 4, 1), (2, 2, 2)):
+        prob, J, rhs = tiny_system(dims, config=2)
+        s = oracle.split(J)
+        App, Aps, Asp, Ass = (s[k].to_dense() for k in ("App", "Aps", "Asp", "Ass"))
+        n = J.n
+        I, Z = np.eye(n), np.zeros((n, n))
+        Ainv = np.linalg.inv(Ass)
+        S = App - Aps @ Ainv @ Asp
+        U = np.block([[I, Aps @ Ainv], [Z, I]])
+        Dg = np.block([[S, Z], [Z, Ass]])
+        L = np.block([[I, Z], [Ainv @ Asp, I]])
+        Jv = np.block([[App, Aps], [Asp, Ass]])
+        perm = np.concatenate([np.arange(0, 2 * n, 2), np.arange(1, 2 * n, 2)])
+        assert np.array_equal(Jv, J.to_dense()[np.ix_(perm, perm)])
+        assert np.max(np.abs(U @ Dg @ L - Jv)) <= 1e-12 * np.max(np.abs(Jv))
+        # M = U diag(S, A_ss) = [[S, A_ps],[0, A_ss]]
+        assert np.max(np.abs(U @ Dg - np.block([[S, Aps], [Z, Ass]]))) <= 1e-12 * np.max(np.abs(Jv))
+
+
+# ---------------------------------------------------------------------------- BF apply and exactness
+BIG = 10 ** 6     # max_coarse >= n makes level 0 the coarsest: the V-cycle is a dense LU solve
+
+
+def test_algorithm3_equals_matrix_form():
+    """Alg. 3 with exact inner solves equals M_bf^-1 of P:L252-257 to 1e-12."""
+    for dims in ((4, 4, 1), (3, 3, 2)):
+        prob, J, rhs = tiny_system(dims, config=1)
+        bf = oracle.BF(J, max_coarse=BIG)
+        assert bf.nlev(0) == 1 and bf.nlev(1) == 1
+        App, Aps, Ass = (bf.matrix(k).to_dense() for k in ("App", "Aps", "Ass"))
+        St = bf.matrix("S").to_dense()
+        n = J.n
+        Si, Ai = np.linalg.inv(St), np.linalg.inv(Ass)
+        Mbf = np.block([[Si, -Si @ Aps @ Ai], [np.zeros((n, n)), Ai]])
+        perm = np.concatenate([np.arange(0, 2 * n, 2), np.arange(1, 2 * n, 2)])
+        for seed in range(3):
+            v = seeded_vector(2 * n, seed)
+            z = bf.apply(v)
+            zv = Mbf @ v[perm]
+            assert np.max(np.abs(z[perm] - zv)) <= 1e-12 * np.max(np.abs(zv))
+
+
+def test_bf_exactness_gmres_iterations():
+    """With exact inner solves: A_ss diagonal -> S~ = S -> (J M^-1 - I)^2 = 0 -> GMRES <= 2
+    iterations; A_sp = 0 -> M = J -> 1 iteration."""
+    prob, J, rhs = tiny_system((5, 4, 1), config=1)
+    D = J.to_dense()
+    App, Aps, Asp, Ass = D[0::2, 0::2], D[0::2, 1::2], D[1::2, 0::2], D[1::2, 1::2]
+    Jd = bsr_from_dense_blocks(App, Aps, Asp, np.diag(np.diag(Ass)))
+    r = oracle.BF(Jd, max_coarse=BIG).gmres(rhs, tol=1e-12)
+    assert r["converged"] and r["iters"] <= 2
+    J0 = bsr_from_dense_blocks(App, Aps, np.zeros_like(Asp), Ass)
+    r = oracle.BF(J0, max_coarse=BIG).gmres(rhs, tol=1e-12)
+    assert r["converged"] and r["iters"] == 1
+    # identity Jacobian -> 1 iteration
+    n = J.n
+    Ji = bsr_from_dense_blocks(np.eye(n), np.zeros((n, n)), np.zeros((n, n)), np.eye(n))
+    r = oracle.BF(Ji).gmres(rhs, tol=1e-12)
+    assert r["iters"] == 1 and r["converged"] and np.allclose(r["x"], rhs, rtol=1e-14)
+
+
+# ---------------------------------------------------------------------------- strength / PMIS
+def test_pmis_hand_cases():
+    A = CSR.from_scipy(lap1d(7))
+    strong = oracle.strength(A, 0.25)
+    rows = np.repeat(np.arange(7), np.diff(A.rp))
+    assert np.array_equal(strong.astype(bool), A.ci != rows)
+    n_cases = 0
+    for line in open(os.path.join(GOLD, "pmis_hand.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, hs, cf = [x.strip() for x in line.split("|")]
+        got = oracle.pmis(A, strong, np.array(hs.split(), np.uint32))
+        assert np.array_equal(got, np.array(cf.split(), np.int8)), name
+        n_cases += 1
+    assert n_cases == 2
+
+
+def test_strength_definition():
+    # sign-aware: row with negative diagonal takes positive off-diagonals as strong (Q24)
+    D = np.array([[4.0, -1.0, -0.2, 0.5], [-1.0, 4.0, -1.0, 0.0], [1.0, 0.5, -3.0, 0.1], [0.0, 0.0, 0.0, 2.0]])
+    A = CSR.from_dense(D)
+    s = oracle.strength(A, 0.25)
+    got = np.zeros_like(D, dtype=bool)
+    rows = np.repeat(np.arange(4), np.diff(A.rp))
+    got[rows, A.ci] = s.astype(bool)
+    exp = np.array([[0, 1, 0, 0], [1, 0, 1, 0], [1, 1, 0, 0], [0, 0, 0, 0]], bool)
+    assert np.array_equal(got, exp)
+
+
+def test_diagonal_matrix_single_level():
+    A = CSR.from_scipy(sp.diags(np.linspace(1, 2, 500)).tocsr())
+    amg = oracle.AMG(A)
+    assert amg.nlev == 1
+    b = seeded_vector(500, 1)
+    assert np.allclose(amg.vcycle(b), b / np.linspace(1, 2, 500), rtol=1e-15)
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_pmis_invariants(config):
+    prob, J, rhs = tiny_system((12, 10, 1) if config == 1 else (8, 7, 6), config=config)
+    bf = oracle.BF(J)
+    for which in (0, 1):
+        for l in range(bf.nlev(which) - 1):
+            L = bf.level(which, l)
+            A, cf, strong = L["A"], L["cf"], L["strong"].astype(bool)
+            n = A.nrows
+            assert set(np.unique(cf)) <= {0, 1}
+            rows = np.repeat(np.arange(n), np.diff(A.rp))
+            lam = np.bincount(A.ci[strong], minlength=n)
+            hasC = np.bincount(rows[strong & (cf[A.ci] == 1)], minlength=n) > 0
+            # every F point either had lambda = 0 or has a strong C neighbour
+            assert np.all((cf == 1) | (lam == 0) | hasC)
+            # repeatability (bitwise)
+            hh = np.array([oracle.h32(0x1611, l, i) for i in range(n)], np.uint32)
+            assert np.array_equal(oracle.pmis(A, strong.astype(np.uint8), hh), cf)
+
+
+# ---------------------------------------------------------------------------- interpolation / Galerkin
+def test_interp_closed_forms():
+    A = CSR.from_scipy(lap1d(9))
+    strong = oracle.strength(A)
+    cf = np.array([0, 1, 0, 1, 0, 1, 0, 1, 0], np.int8)
+    for norm in (0, 1):
+        P = oracle.interp(A, strong, cf, norm=norm).to_dense()
+        assert np.array_equal(P[1::2], np.eye(4))                 # C rows are unit rows
+        for i in (2, 4, 6):
+            assert P[i, i // 2 - 1] == 0.5 and P[i, i // 2] == 0.5   # linear interpolation
+        assert P[0, 0] == (0.5 if norm == 0 else 1.0)             # end row: row sum 1 != 0
+    # C F F C: the F next to a C has no common C with its strong F neighbour -> lumping, w = 1
+    A = CSR.from_scipy(sp.csr_matrix(np.array([[1.0, -1, 0, 0], [-1, 2, -1, 0], [0, -1, 2, -1], [0, 0, -1, 1]])))
+    P = oracle.interp(A, oracle.strength(A), np.array([1, 0, 0, 1], np.int8), norm=0).to_dense()
+    assert P[1, 0] == 1.0 and P[2, 1] == 1.0 and P[1, 1] == 0.0 and P.shape == (4, 2)
+
+
+def test_interp_zero_row_sum_preserves_constants():
+    A = lap(12, 2).tolil()
+    # pure-Neumann-like zero row sums
+    A.setdiag(0)
+    A = A.tocsr()
+    A = A - sp.diags(np.asarray(A.sum(1)).ravel())
+    Ac = CSR.from_scipy(A.tocsr())
+    for norm in (0, 1):
+        amgP = None
+        strong = oracle.strength(Ac)
+        hh = np.array([oracle.h32(5, 0, i) for i in range(Ac.nrows)], np.uint32)
+        cf = oracle.pmis(Ac, strong, hh)
+        P = oracle.interp(Ac, strong, cf, norm=norm).to_scipy()
+        ps = P @ np.ones(P.shape[1])
+        nonempty = np.diff(P.indptr) > 0
+        assert np.allclose(ps[nonempty], 1.0, rtol=0, atol=1e-14)
+
+
+def test_galerkin_closed_form():
+    """1D Poisson on 2M+1 points, C at odd indices, linear interpolation (Q26 denominators):
+    A_c = 1/2 tridiag(-1,2,-1) exactly (SURVEY c.5 Galerkin)."""
+    M = 6
+    A = CSR.from_scipy(lap1d(2 * M + 1))
+    cf = np.array([i % 2 for i in range(2 * M + 1)], np.int8)
+    P = oracle.interp(A, oracle.strength(A), cf, norm=0)
+    R = oracle.transpose(P)
+    Ac = oracle.matmul(R, oracle.matmul(A, P))
+    assert np.array_equal(Ac.to_dense(), 0.5 * lap1d(M).toarray())
+    assert np.array_equal(R.to_dense(), P.to_dense().T)
+
+
+@pytest.mark.parametrize("config", [1, 2, 4])
+def test_hierarchy_vs_dense(config):
+    """Every level: P^T A P against dense numpy <= 1e-12 relative; R = P^T exactly."""
+    dims = {1: (16, 16, 1), 2: (8, 8, 8), 4: (40, 6, 8)}[config]
+    prob, J, rhs = tiny_system(dims, config=config)
+    bf = oracle.BF(J)
+    for which in (0, 1):
+        for l in range(bf.nlev(which) - 1):
+            L, Ln = bf.level(which, l), bf.level(which, l + 1)
+            A, P, R = L["A"].to_dense(), L["P"].to_dense(), L["R"].to_dense()
+            assert np.array_equal(R, P.T)
+            Ac = P.T @ A @ P
+            assert np.max(np.abs(Ln["A"].to_dense() - Ac)) <= 1e-12 * np.max(np.abs(Ac))
+            d = A.diagonal() + (np.abs(A).sum(1) - np.abs(A.diagonal()))
+            assert np.allclose(L["dl1"], d, rtol=1e-14)
+
+
+def test_coarse_lu_solve():
+    rng = np.random.default_rng(2)
+    D = rng.uniform(-1, 1, (40, 40)) * (rng.uniform(size=(40, 40)) < 0.3) + 5 * np.eye(40)
+    amg = oracle.AMG(CSR.from_dense(D))
+    assert amg.nlev == 1
+    b = seeded_vector(40, 3)
+    x = amg.vcycle(b)
+    assert np.max(np.abs(x - np.linalg.solve(D, b))) <= 1e-12 * np.linalg.cond(D) * np.max(np.abs(x))
+
+
+def test_chebyshev_error_reduction():
+    """On diag(lambda), lambda in [lo,1] with d = 1, one degree-m Chebyshev pass reduces the error
+    by max |p(lambda)| = 1/T_m((1+lo)/(1-lo)) (Q27)."""
+    lo = 0.3
+    lam = np.linspace(lo, 1.0, 2001)
+    A = CSR.from_scipy(sp.diags(lam).tocsr())
+    for m in (1, 2, 3, 4):
+        e0 = np.ones_like(lam)
+        x = oracle.smooth(A, np.ones_like(lam), np.zeros_like(lam), e0, kind=1, degree=m, lo=lo)
+        sigma = (1 + lo) / (1 - lo)
+        Tm = np.cosh(m * np.arccosh(sigma))
+        assert abs(np.max(np.abs(x)) - 1 / Tm) <= 1e-12
+    # l1-Jacobi pass: x <- x + (b - A x)/d
+    x = oracle.smooth(A, 2 * np.ones_like(lam), np.ones_like(lam), np.zeros_like(lam), kind=0)
+    assert np.allclose(x, 0.5)
+
+
+# ---------------------------------------------------------------------------- V-cycle
+def test_vcycle_basic_properties():
+    prob, J, rhs = tiny_system((16, 12, 1), config=1)
+    bf = oracle.BF(J)
+    n = J.n
+    for which in (0, 1):
+        assert np.all(bf.vcycle(which, np.zeros(n)) == 0.0)
+        a, b = seeded_vector(n, 1), seeded_vector(n, 2)
+        lin = bf.vcycle(which, 2.0 * a - 3.0 * b)
+        ref = 2.0 * bf.vcycle(which, a) - 3.0 * bf.vcycle(which, b)
+        assert np.max(np.abs(lin - ref)) <= 1e-12 * np.max(np.abs(ref))
+    amg = oracle.AMG(CSR.from_scipy(lap(6, 2)))
+    assert amg.nlev == 1
+    b = seeded_vector(36, 4)
+    assert np.allclose(lap(6, 2) @ amg.vcycle(b), b, rtol=1e-12, atol=1e-12)
+
+
+def _conv_factor(A, amg, its=14):
+    x = seeded_vector(A.shape[0], 11)
+    rs = []
+    for _ in range(its):
+        r = -A @ x
+        rs.append(np.linalg.norm(r))
+        x = x + amg.vcycle(r)
+    return rs[-1] / rs[-2]
+
+
+def test_poisson_convergence_factor():
+    """BJ oracle check 3: asymptotic V(1,1) l1-Jacobi convergence factor on the 2D 5-point /
+    3D 7-point Laplacian, bounded and non-growing under refinement.  Bound calibrated once for
+    PMIS + classical interpolation + l1-Jacobi (l1-Jacobi on the Laplacian is Jacobi damped by
+    1/2, smoothing factor 3/4): 2D <= 0.75, 3D <= 0.70, growth <= +0.05 per refinement."""
+    for d, sizes, bound in ((2, (32, 64, 128), 0.75), (3, (16, 32), 0.70)):
+        f = []
+        for m in sizes:
+            A = lap(m, d)
+            f.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A))))
+        assert max(f) <= bound, (d, f)
+        assert all(f[i + 1] <= f[i] + 0.05 for i in range(len(f) - 1)), (d, f)
+
+
+# ---------------------------------------------------------------------------- GMRES / whole solve
+def test_manufactured_solution():
+    """BJ oracle check 4: seeded x*, b = J x*, tol 1e-12 -> |x - x*|/|x*| <= 10 kappa 1e-12."""
+    for config, dims in ((1, (8, 8, 1)), (2, (5, 5, 4))):
+        prob, J, rhs = tiny_system(dims, config=config)
+        D = J.to_dense()
+        xs = seeded_vector(2 * J.n, 5)
+        b = D @ xs
+        r = oracle.BF(J).gmres(b, tol=1e-12, maxit=400)
+        assert r["converged"]
+        kappa = np.linalg.cond(D)
+        assert np.linalg.norm(r["x"] - xs) / np.linalg.norm(xs) <= 10 * kappa * 1e-12
+        assert np.linalg.norm(b - D @ r["x"]) / np.linalg.norm(b) <= 1e-12
+        xsp = spla.spsolve(J.to_scipy().tocsc(), b)
+        assert np.linalg.norm(r["x"] - xsp) / np.linalg.norm(xsp) <= 10 * kappa * 1e-12
+
+
+def test_gmres_vs_scipy_and_monotone():
+    """Against scipy.sparse.linalg.gmres on J M^-1 with the oracle's BF apply as the operator
+    (same restart 30, rtol 1e-8, x0 = 0): iteration counts within +-2; non-increasing estimates."""
+    prob, J, rhs = make_system(1)
+    bf = oracle.BF(J)
+    r = bf.gmres(rhs, tol=1e-8, restart=30, maxit=500)
+    assert r["converged"]
+    assert np.all(np.diff(r["hist"]) <= 1e-15)
+    Jm = J.to_scipy().tocsr()
+    n2 = 2 * J.n
+    op = spla.LinearOperator((n2, n2), matvec=lambda v: Jm @ bf.apply(v))
+    cnt = [0]
+    y, info = spla.gmres(op, rhs, rtol=1e-8, restart=30, maxiter=50,
+                         callback=lambda res: cnt.__setitem__(0, cnt[0] + 1), callback_type="pr_norm")
+    assert info == 0
+    assert abs(cnt[0] - r["iters"]) <= 2, (cnt[0], r["iters"])
+    D = J.to_scipy()
+    assert np.linalg.norm(rhs - D @ r["x"]) / np.linalg.norm(rhs) <= 1e-8
+    assert abs(r["relres"] - np.linalg.norm(rhs - D @ r["x"]) / np.linalg.norm(rhs)) <= 1e-12
+
+
+def test_gmres_maxit_and_zero_rhs():
+    prob, J, rhs = make_system(1, dims=(10, 10, 1))
+    bf = oracle.BF(J)
+    r = bf.gmres(rhs, tol=1e-14, maxit=5)
+    assert r["iters"] == 5 and not r["converged"]
+    r = bf.gmres(np.zeros_like(rhs))
+    assert r["iters"] == 0 and r["converged"] and np.all(r["x"] == 0)
+    # var_order = 1 (S_n first) on the swapped system gives the swapped solution
+    from workload import BSR2
+    Jsw = BSR2(J.n, J.row_ptr, J.col_idx, np.ascontiguousarray(J.vals[:, ::-1, ::-1]))
+    r0 = bf.gmres(rhs, tol=1e-10)
+    bsw = rhs.reshape(-1, 2)[:, ::-1].ravel().copy()
+    r1 = oracle.BF(Jsw, var_order=1).gmres(bsw, tol=1e-10)
+    assert r0["iters"] == r1["iters"]
+    xs = r1["x"].reshape(-1, 2)[:, ::-1].ravel()
+    assert np.linalg.norm(xs - r0["x"]) <= 1e-9 * np.linalg.norm(r0["x"])
+
+
+def test_hash_deterministic():
+    hs = np.array([oracle.h32(0x1611, 0, i) for i in range(4096)], np.uint64)
+    assert len(np.unique(hs)) > 4080          # no systematic collisions
+    assert 0.4 < (hs / 2**32).mean() < 0.6
+    assert oracle.h32(1, 2, 3) == oracle.h32(1, 2, 3) and oracle.h32(1, 2, 3) != oracle.h32(1, 3, 3)
