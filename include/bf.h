@@ -1,0 +1,153 @@
+/* bf.h -- C-ABI of the B200-native BF-AMG-GMRES linear solver (libbf.so).
+ *
+ * The library solves  J c = q for the 2x2-block Jacobian of the fully
+ * implicit two-phase (p_w, S_n) cell-centred FV model by
+ * restarted GMRES right-preconditioned as  J M^-1 c^ = q, c = M^-1 c^
+ * (`precon-system`) with the block-factorization preconditioner
+ * M_bf (Algorithm 3; matrix form `m_bf`): one AMG
+ * V-cycle on A_ss, the A_ps coupling, one AMG V-cycle on the SIMPLE approximate
+ * Schur complement  S~ = A_pp - A_ps diag(A_ss)^-1 A_sp  (`SIMPLE-Schur`,
+ * P:L236-241, read with A_sp in the last slot -- DESIGN.md R1).
+ *
+ * Everything on the path runs in hand-written CUDA kernels for sm_100a on one
+ * GPU in fp64.  No torch types cross this boundary: plain pointers and sizes.
+ *
+ * Conventions
+ *   - cells c = 0..n_cells-1, c = i + nx*(j + ny*k) (lexicographic).
+ *   - Jacobian: point-interleaved 2x2 BSR ("point" ordering):
+ *       row_ptr[n_cells+1] (int32, row_ptr[0] = 0, non-decreasing),
+ *       col_idx[nnzb]      (int32, strictly ascending within each row, diagonal present),
+ *       vals[4*nnzb]       (f64, one 2x2 block per entry).
+ *     block_order 0: row-major  {b00, b01, b10, b11};  1: column-major {b00, b10, b01, b11}.
+ *     var_order   0: index 0 is (water equation, p_w), index 1 is (n-phase equation, S_n),
+ *                    so the canonical block is [[a_pp, a_ps], [a_sp, a_ss]];
+ *                 1: indices swapped (S_n first).
+ *   - Vectors (rhs, x, ...) have length 2*n_cells, interleaved in the same var_order:
+ *     x[2c + ip] = dp_c, x[2c + is] = dS_c (ip = var_order, is = 1 - var_order).
+ *   - All calls are ordered on the CUDA stream passed in (cudaStream_t as void*;
+ *     NULL = legacy default stream) and block until their host outputs are ready.
+ *
+ * Ownership: bf_setup copies the Jacobian (host or device) into memory owned by the
+ * handle (stream-ordered allocations on the setup stream).  The handle owns every
+ * device buffer it allocates; bf_destroy frees them.  Caller buffers are never
+ * retained after a call returns.
+ *
+ * Errors: every call returns a bf_status; no exception crosses the ABI.  On error
+ * bf_last_error(h) (or bf_last_error(NULL) for a failed bf_setup) names the failing
+ * item (cell, row, level, pivot).  Non-convergence of GMRES is NOT an error:
+ * bf_solve returns BF_OK with *converged = 0 and x holding the last iterate.
+ * A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef BF_H
+#define BF_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BF_OK = 0,
+  BF_ERR_ARG = 1,             /* bad argument / size / option */
+  BF_ERR_PATTERN = 2,         /* row_ptr not monotone, col_idx not ascending / out of range, no diagonal block */
+  BF_ERR_NONFINITE = 3,       /* NaN/Inf in the Jacobian values or the rhs */
+  BF_ERR_ZERO_DIAG = 4,       /* A_ss(c,c) == 0 (S~ needs diag(A_ss)^-1) */
+  BF_ERR_COARSE_SINGULAR = 5, /* coarsest AMG matrix singular (|pivot| <= 1e-14 max|a|) */
+  BF_ERR_CUDA = 6,            /* CUDA runtime error (message carries cudaGetErrorString) */
+  BF_ERR_OOM = 7,             /* device allocation failed */
+  BF_ERR_LIMIT = 8            /* an implementation limit was exceeded (message names it) */
+} bf_status;
+
+typedef struct {
+  int32_t nx, ny, nz;          /* grid; n_cells must equal nx*ny*nz (nx=n_cells,ny=nz=1 allowed) */
+  int32_t n_cells;             /* block rows */
+  int64_t nnzb;                /* number of 2x2 blocks (== row_ptr[n_cells]) */
+  const int32_t *row_ptr;      /* [n_cells+1] */
+  const int32_t *col_idx;      /* [nnzb] */
+  const double *vals;          /* [4*nnzb] */
+  int32_t block_order;         /* 0 row-major, 1 column-major */
+  int32_t var_order;           /* 0 (p_w, S_n), 1 (S_n, p_w) */
+  int32_t mem;                 /* 0: the three arrays are host pointers, 1: device pointers */
+  int32_t reserved;
+} bf_bsr2;
+
+typedef struct {
+  double theta;                /* strength threshold (R4), default 0.25 */
+  int32_t max_levels;          /* default 25 */
+  int32_t max_coarse;          /* coarsest level dense-LU size limit, default 64, max 128 */
+  int32_t smoother;            /* 0 l1-Jacobi (default), 1 Chebyshev (R5) */
+  int32_t nu_pre, nu_post;     /* smoothing passes, default 1, 1 */
+  int32_t cheb_degree;         /* Chebyshev degree, default 2 */
+  double cheb_lo;              /* Chebyshev interval [cheb_lo, 1] on D_l1^-1 A, default 0.3 */
+  uint64_t seed;               /* PMIS hash seed, default 0x1611 */
+  int32_t orth;                /* 0 CGS2 (default), 1 CGS1 */
+  int32_t schur_as_printed;    /* 0: A_sp (default, R1); 1: literal P:L239 (A_pp), diagnostics only */
+  int32_t interp_norm;         /* 1: interpolation weights normalised so P 1 = 1 (default, R8); 0: Q26 denominators */
+  int32_t timing;              /* 1: record CUDA events around the J SpMV and the GMRES
+                                  orthogonalisation kernels (bf_kernel_time) */
+} bf_options;
+
+typedef struct bf_ctx *bf_handle;
+
+/* Fill *opt with the defaults listed above. */
+bf_status bf_default_options(bf_options *opt);
+
+/* Validate and ingest J, build the field split, S~ and
+ * the two AMG hierarchies (A_ss and S~; PMIS + classical interpolation + Galerkin,
+ * P:L145, L275).  opt may be NULL (defaults).  On success *out is a new handle; on
+ * error *out = NULL and all partial state is freed. */
+bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *cuda_stream, bf_handle *out);
+
+/* Restarted right-preconditioned GMRES(restart) on J x = rhs.
+ *   rhs, x: length 2*n_cells; vec_mem 0 = host pointers, 1 = device pointers.
+ *   x: in = x0, out = the last iterate.
+ *   tol: relative to ||rhs||_2 (P:L275 form); the Givens estimate drives the loop and
+ *        the true residual is recomputed at the end of every cycle (R11).
+ *   maxit: cap on Arnoldi steps summed over restarts.
+ *   *iters: Arnoldi steps taken.  res_hist (host, may be NULL, length >= maxit+1):
+ *        res_hist[0] = ||r0||/||rhs||, res_hist[k] = Givens estimate after step k.
+ *   *converged: 1 if the true relative residual <= tol.  *final_true_relres: that residual.
+ *   ||rhs|| == 0 gives x = 0, iters = 0, converged = 1. */
+bf_status bf_solve(bf_handle h, const double *rhs, double *x, double tol, int32_t restart,
+                   int32_t maxit, int32_t vec_mem, int32_t *iters, double *res_hist,
+                   int32_t *converged, double *final_true_relres, void *cuda_stream);
+
+/* Free all device memory of the handle (NULL is a no-op). */
+bf_status bf_destroy(bf_handle h);
+
+/* Last error message of the handle; NULL: the calling thread's last bf_setup error. */
+const char *bf_last_error(bf_handle h);
+
+/* ---- introspection (parity tests, statistics) ---------------------------------- */
+/* y = J x (P:L138-140 operator), vectors as in bf_solve. */
+bf_status bf_spmv(bf_handle h, const double *x, double *y, int32_t vec_mem, void *cuda_stream);
+/* z = M_bf^-1 r: one application of Algorithm 3. */
+bf_status bf_apply_precond(bf_handle h, const double *r, double *z, int32_t vec_mem, void *cuda_stream);
+/* x = one V-cycle of hierarchy `which` (0 A_ss, 1 S~) applied to b (length n_cells). */
+bf_status bf_vcycle(bf_handle h, int32_t which, const double *b, double *x, int32_t vec_mem,
+                    void *cuda_stream);
+bf_status bf_num_levels(bf_handle h, int32_t which, int32_t *nlev);
+/* Level sizes; then (optionally, host buffers of the reported sizes, any may be NULL)
+ * A_l (CSR, int32 row_ptr[n+1]), cf[n] (1 = C, 0 = F; level < nlev-1), P_l (n x n_{l+1}),
+ * the l1 diagonal dl1[n]. */
+bf_status bf_get_level(bf_handle h, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
+                       int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val,
+                       int8_t *cf, int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1);
+/* which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~.  Sizes first; arrays optional (host). */
+bf_status bf_get_block(bf_handle h, int32_t which, int64_t *nnz, int32_t *rowptr, int32_t *col,
+                       double *val);
+/* Accumulated device time (ms, CUDA events on the solve stream), number of timed
+ * regions and ALGORITHMIC bytes moved (each operand once per use)
+ * of an instrumented kernel class since setup (requires opt.timing = 1):
+ *   0 J SpMV (36 nnzb + 36 n bytes per launch), 1 GMRES orthogonalisation passes,
+ *   2 whole BF apply, 3 whole bf_solve.  Any output pointer may be NULL. */
+bf_status bf_kernel_time(bf_handle h, int32_t kclass, double *ms, int64_t *launches, double *alg_bytes);
+/* Number of kernels this library launched since the handle was created. */
+bf_status bf_launch_count(bf_handle h, int64_t *launches);
+/* Device bytes currently held by the handle. */
+bf_status bf_device_bytes(bf_handle h, int64_t *bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,287 @@
+"""Thin ctypes binding of libbf.so (include/bf.h).  Argument marshalling only: every
+step of the BF-AMG-GMRES path runs in the library's CUDA kernels.  There is no CPU
+fallback: if libbf.so is missing, importing this module raises; if no CUDA device is
+present, the library calls return BF_ERR_CUDA and these wrappers raise BFError.
+
+Arrays may be torch tensors (CUDA tensors are passed as device pointers, CPU tensors
+as host pointers) or numpy arrays (host pointers).  PyTorch is used only for device
+memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbf.so")
+
+BF_OK = 0
+STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE", 4: "BF_ERR_ZERO_DIAG",
+          5: "BF_ERR_COARSE_SINGULAR", 6: "BF_ERR_CUDA", 7: "BF_ERR_OOM", 8: "BF_ERR_LIMIT"}
+
+# every symbol declared in include/bf.h
+EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_destroy", "bf_last_error", "bf_spmv",
+           "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_block",
+           "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
+
+
+class BFError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class bf_bsr2(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("n_cells", C.c_int32),
+                ("nnzb", C.c_int64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("vals", C.c_void_p),
+                ("block_order", C.c_int32), ("var_order", C.c_int32), ("mem", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class bf_options(C.Structure):
+    _fields_ = [("theta", C.c_double), ("max_levels", C.c_int32), ("max_coarse", C.c_int32),
+                ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
+                ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
+                ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
+                ("timing", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1611_00127_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp, i32, i64, dp = C.c_void_p, C.c_int32, C.c_int64, P(C.c_double)
+    L.bf_default_options.argtypes = [P(bf_options)]
+    L.bf_setup.argtypes = [P(bf_bsr2), P(bf_options), vp, P(vp)]
+    L.bf_solve.argtypes = [vp, vp, vp, C.c_double, i32, i32, i32, P(i32), dp, P(i32), dp, vp]
+    L.bf_destroy.argtypes = [vp]
+    L.bf_last_error.argtypes = [vp]
+    L.bf_last_error.restype = C.c_char_p
+    L.bf_spmv.argtypes = [vp, vp, vp, i32, vp]
+    L.bf_apply_precond.argtypes = [vp, vp, vp, i32, vp]
+    L.bf_vcycle.argtypes = [vp, i32, vp, vp, i32, vp]
+    L.bf_num_levels.argtypes = [vp, i32, P(i32)]
+    L.bf_get_level.argtypes = [vp, i32, i32, P(i32), P(i64), P(i64), vp, vp, vp, vp, vp, vp, vp, vp]
+    L.bf_get_block.argtypes = [vp, i32, P(i64), vp, vp, vp]
+    L.bf_kernel_time.argtypes = [vp, i32, dp, P(i64), dp]
+    L.bf_launch_count.argtypes = [vp, P(i64)]
+    L.bf_device_bytes.argtypes = [vp, P(i64)]
+    for name in EXPORTS:
+        L[name].restype = L[name].restype if name == "bf_last_error" else C.c_int
+    L.bf_last_error.restype = C.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def _check(st, h=None):
+    if st != BF_OK:
+        raise BFError(st, lib.bf_last_error(h).decode(errors="replace"))
+
+
+def _ptr(a):
+    """(pointer, mem) of a torch tensor or numpy array: mem 1 = device, 0 = host."""
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(a.data_ptr()), (1 if a.is_cuda else 0)
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return C.c_void_p(a.ctypes.data), 0
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _stream(stream):
+    if stream is not None:
+        return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:
+        pass
+    return C.c_void_p(0)
+
+
+def bf_default_options(**kw) -> bf_options:
+    o = bf_options()
+    _check(lib.bf_default_options(C.byref(o)))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise AttributeError(k)
+        setattr(o, k, v)
+    return o
+
+
+def bf_setup(row_ptr, col_idx, vals, dims, block_order=0, var_order=0, opt=None, stream=None):
+    """row_ptr int32[n+1], col_idx int32[nnzb], vals f64[nnzb*4] (all host or all device)."""
+    (rp, m0), (ci, m1), (v, m2) = _ptr(row_ptr), _ptr(col_idx), _ptr(vals)
+    if len({m0, m1, m2}) != 1:
+        raise ValueError("row_ptr, col_idx and vals must all be host or all be device arrays")
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    nnzb = int(col_idx.shape[0])
+    J = bf_bsr2(nx, ny, nz, n, nnzb, rp, ci, v, block_order, var_order, m0, 0)
+    h = C.c_void_p()
+    st = lib.bf_setup(C.byref(J), C.byref(opt) if opt is not None else None, _stream(stream), C.byref(h))
+    _check(st, None)
+    return h
+
+
+def bf_destroy(h):
+    lib.bf_destroy(h)
+
+
+def bf_last_error(h=None) -> str:
+    return lib.bf_last_error(h).decode(errors="replace")
+
+
+def bf_solve(h, rhs, x, tol=1e-8, restart=30, maxit=500, res_hist=True, stream=None):
+    (b, mb), (xp, mx) = _ptr(rhs), _ptr(x)
+    if mb != mx:
+        raise ValueError("rhs and x must both be host or both be device arrays")
+    iters, conv = C.c_int32(), C.c_int32()
+    rel = C.c_double()
+    hist = np.zeros(maxit + 1) if res_hist else None
+    st = lib.bf_solve(h, b, xp, tol, restart, maxit, mb, C.byref(iters),
+                      hist.ctypes.data_as(C.POINTER(C.c_double)) if hist is not None else None,
+                      C.byref(conv), C.byref(rel), _stream(stream))
+    _check(st, h)
+    out = dict(iters=iters.value, converged=bool(conv.value), relres=rel.value)
+    if hist is not None:
+        out["hist"] = hist[:iters.value + 1]
+    return out
+
+
+def bf_spmv(h, x, y, stream=None):
+    (xp, mx), (yp, my) = _ptr(x), _ptr(y)
+    assert mx == my
+    _check(lib.bf_spmv(h, xp, yp, mx, _stream(stream)), h)
+
+
+def bf_apply_precond(h, r, z, stream=None):
+    (rp, mr), (zp, mz) = _ptr(r), _ptr(z)
+    assert mr == mz
+    _check(lib.bf_apply_precond(h, rp, zp, mr, _stream(stream)), h)
+
+
+def bf_vcycle(h, which, b, x, stream=None):
+    (bp, mb), (xp, mx) = _ptr(b), _ptr(x)
+    assert mb == mx
+    _check(lib.bf_vcycle(h, which, bp, xp, mb, _stream(stream)), h)
+
+
+def bf_num_levels(h, which) -> int:
+    n = C.c_int32()
+    _check(lib.bf_num_levels(h, which, C.byref(n)), h)
+    return n.value
+
+
+def bf_get_level(h, which, level):
+    """Copy level `level` of hierarchy `which` (0 A_ss, 1 S~) to host numpy arrays."""
+    n, nA, nP = C.c_int32(), C.c_int64(), C.c_int64()
+    _check(lib.bf_get_level(h, which, level, C.byref(n), C.byref(nA), C.byref(nP), *([None] * 8)), h)
+    n, nA, nP = n.value, nA.value, nP.value
+    Arp = np.empty(n + 1, np.int32)
+    Aci = np.empty(nA, np.int32)
+    Av = np.empty(nA)
+    cf = np.empty(n, np.int8)
+    dl1 = np.empty(n)
+    coarsest = level == bf_num_levels(h, which) - 1
+    Prp = np.empty(n + 1, np.int32)
+    Pci = np.empty(max(nP, 1), np.int32)
+    Pv = np.empty(max(nP, 1))
+    p = lambda a: C.c_void_p(a.ctypes.data)
+    _check(lib.bf_get_level(h, which, level, None, None, None, p(Arp), p(Aci), p(Av),
+                            None if coarsest else p(cf), None if coarsest else p(Prp),
+                            None if coarsest else p(Pci), None if coarsest else p(Pv), p(dl1)), h)
+    out = dict(n=n, A=(Arp, Aci, Av), dl1=dl1)
+    if not coarsest:
+        out.update(cf=cf, P=(Prp, Pci[:nP], Pv[:nP]))
+    return out
+
+
+def bf_get_block(h, which):
+    """which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~ -> (row_ptr, col, val) host arrays."""
+    nnz = C.c_int64()
+    _check(lib.bf_get_block(h, which, C.byref(nnz), None, None, None), h)
+    # rows = n_cells: recover from level 0 size of hierarchy 0
+    n = bf_get_level_size(h)
+    rp = np.empty(n + 1, np.int32)
+    ci = np.empty(max(nnz.value, 1), np.int32)
+    v = np.empty(max(nnz.value, 1))
+    p = lambda a: C.c_void_p(a.ctypes.data)
+    _check(lib.bf_get_block(h, which, None, p(rp), p(ci), p(v)), h)
+    return rp, ci[:nnz.value], v[:nnz.value]
+
+
+def bf_get_level_size(h, which=0, level=0) -> int:
+    n = C.c_int32()
+    _check(lib.bf_get_level(h, which, level, C.byref(n), None, None, *([None] * 8)), h)
+    return n.value
+
+
+def bf_kernel_time(h, kclass):
+    """-> (ms, timed regions, algorithmic bytes) of kernel class kclass (needs timing=1)."""
+    ms, cnt, by = C.c_double(), C.c_int64(), C.c_double()
+    _check(lib.bf_kernel_time(h, kclass, C.byref(ms), C.byref(cnt), C.byref(by)), h)
+    return ms.value, cnt.value, by.value
+
+
+def bf_launch_count(h) -> int:
+    n = C.c_int64()
+    _check(lib.bf_launch_count(h, C.byref(n)), h)
+    return n.value
+
+
+def bf_device_bytes(h) -> int:
+    n = C.c_int64()
+    _check(lib.bf_device_bytes(h, C.byref(n)), h)
+    return n.value
+
+
+class BFSolver:
+    """Owning wrapper: setup on construction, bf_destroy on close()/garbage collection."""
+
+    def __init__(self, row_ptr, col_idx, vals, dims, block_order=0, var_order=0, stream=None, **opts):
+        self.opt = bf_default_options(**opts)
+        self.h = bf_setup(row_ptr, col_idx, vals, dims, block_order, var_order, self.opt, stream)
+        self.n = dims[0] * dims[1] * dims[2]
+
+    def solve(self, rhs, x, tol=1e-8, restart=30, maxit=500, stream=None):
+        return bf_solve(self.h, rhs, x, tol, restart, maxit, True, stream)
+
+    def spmv(self, x, y, stream=None):
+        bf_spmv(self.h, x, y, stream)
+
+    def apply_precond(self, r, z, stream=None):
+        bf_apply_precond(self.h, r, z, stream)
+
+    def vcycle(self, which, b, x, stream=None):
+        bf_vcycle(self.h, which, b, x, stream)
+
+    def num_levels(self, which):
+        return bf_num_levels(self.h, which)
+
+    def level(self, which, l):
+        return bf_get_level(self.h, which, l)
+
+    def block(self, which):
+        return bf_get_block(self.h, which)
+
+    def close(self):
+        if getattr(self, "h", None):
+            bf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

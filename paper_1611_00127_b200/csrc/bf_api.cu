@@ -1,0 +1,352 @@
+// bf_api.cu -- the C-ABI entry points of libbf.so (include/bf.h), handle and memory
+// management, error translation.  No exception crosses the ABI.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "bf_internal.cuh"
+
+static thread_local std::string g_setup_err;
+
+namespace bf {
+
+void cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    (void)cudaGetLastError();
+    throw Error(BF_ERR_OOM, std::string("device allocation failed: ") + what);
+  }
+  throw Error(BF_ERR_CUDA, std::string(cudaGetErrorString(e)) + " at " + what);
+}
+
+void *dalloc(bf_ctx *c, size_t bytes) {
+  void *p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw Error(BF_ERR_OOM, "cudaMallocAsync of " + std::to_string(bytes) + " bytes failed (" +
+                                cudaGetErrorString(e) + ")");
+  }
+  c->allocs.emplace_back(p, bytes);
+  c->dev_bytes += (int64_t)bytes;
+  return p;
+}
+
+void dfree(bf_ctx *c, void *p) {
+  if (!p) return;
+  for (size_t i = 0; i < c->allocs.size(); i++) {
+    if (c->allocs[i].first == p) {
+      c->dev_bytes -= (int64_t)c->allocs[i].second;
+      c->allocs[i] = c->allocs.back();
+      c->allocs.pop_back();
+      cudaFreeAsync(p, c->stream);
+      return;
+    }
+  }
+}
+
+void free_csr(bf_ctx *c, DCsr &A) {
+  dfree(c, A.rp);
+  dfree(c, A.ci);
+  dfree(c, A.v);
+  A = DCsr();
+}
+
+void timer_begin(bf_ctx *c, int k, cudaEvent_t *start) {
+  *start = nullptr;
+  if (!c->opt.timing) return;
+  BF_CUDA(cudaEventCreate(start));
+  BF_CUDA(cudaEventRecord(*start, c->stream));
+}
+
+void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes) {
+  if (!c->opt.timing || !start) return;
+  c->timers[k].bytes += alg_bytes;
+  cudaEvent_t stop;
+  BF_CUDA(cudaEventCreate(&stop));
+  BF_CUDA(cudaEventRecord(stop, c->stream));
+  c->timers[k].pending.push_back(start);
+  c->timers[k].pending.push_back(stop);
+  c->timers[k].launches++;
+}
+
+void timer_flush(bf_ctx *c) {
+  for (auto &t : c->timers) {
+    for (size_t i = 0; i + 1 < t.pending.size(); i += 2) {
+      BF_CUDA(cudaEventSynchronize(t.pending[i + 1]));
+      float ms = 0.f;
+      BF_CUDA(cudaEventElapsedTime(&ms, t.pending[i], t.pending[i + 1]));
+      t.ms += ms;
+      cudaEventDestroy(t.pending[i]);
+      cudaEventDestroy(t.pending[i + 1]);
+    }
+    t.pending.clear();
+  }
+}
+
+}  // namespace bf
+
+using namespace bf;
+
+static void destroy_ctx(bf_ctx *c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto &t : c->timers)
+    for (auto e : t.pending) cudaEventDestroy(e);
+  for (auto &a : c->allocs) cudaFreeAsync(a.first, c->stream);
+  c->allocs.clear();
+  if (c->hpin) cudaFreeHost(c->hpin);
+  cudaStreamSynchronize(c->stream);
+  delete c;
+}
+
+#define BF_GUARD_BEGIN try {
+#define BF_GUARD_END(ctx)                                           \
+  }                                                                 \
+  catch (const Error &e) {                                          \
+    if (ctx) (ctx)->err = e.msg;                                    \
+    return e.st;                                                    \
+  }                                                                 \
+  catch (const std::exception &e) {                                 \
+    if (ctx) (ctx)->err = std::string("internal error: ") + e.what(); \
+    return BF_ERR_CUDA;                                             \
+  }
+
+extern "C" {
+
+bf_status bf_default_options(bf_options *o) {
+  if (!o) return BF_ERR_ARG;
+  memset(o, 0, sizeof *o);
+  o->theta = 0.25;
+  o->max_levels = 25;
+  o->max_coarse = 64;
+  o->smoother = 0;
+  o->nu_pre = 1;
+  o->nu_post = 1;
+  o->cheb_degree = 2;
+  o->cheb_lo = 0.3;
+  o->seed = 0x1611ULL;
+  o->orth = 0;
+  o->schur_as_printed = 0;
+  o->interp_norm = 1;
+  o->timing = 0;
+  return BF_OK;
+}
+
+static const char *check_options(const bf_options *o) {
+  if (!(o->theta > 0.0 && o->theta <= 1.0)) return "theta must be in (0, 1]";
+  if (o->max_levels < 1 || o->max_levels > BF_MAXL) return "max_levels must be in [1, 64]";
+  if (o->max_coarse < 1 || o->max_coarse > 128) return "max_coarse must be in [1, 128]";
+  if (o->smoother != 0 && o->smoother != 1) return "smoother must be 0 or 1";
+  if (o->nu_pre < 0 || o->nu_post < 0 || o->nu_pre > 8 || o->nu_post > 8) return "nu_pre/nu_post in [0, 8]";
+  if (o->smoother == 1 && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
+  if (o->smoother == 1 && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
+  if (o->orth != 0 && o->orth != 1) return "orth must be 0 or 1";
+  return nullptr;
+}
+
+bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_handle *out) {
+  if (out) *out = nullptr;
+  g_setup_err.clear();
+  if (!J || !out) {
+    g_setup_err = "bf_setup: J and out must be non-NULL";
+    return BF_ERR_ARG;
+  }
+  bf_ctx *c = new bf_ctx();
+  c->stream = (cudaStream_t)stream;
+  if (opt) c->opt = *opt;
+  else bf_default_options(&c->opt);
+  if (const char *m = check_options(&c->opt)) {
+    g_setup_err = std::string("bf_setup: ") + m;
+    delete c;
+    return BF_ERR_ARG;
+  }
+  try {
+    int dev = 0;
+    BF_CUDA(cudaGetDevice(&dev));
+    BF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    validate_and_ingest(c, J);
+    build_split(c);
+    build_schur(c);
+    build_hierarchy(c, 0, c->blk[3]);
+    build_hierarchy(c, 1, c->blk[4]);
+    alloc_solve_workspace(c, 30);
+    BF_CUDA(cudaStreamSynchronize(c->stream));
+  } catch (const Error &e) {
+    g_setup_err = e.msg;
+    bf_status st = e.st;
+    destroy_ctx(c);
+    return st;
+  } catch (const std::exception &e) {
+    g_setup_err = std::string("internal error: ") + e.what();
+    destroy_ctx(c);
+    return BF_ERR_CUDA;
+  }
+  *out = c;
+  return BF_OK;
+}
+
+bf_status bf_destroy(bf_handle h) {
+  destroy_ctx(h);
+  return BF_OK;
+}
+
+const char *bf_last_error(bf_handle h) { return h ? h->err.c_str() : g_setup_err.c_str(); }
+
+// copy a 2n vector in or out; returns a device pointer (the handle's buffer when host)
+static const double *vec_in(bf_ctx *c, const double *p, int mem, double *tmp) {
+  if (mem == 1) return p;
+  BF_CUDA(cudaMemcpyAsync(tmp, p, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+  return tmp;
+}
+
+bf_status bf_solve(bf_handle c, const double *rhs, double *x, double tol, int32_t restart,
+                   int32_t maxit, int32_t vec_mem, int32_t *iters, double *res_hist,
+                   int32_t *converged, double *relres, void *stream) {
+  if (!c) return BF_ERR_ARG;
+  if (!rhs || !x || !iters || !converged || !relres || restart < 1 || restart > 512 || maxit < 0 ||
+      !(tol >= 0.0) || (vec_mem != 0 && vec_mem != 1)) {
+    c->err = "bf_solve: bad argument (rhs/x/iters/converged/relres non-NULL, 1 <= restart <= 512, maxit >= 0, tol >= 0, vec_mem 0|1)";
+    return BF_ERR_ARG;
+  }
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  c->err.clear();
+  cudaEvent_t t0;
+  timer_begin(c, 3, &t0);
+  alloc_solve_workspace(c, restart);
+  const double *b = vec_in(c, rhs, vec_mem, c->bd);
+  double *xd = x;
+  if (vec_mem == 0) {
+    BF_CUDA(cudaMemcpyAsync(c->xd, x, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+    xd = c->xd;
+  }
+  gmres(c, b, xd, tol, restart, maxit, iters, res_hist, converged, relres);
+  if (vec_mem == 0)
+    BF_CUDA(cudaMemcpyAsync(x, c->xd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  timer_end(c, 3, t0);
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  timer_flush(c);
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_spmv(bf_handle c, const double *x, double *y, int32_t vec_mem, void *stream) {
+  if (!c || !x || !y || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  const double *xd = vec_in(c, x, vec_mem, c->bd);
+  double *yd = vec_mem ? y : c->xd;
+  cudaEvent_t t0;
+  timer_begin(c, 0, &t0);
+  bsr_spmv(c, xd, yd);
+  timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
+  if (!vec_mem)
+    BF_CUDA(cudaMemcpyAsync(y, yd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  timer_flush(c);
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_apply_precond(bf_handle c, const double *r, double *z, int32_t vec_mem, void *stream) {
+  if (!c || !r || !z || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  const double *rd = vec_in(c, r, vec_mem, c->bd);
+  double *zd = vec_mem ? z : c->xd;
+  cudaEvent_t t0;
+  timer_begin(c, 2, &t0);
+  bf_apply(c, rd, zd);
+  timer_end(c, 2, t0);
+  if (!vec_mem)
+    BF_CUDA(cudaMemcpyAsync(z, zd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  timer_flush(c);
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int32_t vec_mem, void *stream) {
+  if (!c || !b || !x || which < 0 || which > 1 || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  size_t bytes = sizeof(double) * (size_t)c->n;
+  const double *bd = b;
+  double *xd = x;
+  if (!vec_mem) {
+    BF_CUDA(cudaMemcpyAsync(c->bd, b, bytes, cudaMemcpyHostToDevice, c->stream));
+    bd = c->bd;
+    xd = c->xd;
+  }
+  vcycle(c, which, bd, xd);
+  if (!vec_mem) BF_CUDA(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_num_levels(bf_handle c, int32_t which, int32_t *nlev) {
+  if (!c || !nlev || which < 0 || which > 1) return BF_ERR_ARG;
+  *nlev = c->h[which].nlev;
+  return BF_OK;
+}
+
+static void copy_csr_out(bf_ctx *c, const DCsr &A, int32_t *rp, int32_t *ci, double *v) {
+  if (rp) BF_CUDA(cudaMemcpyAsync(rp, A.rp, sizeof(int32_t) * (A.n + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (ci && A.nnz) BF_CUDA(cudaMemcpyAsync(ci, A.ci, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToHost, c->stream));
+  if (v && A.nnz) BF_CUDA(cudaMemcpyAsync(v, A.v, sizeof(double) * A.nnz, cudaMemcpyDeviceToHost, c->stream));
+}
+
+bf_status bf_get_level(bf_handle c, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
+                       int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val, int8_t *cf,
+                       int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1) {
+  if (!c || which < 0 || which > 1 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  const Level &L = c->h[which].lv[level];
+  bool coarsest = level == c->h[which].nlev - 1;
+  if (n) *n = L.A.n;
+  if (nnz_A) *nnz_A = L.A.nnz;
+  if (nnz_P) *nnz_P = coarsest ? 0 : L.P.nnz;
+  copy_csr_out(c, L.A, A_rowptr, A_col, A_val);
+  if (!coarsest) {
+    if (cf) BF_CUDA(cudaMemcpyAsync(cf, L.cf, L.A.n, cudaMemcpyDeviceToHost, c->stream));
+    copy_csr_out(c, L.P, P_rowptr, P_col, P_val);
+  }
+  if (dl1) BF_CUDA(cudaMemcpyAsync(dl1, L.dl1, sizeof(double) * L.A.n, cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_get_block(bf_handle c, int32_t which, int64_t *nnz, int32_t *rowptr, int32_t *col, double *val) {
+  if (!c || which < 0 || which > 4) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  if (nnz) *nnz = c->blk[which].nnz;
+  copy_csr_out(c, c->blk[which], rowptr, col, val);
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_kernel_time(bf_handle c, int32_t k, double *ms, int64_t *launches, double *alg_bytes) {
+  if (!c || k < 0 || k > 3) return BF_ERR_ARG;
+  if (ms) *ms = c->timers[k].ms;
+  if (launches) *launches = c->timers[k].launches;
+  if (alg_bytes) *alg_bytes = c->timers[k].bytes;
+  return BF_OK;
+}
+
+bf_status bf_launch_count(bf_handle c, int64_t *launches) {
+  if (!c || !launches) return BF_ERR_ARG;
+  *launches = c->launches;
+  return BF_OK;
+}
+
+bf_status bf_device_bytes(bf_handle c, int64_t *bytes) {
+  if (!c || !bytes) return BF_ERR_ARG;
+  *bytes = c->dev_bytes;
+  return BF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// bf_internal.cuh -- internal data structures of libbf.so (not part of the ABI).
+//
+// Device data layout (HBM, fp64 values, int32 indices):
+//   J        : canonical point-interleaved 2x2 BSR, row_ptr[n+1], col[nnzb],
+//              vals as double2 pairs [nnzb][2] = {(a_pp,a_ps),(a_sp,a_ss)} (32 B / block)
+//   blocks   : A_pp, A_ps, A_sp, A_ss, S~ as scalar CSR (int32 rp/ci, f64 v)
+//   AMG      : per level A_l, P_l, R_l = P_l^T (CSR), cf[n_l] (int8), dl1[n_l] (f64),
+//              work vectors b_l, x_l, r_l, t_l (f64[n_l]); coarsest: dense LU (smem-staged)
+//   GMRES    : V (restart+1) x N (column-contiguous), w, z, r, x (f64[N]), N = 2 n
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bf.h"
+
+#define BF_MAXL 64
+
+namespace bf {
+
+struct DCsr {
+  int32_t n = 0, m = 0;  // rows, cols
+  int64_t nnz = 0;
+  int32_t *rp = nullptr, *ci = nullptr;
+  double *v = nullptr;
+};
+
+struct Level {
+  DCsr A, P, R;
+  int8_t *cf = nullptr;
+  double *dl1 = nullptr;
+  double *b = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
+  double *d = nullptr;  // 1 / dl1 (smoother scaling)
+};
+
+struct Hier {
+  int nlev = 0;
+  Level lv[BF_MAXL];
+  double *lu = nullptr;  // nL x nL row-major LU (unit lower L below the diagonal)
+  int32_t *piv = nullptr;
+  int32_t nL = 0;
+  bool dense = false;  // coarsest level solved by LU (else 4 l1-Jacobi sweeps)
+};
+
+struct Timer {
+  double ms = 0.0;
+  int64_t launches = 0;
+  double bytes = 0.0;
+  std::vector<cudaEvent_t> pending;  // pairs (start, stop)
+};
+
+class Error {
+ public:
+  bf_status st;
+  std::string msg;
+  Error(bf_status s, std::string m) : st(s), msg(std::move(m)) {}
+};
+
+}  // namespace bf
+
+struct bf_ctx {
+  bf_options opt{};
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int32_t n = 0;  // cells
+  int64_t nnzb = 0;
+  int32_t var_order = 0;
+  int32_t *brp = nullptr, *bci = nullptr;
+  double *bv = nullptr;  // canonical (p,s) row-major blocks
+  bf::DCsr blk[5];       // A_pp, A_ps, A_sp, A_ss, S~
+  double *dss = nullptr;
+  bf::Hier h[2];
+  // solve workspace
+  int32_t Vm = 0;
+  double *V = nullptr, *w = nullptr, *z = nullptr, *r = nullptr, *xd = nullptr, *bd = nullptr;
+  double *vp = nullptr, *vs = nullptr, *sv = nullptr, *pv = nullptr;  // BF apply split vectors
+  double *red = nullptr;        // reduction partials
+  double *hdev = nullptr;       // reduced coefficients (device)
+  double *hpin = nullptr;       // pinned host mirror
+  unsigned int *counter = nullptr;
+  int red_blocks = 0;
+  // bookkeeping
+  std::vector<std::pair<void *, size_t>> allocs;
+  int64_t dev_bytes = 0;
+  int64_t launches = 0;
+  bf::Timer timers[4];
+  int num_sms = 148;
+};
+
+namespace bf {
+
+// ---- error / allocation helpers (bf_api.cu) --------------------------------------
+void cuda_check(cudaError_t e, const char *what);
+void *dalloc(bf_ctx *c, size_t bytes);
+void dfree(bf_ctx *c, void *p);
+template <class T>
+T *dalloc_t(bf_ctx *c, size_t count) {
+  return static_cast<T *>(dalloc(c, count * sizeof(T) + 16));
+}
+void free_csr(bf_ctx *c, DCsr &A);
+void timer_begin(bf_ctx *c, int k, cudaEvent_t *start);
+void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes = 0.0);
+void timer_flush(bf_ctx *c);
+
+#define BF_CUDA(x) ::bf::cuda_check((x), #x)
+#define BF_LAUNCH(c) ((c)->launches++)
+
+// ---- scans (k_util.cu) ------------------------------------------------------------
+// exclusive prefix sum of int32 counts[0..n) into out[0..n], returns out[n] (host sync)
+int64_t exclusive_scan_i32(bf_ctx *c, const int32_t *counts, int32_t *out, int32_t n);
+int64_t exclusive_scan_i64(bf_ctx *c, const int64_t *counts, int64_t *out, int64_t n);
+void sort_pairs_u64_f64(bf_ctx *c, uint64_t *keys, double *vals, int64_t count, int end_bit);
+
+// ---- setup kernels -----------------------------------------------------------------
+void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J);                 // k_split.cu
+void build_split(bf_ctx *c);                                            // k_split.cu
+void build_schur(bf_ctx *c);                                            // k_split.cu
+void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
+void free_hierarchy(bf_ctx *c, Hier &h);
+
+// ---- solve kernels -------------------------------------------------------------
+void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu
+void csr_spmv(bf_ctx *c, const DCsr &A, const double *x, double *y);    // k_spmv.cu
+void vcycle(bf_ctx *c, int which, const double *b, double *x);          // k_vcycle.cu
+void bf_apply(bf_ctx *c, const double *v, double *z);                   // k_vcycle.cu
+void alloc_solve_workspace(bf_ctx *c, int restart);                     // k_gmres.cu
+void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
+           int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace bf

@@ -1,0 +1,362 @@
+// k_gmres.cu -- restarted right-preconditioned GMRES(m) (`precon-system`, P:L138-140;
+// tolerance form P:L275; readings R10-R12) with classical Gram-Schmidt run twice (CGS2)
+// fused into batched dot / axpy passes over the Krylov basis:
+//   pass 1  h  = V_j^T w                              (reads j+1 basis vectors + w)
+//   pass 2  w' = w - V_j h ;  h2 = V_j^T w'           (one read of V_j: axpy and dots fused)
+//   pass 3  v  = w' - V_j h2 ; ||v||^2                (writes v_{j+1} unnormalised)
+// Each pass ends in a deterministic two-level reduction (per-CTA partials, the last CTA to
+// finish sums them in CTA order), so results are reproducible run to run.  One small
+// device->host copy per Arnoldi step feeds the host-side Givens rotations (tiny, O(m)).
+//
+// Roofline: HBM-bound; algorithmic bytes per Arnoldi step with j+1 basis vectors of N f64:
+//   pass 1: 8N (j+2), pass 2: 8N (j+3), pass 3: 8N (j+3)  (+ 16N for the scaling of v_{j+1}).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "bf_internal.cuh"
+
+namespace bf {
+
+constexpr int RED_THREADS = 256;
+constexpr int MAXNV = 32;  // max basis vectors per pass -> restart <= 32
+
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double *partial, double *out, int nout,
+                                                   unsigned int *counter) {
+  __shared__ double sm[RED_THREADS / 32][NV];
+  __shared__ bool last;
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; i++) {
+    double v = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sm[warp][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+    for (int w = 0; w < RED_THREADS / 32; w++) s += sm[w][threadIdx.x];
+    partial[(size_t)blockIdx.x * MAXNV + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicInc(counter, gridDim.x - 1) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < nout) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; b++) s += __ldcg(partial + (size_t)b * MAXNV + threadIdx.x);
+    out[threadIdx.x] = s;
+  }
+}
+
+// pass 1: out[i] = V_i . w, i < NV
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS) k_dots(int64_t N, const double *__restrict__ V,
+                                                      const double *__restrict__ w, double *partial,
+                                                      double *out, unsigned int *counter) {
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) acc[i] = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double wt = __ldcs(w + t);
+#pragma unroll
+    for (int i = 0; i < NV; i++) acc[i] += __ldcs(V + (size_t)i * N + t) * wt;
+  }
+  block_reduce_store<NV>(acc, partial, out, NV, counter);
+}
+
+// pass 2: w <- w - sum_i h_i V_i ; out[i] = V_i . w (new w)
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS) k_axpy_dots(int64_t N, const double *__restrict__ V, double *w,
+                                                           const double *__restrict__ h, double *partial,
+                                                           double *out, unsigned int *counter) {
+  __shared__ double hs[NV];
+  if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) acc[i] = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double v[NV];
+    double wt = w[t];
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+      v[i] = __ldcs(V + (size_t)i * N + t);
+      wt -= hs[i] * v[i];
+    }
+    w[t] = wt;
+#pragma unroll
+    for (int i = 0; i < NV; i++) acc[i] += v[i] * wt;
+  }
+  block_reduce_store<NV>(acc, partial, out, NV, counter);
+}
+
+// pass 3: y = w - sum_i h_i V_i written to `y` (may be the next basis slot); out[0] = ||y||^2
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS) k_axpy_norm(int64_t N, const double *__restrict__ V,
+                                                           const double *__restrict__ w,
+                                                           const double *__restrict__ h, double *__restrict__ y,
+                                                           double *partial, double *out, unsigned int *counter) {
+  __shared__ double hs[NV];
+  if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double acc[1] = {0.0};
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double wt = __ldcs(w + t);
+#pragma unroll
+    for (int i = 0; i < NV; i++) wt -= hs[i] * __ldcs(V + (size_t)i * N + t);
+    y[t] = wt;
+    acc[0] += wt * wt;
+  }
+  block_reduce_store<1>(acc, partial, out, 1, counter);
+}
+
+// u = sum_i y_i V_i
+template <int NV>
+__global__ void k_lincomb(int64_t N, const double *__restrict__ V, const double *__restrict__ yv, double *u) {
+  __shared__ double ys[NV];
+  if (threadIdx.x < NV) ys[threadIdx.x] = yv[threadIdx.x];
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; i++) s += ys[i] * __ldcs(V + (size_t)i * N + t);
+    u[t] = s;
+  }
+}
+
+__global__ void k_scale(int64_t N, const double *__restrict__ a, const double *__restrict__ sptr, double s_host,
+                        double *y) {
+  double s = sptr ? 1.0 / sqrt(*sptr) : s_host;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = a[t] * s;
+}
+
+__global__ void k_sub(int64_t N, const double *__restrict__ a, const double *__restrict__ b, double *y) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = a[t] - b[t];
+}
+
+__global__ void k_add_inplace(int64_t N, double *x, const double *__restrict__ z) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    x[t] += z[t];
+}
+
+__global__ void k_zero_vec(int64_t N, double *x) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    x[t] = 0.0;
+}
+
+#define BF_NV_SWITCH(nv, CALL) \
+  switch (nv) {                \
+    BF_NV_C(1, CALL)           \
+    BF_NV_C(2, CALL)           \
+    BF_NV_C(3, CALL)           \
+    BF_NV_C(4, CALL)           \
+    BF_NV_C(5, CALL)           \
+    BF_NV_C(6, CALL)           \
+    BF_NV_C(7, CALL)           \
+    BF_NV_C(8, CALL)           \
+    BF_NV_C(9, CALL)           \
+    BF_NV_C(10, CALL)          \
+    BF_NV_C(11, CALL)          \
+    BF_NV_C(12, CALL)          \
+    BF_NV_C(13, CALL)          \
+    BF_NV_C(14, CALL)          \
+    BF_NV_C(15, CALL)          \
+    BF_NV_C(16, CALL)          \
+    BF_NV_C(17, CALL)          \
+    BF_NV_C(18, CALL)          \
+    BF_NV_C(19, CALL)          \
+    BF_NV_C(20, CALL)          \
+    BF_NV_C(21, CALL)          \
+    BF_NV_C(22, CALL)          \
+    BF_NV_C(23, CALL)          \
+    BF_NV_C(24, CALL)          \
+    BF_NV_C(25, CALL)          \
+    BF_NV_C(26, CALL)          \
+    BF_NV_C(27, CALL)          \
+    BF_NV_C(28, CALL)          \
+    BF_NV_C(29, CALL)          \
+    BF_NV_C(30, CALL)          \
+    BF_NV_C(31, CALL)          \
+    BF_NV_C(32, CALL)          \
+    default:                   \
+      throw Error(BF_ERR_LIMIT, "GMRES basis block larger than 32"); \
+  }
+#define BF_NV_C(k, CALL) \
+  case k: {              \
+    constexpr int NV = k; \
+    CALL;                \
+  } break;
+
+void alloc_solve_workspace(bf_ctx *c, int restart) {
+  if (restart > MAXNV) throw Error(BF_ERR_ARG, "restart must be <= 32 (fused CGS2 basis passes)");
+  int64_t N = 2 * (int64_t)c->n;
+  if (!c->w) {
+    c->w = dalloc_t<double>(c, N);
+    c->z = dalloc_t<double>(c, N);
+    c->r = dalloc_t<double>(c, N);
+    c->xd = dalloc_t<double>(c, N);
+    c->bd = dalloc_t<double>(c, N);
+    c->vp = dalloc_t<double>(c, c->n);
+    c->red_blocks = c->num_sms * 4;
+    c->red = dalloc_t<double>(c, (size_t)c->red_blocks * MAXNV);
+    c->hdev = dalloc_t<double>(c, 4 * MAXNV + 8);
+    c->counter = dalloc_t<unsigned int>(c, 4);
+    BF_CUDA(cudaMemsetAsync(c->counter, 0, 4 * sizeof(unsigned int), c->stream));
+    BF_CUDA(cudaMallocHost(&c->hpin, sizeof(double) * (4 * MAXNV + 8)));
+  }
+  if (c->Vm < restart + 1) {
+    dfree(c, c->V);
+    c->V = dalloc_t<double>(c, (size_t)(restart + 1) * N);
+    c->Vm = restart + 1;
+  }
+}
+
+static int grid_for(bf_ctx *c) { return c->red_blocks; }
+
+// out = a . b  (host value, synchronises)
+static double dot_host(bf_ctx *c, const double *a, const double *b) {
+  int64_t N = 2 * (int64_t)c->n;
+  k_dots<1><<<grid_for(c), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, c->hdev + 3 * MAXNV, c->counter);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  BF_CUDA(cudaMemcpyAsync(c->hpin, c->hdev + 3 * MAXNV, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return c->hpin[0];
+}
+
+void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, int *iters, double *hist,
+           int *converged, double *relres) {
+  int64_t N = 2 * (int64_t)c->n;
+  int G = grid_for(c);
+  double *V = c->V;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hcol(m + 1);
+  *iters = 0;
+  *converged = 0;
+  double bnorm = std::sqrt(dot_host(c, b, b));
+  if (bnorm == 0.0) {
+    k_zero_vec<<<G, 256, 0, c->stream>>>(N, x);
+    BF_LAUNCH(c);
+    if (hist) hist[0] = 0.0;
+    *converged = 1;
+    *relres = 0.0;
+    return;
+  }
+  // r = b - J x
+  bsr_spmv(c, x, c->w);
+  k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, c->r);
+  BF_LAUNCH(c);
+  double beta = std::sqrt(dot_host(c, c->r, c->r));
+  if (hist) hist[0] = beta / bnorm;
+  *relres = beta / bnorm;
+  if (beta <= tol * bnorm) {
+    *converged = 1;
+    return;
+  }
+  double *hd1 = c->hdev, *hd2 = c->hdev + MAXNV, *hdn = c->hdev + 2 * MAXNV;
+  for (;;) {
+    k_scale<<<G, 256, 0, c->stream>>>(N, c->r, nullptr, 1.0 / beta, V);
+    BF_LAUNCH(c);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    bool breakdown = false;
+    for (int j = 0; j < m; j++) {
+      const double *vj = V + (size_t)j * N;
+      double *vn = V + (size_t)(j + 1) * N;
+      bf_apply(c, vj, c->z);  // z = M^-1 v_j
+      cudaEvent_t t0;
+      timer_begin(c, 0, &t0);
+      bsr_spmv(c, c->z, c->w);  // w = J z
+      timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
+      int nv = j + 1;
+      timer_begin(c, 1, &t0);
+      BF_NV_SWITCH(nv, (k_dots<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1, c->counter)));
+      if (c->opt.orth == 0) {
+        BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, c->red, hd2,
+                                                                            c->counter)));
+        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd2, vn, c->red, hdn,
+                                                                            c->counter)));
+      } else {
+        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, vn, c->red, hdn,
+                                                                            c->counter)));
+      }
+      c->launches += c->opt.orth == 0 ? 3 : 2;
+      timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));
+      BF_CUDA(cudaGetLastError());
+      BF_CUDA(cudaMemcpyAsync(c->hpin, c->hdev, sizeof(double) * (2 * MAXNV + 1), cudaMemcpyDeviceToHost,
+                              c->stream));
+      BF_CUDA(cudaStreamSynchronize(c->stream));
+      double hn = std::sqrt(c->hpin[2 * MAXNV]);
+      for (int i = 0; i <= j; i++) hcol[i] = c->hpin[i] + (c->opt.orth == 0 ? c->hpin[MAXNV + i] : 0.0);
+      if (hn != 0.0) {
+        k_scale<<<G, 256, 0, c->stream>>>(N, vn, nullptr, 1.0 / hn, vn);
+        BF_LAUNCH(c);
+      } else {
+        breakdown = true;
+      }
+      for (int i = 0; i <= j; i++) H[(size_t)i * m + j] = hcol[i];
+      H[(size_t)(j + 1) * m + j] = hn;
+      for (int i = 0; i < j; i++) {  // previous Givens rotations
+        double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
+      double t = std::hypot(a, bb);
+      if (t == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = a / t;
+        sn[j] = bb / t;
+      }
+      H[(size_t)j * m + j] = cs[j] * a + sn[j] * bb;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      (*iters)++;
+      if (hist) hist[*iters] = std::fabs(g[j + 1]) / bnorm;
+      k = j + 1;
+      if (std::fabs(g[j + 1]) <= tol * bnorm || *iters >= maxit || breakdown) break;
+    }
+    // y = H^-1 g ; x += M^-1 (V y)
+    for (int i = k - 1; i >= 0; i--) {
+      double s = g[i];
+      for (int jj = i + 1; jj < k; jj++) s -= H[(size_t)i * m + jj] * y[jj];
+      y[i] = H[(size_t)i * m + i] != 0.0 ? s / H[(size_t)i * m + i] : 0.0;
+    }
+    for (int i = 0; i < k; i++) c->hpin[i] = y[i];
+    double *yd = c->hdev + 3 * MAXNV + 4;  // distinct from dot_host's slot
+    BF_CUDA(cudaMemcpyAsync(c->hdev + MAXNV, c->hpin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+    (void)yd;
+    BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, V, c->hdev + MAXNV, c->w)));
+    BF_LAUNCH(c);
+    bf_apply(c, c->w, c->z);
+    k_add_inplace<<<G, 256, 0, c->stream>>>(N, x, c->z);
+    BF_LAUNCH(c);
+    // true residual at the end of the cycle (R11)
+    bsr_spmv(c, x, c->w);
+    k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, c->r);
+    BF_LAUNCH(c);
+    beta = std::sqrt(dot_host(c, c->r, c->r));
+    *relres = beta / bnorm;
+    if (beta <= tol * bnorm) {
+      *converged = 1;
+      break;
+    }
+    if (*iters >= maxit) break;
+    if (beta == 0.0) {
+      *converged = 1;
+      break;
+    }
+  }
+}
+
+}  // namespace bf

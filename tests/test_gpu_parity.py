@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs (SURVEY.md c.6 bounds, BASELINE.json north_star tolerances)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle
+from workload import make_system, seeded_vector, BSR2
+from gpu_util import torch_dev, gpu_solver, csr_equal
+
+# (config, dims, gravity): several tiles and ragged tails; C1 both gravity variants
+CASES = [(1, None, True), (1, None, False), (1, (13, 7, 1), True), (2, (12, 11, 9), True),
+         (3, (20, 17, 15), True), (4, (40, 9, 16), True), (2, (33, 30, 31), True)]
+IDS = ["C1", "C1-g0", "C1-13x7", "C2-12x11x9", "C3-20x17x15", "C4-40x9x16", "C2-33x30x31"]
+
+
+@pytest.fixture(scope="module", params=list(range(len(CASES))), ids=IDS)
+def pair(request):
+    config, dims, grav = CASES[request.param]
+    prob, J, rhs = make_system(config, gravity=grav, dims=dims)
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    return prob, J, rhs, g, o
+
+
+def test_spmv(pair):
+    prob, J, rhs, g, o = pair
+    for seed in (1, 2):
+        x = seeded_vector(2 * J.n, seed)
+        yo = o.spmv(x)
+        y = torch.empty(2 * J.n, dtype=torch.float64, device="cuda")
+        g.spmv(torch_dev(x), y)
+        y = y.cpu().numpy()
+        assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+        absJx = np.abs(J.to_scipy()) @ np.abs(x)
+        assert np.max(np.abs(y - yo) / absJx) <= 1e-13
+
+
+def test_split_and_schur_bit_exact(pair):
+    prob, J, rhs, g, o = pair
+    for k, name in enumerate(("App", "Aps", "Asp", "Ass", "S")):
+        pat, val = csr_equal(g.block(k), o.matrix(name))
+        assert pat, f"{name} pattern differs"
+        assert val, f"{name} values differ"
+
+
+def test_hierarchy_bit_exact(pair):
+    prob, J, rhs, g, o = pair
+    for which in (0, 1):
+        nl = g.num_levels(which)
+        assert nl == o.nlev(which)
+        for l in range(nl):
+            G, O = g.level(which, l), o.level(which, l)
+            pat, val = csr_equal(G["A"], O["A"])
+            assert pat and val, f"A_{l} of hierarchy {which}: pattern {pat} values {val}"
+            assert np.array_equal(G["dl1"].view(np.uint64), O["dl1"].view(np.uint64))
+            if l < nl - 1:
+                assert np.array_equal(G["cf"], O["cf"]), f"C/F of level {l} hierarchy {which}"
+                pat, val = csr_equal(G["P"], O["P"])
+                assert pat and val, f"P_{l} of hierarchy {which}"
+
+
+def test_vcycle_and_bf_apply(pair):
+    prob, J, rhs, g, o = pair
+    n = J.n
+    for which in (0, 1):
+        b = seeded_vector(n, 10 + which)
+        xo = o.vcycle(which, b)
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.vcycle(which, torch_dev(b), x)
+        x = x.cpu().numpy()
+        assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+    v = seeded_vector(2 * n, 7)
+    zo = o.apply(v)
+    z = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(v), z)
+    z = z.cpu().numpy()
+    assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo)
+
+
+def test_gmres(pair):
+    prob, J, rhs, g, o = pair
+    ro = o.gmres(rhs, tol=1e-8, restart=30, maxit=500)
+    x = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=1e-8, restart=30, maxit=500)
+    xg = x.cpu().numpy()
+    assert r["converged"] == ro["converged"]
+    assert abs(r["iters"] - ro["iters"]) <= 1, (r["iters"], ro["iters"])
+    # true residual with the oracle's SpMV
+    tr = np.linalg.norm(rhs - o.spmv(xg)) / np.linalg.norm(rhs)
+    if ro["converged"]:
+        assert tr <= 1e-8
+    for f in (0, 1):   # p and S parts separately (Q33)
+        a, b = xg[f::2], ro["x"][f::2]
+        assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
+    # forced equal iteration count (tol = 0, maxit = oracle's count)
+    k = max(ro["iters"] - 1, 1)
+    ro2 = o.gmres(rhs, tol=0.0, restart=30, maxit=k)
+    x2 = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
+    r2 = g.solve(torch_dev(rhs), x2, tol=0.0, restart=30, maxit=k)
+    assert r2["iters"] == ro2["iters"] == k
+    x2 = x2.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(x2[f::2] - ro2["x"][f::2]) <= 1e-6 * np.linalg.norm(ro2["x"][f::2])
+    # residual histories agree where both are meaningful
+    m = min(len(r["hist"]), len(ro["hist"]))
+    assert np.allclose(r["hist"][:m], ro["hist"][:m], rtol=1e-5, atol=1e-12)
+
+
+def test_host_pointers_and_layout_options():
+    prob, J, rhs = make_system(1, dims=(9, 8, 1))
+    o = oracle.BF(J)
+    ro = o.gmres(rhs, tol=1e-8)
+    for on_device, bo in ((False, 0), (True, 1), (False, 1)):
+        g = gpu_solver(J, prob.dims, on_device=on_device, block_order=bo)
+        x = np.zeros(2 * J.n)
+        r = g.solve(np.ascontiguousarray(rhs), x, tol=1e-8)
+        assert abs(r["iters"] - ro["iters"]) <= 1
+        assert np.linalg.norm(x - ro["x"]) <= 1e-6 * np.linalg.norm(ro["x"])
+    # var_order = 1: swapped variables
+    Jsw = BSR2(J.n, J.row_ptr, J.col_idx, np.ascontiguousarray(J.vals[:, ::-1, ::-1]))
+    g = gpu_solver(Jsw, prob.dims, var_order=1)
+    x = np.zeros(2 * J.n)
+    bsw = np.ascontiguousarray(rhs.reshape(-1, 2)[:, ::-1].ravel())
+    r = g.solve(bsw, x, tol=1e-8)
+    xs = x.reshape(-1, 2)[:, ::-1].ravel()
+    assert np.linalg.norm(xs - ro["x"]) <= 1e-6 * np.linalg.norm(ro["x"])
+
+
+def test_options_parity():
+    """Non-default options are implemented identically on both sides."""
+    prob, J, rhs = make_system(2, dims=(10, 9, 8))
+    for opts in (dict(smoother=1), dict(interp_norm=0), dict(orth=1), dict(nu_pre=2, nu_post=2),
+                 dict(theta=0.5, max_coarse=30), dict(schur_as_printed=1), dict(nu_pre=0)):
+        o = oracle.BF(J, **opts)
+        g = gpu_solver(J, prob.dims, **opts)
+        for which in (0, 1):
+            assert g.num_levels(which) == o.nlev(which)
+            for l in range(o.nlev(which) - 1):
+                assert np.array_equal(g.level(which, l)["cf"], o.level(which, l)["cf"]), opts
+        v = seeded_vector(2 * J.n, 3)
+        zo = o.apply(v)
+        z = np.zeros(2 * J.n)
+        g.apply_precond(v, z)
+        assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo), opts
+        ro = o.gmres(rhs, tol=1e-8, maxit=300)
+        x = np.zeros(2 * J.n)
+        r = g.solve(rhs, x, tol=1e-8, maxit=300)
+        assert abs(r["iters"] - ro["iters"]) <= 1, (opts, r["iters"], ro["iters"])
+
+
+def test_edge_cases():
+    from paper_1611_00127_b200 import BFError
+    # single cell
+    J = BSR2(1, np.array([0, 1], np.int32), np.array([0], np.int32), np.array([[[2.0, 1.0], [1.0, 4.0]]]))
+    g = gpu_solver(J, (1, 1, 1))
+    b = np.array([1.0, 2.0])
+    x = np.zeros(2)
+    r = g.solve(b, x, tol=1e-12)
+    assert r["converged"] and np.allclose(x, np.linalg.solve(J.to_dense(), b), rtol=1e-12)
+    # zero rhs
+    prob, J, rhs = make_system(1, dims=(5, 5, 1))
+    g = gpu_solver(J, prob.dims)
+    x = np.ones(2 * J.n)
+    r = g.solve(np.zeros(2 * J.n), x)
+    assert r["iters"] == 0 and r["converged"] and np.all(x == 0)
+    # maxit reached -> not converged, not an error
+    r = g.solve(rhs, np.zeros(2 * J.n), tol=1e-15, maxit=3)
+    assert r["iters"] == 3 and not r["converged"]
+    # errors name the item
+    Jz = BSR2(J.n, J.row_ptr, J.col_idx, J.vals.copy())
+    q = J.row_ptr[7] + list(J.col_idx[J.row_ptr[7]:J.row_ptr[8]]).index(7)
+    Jz.vals[q, 1, 1] = 0.0
+    with pytest.raises(BFError, match="BF_ERR_ZERO_DIAG.*cell 7"):
+        gpu_solver(Jz, prob.dims)
+    Jn = BSR2(J.n, J.row_ptr, J.col_idx, J.vals.copy())
+    Jn.vals[3, 0, 1] = np.nan
+    with pytest.raises(BFError, match="BF_ERR_NONFINITE"):
+        gpu_solver(Jn, prob.dims)
+    ci = J.col_idx.copy()
+    ci[J.row_ptr[4]], ci[J.row_ptr[4] + 1] = ci[J.row_ptr[4] + 1], ci[J.row_ptr[4]]
+    with pytest.raises(BFError, match="BF_ERR_PATTERN.*row 4"):
+        gpu_solver(BSR2(J.n, J.row_ptr, ci, J.vals), prob.dims)
+    with pytest.raises(BFError, match="BF_ERR_ARG.*max_coarse"):
+        gpu_solver(J, prob.dims, max_coarse=1000)
+    with pytest.raises(BFError, match="BF_ERR_PATTERN"):
+        gpu_solver(J, (J.n + 1, 1, 1))      # n_cells from dims disagrees with row_ptr
+
+
+def test_determinism_repeat_setup():
+    prob, J, rhs = make_system(2, dims=(16, 15, 14))
+    g1 = gpu_solver(J, prob.dims)
+    g2 = gpu_solver(J, prob.dims)
+    for which in (0, 1):
+        for l in range(g1.num_levels(which)):
+            a, b = g1.level(which, l), g2.level(which, l)
+            for k in ("A", "P"):
+                if k in a:
+                    for u, v in zip(a[k], b[k]):
+                        assert np.array_equal(u, v)
+    x1, x2 = np.zeros(2 * J.n), np.zeros(2 * J.n)
+    r1, r2 = g1.solve(rhs, x1), g2.solve(rhs, x2)
+    assert r1["iters"] == r2["iters"] and np.array_equal(x1, x2)
