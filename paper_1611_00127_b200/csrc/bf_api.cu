@@ -1,6 +1,9 @@
 // bf_api.cu -- the C-ABI entry points of libbf.so (include/bf.h), handle and memory
 // management, error translation.  No exception crosses the ABI.
+#include <chrono>
+#include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -17,6 +20,28 @@ void cuda_check(cudaError_t e, const char *what) {
     throw Error(BF_ERR_OOM, std::string("device allocation failed: ") + what);
   }
   throw Error(BF_ERR_CUDA, std::string(cudaGetErrorString(e)) + " at " + what);
+}
+
+// process-wide pool of small pinned host buffers (cudaMallocHost costs milliseconds; a
+// setup+solve step must not pay it every time).  Thread-safe; one buffer per live handle.
+static std::mutex g_pin_mu;
+static std::vector<double *> g_pin_free;
+
+double *pinned_acquire() {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (!g_pin_free.empty()) {
+    double *p = g_pin_free.back();
+    g_pin_free.pop_back();
+    return p;
+  }
+  void *p = nullptr;
+  cuda_check(cudaMallocHost(&p, kPinnedBytes), "cudaMallocHost");
+  return static_cast<double *>(p);
+}
+
+void pinned_release(double *p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
 }
 
 void *dalloc(bf_ctx *c, size_t bytes) {
@@ -52,18 +77,28 @@ void free_csr(bf_ctx *c, DCsr &A) {
   A = DCsr();
 }
 
+static cudaEvent_t event_get(bf_ctx *c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  BF_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
 void timer_begin(bf_ctx *c, int k, cudaEvent_t *start) {
   *start = nullptr;
   if (!c->opt.timing) return;
-  BF_CUDA(cudaEventCreate(start));
+  *start = event_get(c);
   BF_CUDA(cudaEventRecord(*start, c->stream));
 }
 
 void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes) {
   if (!c->opt.timing || !start) return;
   c->timers[k].bytes += alg_bytes;
-  cudaEvent_t stop;
-  BF_CUDA(cudaEventCreate(&stop));
+  cudaEvent_t stop = event_get(c);
   BF_CUDA(cudaEventRecord(stop, c->stream));
   c->timers[k].pending.push_back(start);
   c->timers[k].pending.push_back(stop);
@@ -77,8 +112,8 @@ void timer_flush(bf_ctx *c) {
       float ms = 0.f;
       BF_CUDA(cudaEventElapsedTime(&ms, t.pending[i], t.pending[i + 1]));
       t.ms += ms;
-      cudaEventDestroy(t.pending[i]);
-      cudaEventDestroy(t.pending[i + 1]);
+      c->event_pool.push_back(t.pending[i]);
+      c->event_pool.push_back(t.pending[i + 1]);
     }
     t.pending.clear();
   }
@@ -93,9 +128,13 @@ static void destroy_ctx(bf_ctx *c) {
   cudaStreamSynchronize(c->stream);
   for (auto &t : c->timers)
     for (auto e : t.pending) cudaEventDestroy(e);
+  for (auto e : c->event_pool) cudaEventDestroy(e);
   for (auto &a : c->allocs) cudaFreeAsync(a.first, c->stream);
   c->allocs.clear();
-  if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->hpin) bf::pinned_release(c->hpin);
+  if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
+  if (c->apply_graph) cudaGraphDestroy(c->apply_graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaStreamSynchronize(c->stream);
   delete c;
 }
@@ -165,13 +204,32 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     int dev = 0;
     BF_CUDA(cudaGetDevice(&dev));
     BF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaMemPool_t pool;
+    BF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;  // keep freed blocks cached: setup allocates/frees many temporaries
+    BF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    const char *verbose = getenv("BF_VERBOSE");
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+      if (!verbose) return;
+      BF_CUDA(cudaStreamSynchronize(c->stream));
+      auto t1 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[bf_setup] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+      t0 = t1;
+    };
     validate_and_ingest(c, J);
+    lap("ingest");
     build_split(c);
+    lap("split");
     build_schur(c);
+    lap("schur");
     build_hierarchy(c, 0, c->blk[3]);
+    lap("amg A_ss");
     build_hierarchy(c, 1, c->blk[4]);
+    lap("amg S~");
     alloc_solve_workspace(c, 30);
     BF_CUDA(cudaStreamSynchronize(c->stream));
+    lap("workspace");
   } catch (const Error &e) {
     g_setup_err = e.msg;
     bf_status st = e.st;

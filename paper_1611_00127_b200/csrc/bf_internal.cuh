@@ -86,6 +86,14 @@ struct bf_ctx {
   int64_t dev_bytes = 0;
   int64_t launches = 0;
   bf::Timer timers[4];
+  std::vector<cudaEvent_t> event_pool;
+  // CUDA graph of the BF apply (k_vcycle.cu)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t apply_graph = nullptr;
+  cudaGraphExec_t apply_exec = nullptr;
+  cudaGraphNode_t apply_split_node = nullptr;
+  cudaKernelNodeParams split_params{};
+  int64_t apply_graph_kernels = 0;
   int num_sms = 148;
 };
 
@@ -100,6 +108,9 @@ T *dalloc_t(bf_ctx *c, size_t count) {
   return static_cast<T *>(dalloc(c, count * sizeof(T) + 16));
 }
 void free_csr(bf_ctx *c, DCsr &A);
+constexpr size_t kPinnedBytes = 4096;
+double *pinned_acquire();
+void pinned_release(double *p);
 void timer_begin(bf_ctx *c, int k, cudaEvent_t *start);
 void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes = 0.0);
 void timer_flush(bf_ctx *c);
@@ -125,6 +136,7 @@ void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spm
 void csr_spmv(bf_ctx *c, const DCsr &A, const double *x, double *y);    // k_spmv.cu
 void vcycle(bf_ctx *c, int which, const double *b, double *x);          // k_vcycle.cu
 void bf_apply(bf_ctx *c, const double *v, double *z);                   // k_vcycle.cu
+void bf_apply_graph(bf_ctx *c, const double *v, double *z);             // k_vcycle.cu
 void alloc_solve_workspace(bf_ctx *c, int restart);                     // k_gmres.cu
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu

@@ -12,6 +12,8 @@
 //   pass 1: 8N (j+2), pass 2: 8N (j+3), pass 3: 8N (j+3)  (+ 16N for the scaling of v_{j+1}).
 #include <cmath>
 #include <cstring>
+#include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "bf_internal.cuh"
@@ -55,23 +57,26 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double *pa
 
 // pass 1: out[i] = V_i . w, i < NV
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS) k_dots(int64_t N, const double *__restrict__ V,
+__global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double *__restrict__ V,
                                                       const double *__restrict__ w, double *partial,
                                                       double *out, unsigned int *counter) {
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; i++) acc[i] = 0.0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double v[NV];  // all NV loads in flight before the FMAs (memory-level parallelism)
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
     double wt = __ldcs(w + t);
 #pragma unroll
-    for (int i = 0; i < NV; i++) acc[i] += __ldcs(V + (size_t)i * N + t) * wt;
+    for (int i = 0; i < NV; i++) acc[i] += v[i] * wt;
   }
   block_reduce_store<NV>(acc, partial, out, NV, counter);
 }
 
 // pass 2: w <- w - sum_i h_i V_i ; out[i] = V_i . w (new w)
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS) k_axpy_dots(int64_t N, const double *__restrict__ V, double *w,
+__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_dots(int64_t N, const double *__restrict__ V, double *w,
                                                            const double *__restrict__ h, double *partial,
                                                            double *out, unsigned int *counter) {
   __shared__ double hs[NV];
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_axpy_dots(int64_t N, const doub
 
 // pass 3: y = w - sum_i h_i V_i written to `y` (may be the next basis slot); out[0] = ||y||^2
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS) k_axpy_norm(int64_t N, const double *__restrict__ V,
+__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const double *__restrict__ V,
                                                            const double *__restrict__ w,
                                                            const double *__restrict__ h, double *__restrict__ y,
                                                            double *partial, double *out, unsigned int *counter) {
@@ -106,9 +111,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_axpy_norm(int64_t N, const doub
   __syncthreads();
   double acc[1] = {0.0};
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
     double wt = __ldcs(w + t);
 #pragma unroll
-    for (int i = 0; i < NV; i++) wt -= hs[i] * __ldcs(V + (size_t)i * N + t);
+    for (int i = 0; i < NV; i++) wt -= hs[i] * v[i];
     y[t] = wt;
     acc[0] += wt * wt;
   }
@@ -209,7 +217,7 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
     c->hdev = dalloc_t<double>(c, 4 * MAXNV + 8);
     c->counter = dalloc_t<unsigned int>(c, 4);
     BF_CUDA(cudaMemsetAsync(c->counter, 0, 4 * sizeof(unsigned int), c->stream));
-    BF_CUDA(cudaMallocHost(&c->hpin, sizeof(double) * (4 * MAXNV + 8)));
+    c->hpin = pinned_acquire();  // >= (4 MAXNV + 8) doubles
   }
   if (c->Vm < restart + 1) {
     dfree(c, c->V);
@@ -220,10 +228,27 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
 
 static int grid_for(bf_ctx *c) { return c->red_blocks; }
 
+// one full wave: SMs x resident CTAs of this kernel (no partial second wave for the
+// grid-stride reductions), capped by the partial-sum buffer (4 CTAs per SM)
+template <class K>
+static int wave_grid(bf_ctx *c, K kernel) {
+  static std::unordered_map<const void *, int> cache;
+  auto it = cache.find((const void *)kernel);
+  int per_sm;
+  if (it == cache.end()) {
+    BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, RED_THREADS, 0));
+    cache[(const void *)kernel] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  per_sm = std::max(1, std::min(per_sm, 4));
+  return c->num_sms * per_sm;
+}
+
 // out = a . b  (host value, synchronises)
 static double dot_host(bf_ctx *c, const double *a, const double *b) {
   int64_t N = 2 * (int64_t)c->n;
-  k_dots<1><<<grid_for(c), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, c->hdev + 3 * MAXNV, c->counter);
+  k_dots<1><<<wave_grid(c, k_dots<1>), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, c->hdev + 3 * MAXNV, c->counter);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   BF_CUDA(cudaMemcpyAsync(c->hpin, c->hdev + 3 * MAXNV, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -270,21 +295,21 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     for (int j = 0; j < m; j++) {
       const double *vj = V + (size_t)j * N;
       double *vn = V + (size_t)(j + 1) * N;
-      bf_apply(c, vj, c->z);  // z = M^-1 v_j
+      bf_apply_graph(c, vj, c->z);  // z = M^-1 v_j
       cudaEvent_t t0;
       timer_begin(c, 0, &t0);
       bsr_spmv(c, c->z, c->w);  // w = J z
       timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
       int nv = j + 1;
       timer_begin(c, 1, &t0);
-      BF_NV_SWITCH(nv, (k_dots<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1, c->counter)));
+      BF_NV_SWITCH(nv, (k_dots<NV><<<wave_grid(c, k_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1, c->counter)));
       if (c->opt.orth == 0) {
-        BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, c->red, hd2,
+        BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<wave_grid(c, k_axpy_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, c->red, hd2,
                                                                             c->counter)));
-        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd2, vn, c->red, hdn,
+        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd2, vn, c->red, hdn,
                                                                             c->counter)));
       } else {
-        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<G, RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, vn, c->red, hdn,
+        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, vn, c->red, hdn,
                                                                             c->counter)));
       }
       c->launches += c->opt.orth == 0 ? 3 : 2;
@@ -338,7 +363,7 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     (void)yd;
     BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, V, c->hdev + MAXNV, c->w)));
     BF_LAUNCH(c);
-    bf_apply(c, c->w, c->z);
+    bf_apply_graph(c, c->w, c->z);
     k_add_inplace<<<G, 256, 0, c->stream>>>(N, x, c->z);
     BF_LAUNCH(c);
     // true residual at the end of the cycle (R11)

@@ -10,71 +10,110 @@ enum CsrMode {
   OP_SPMV = 0,          // y = A x
   OP_RESID = 1,         // y = b - A x
   OP_SMOOTH = 2,        // dn = alpha dir + beta (b - A x) * dinv ; y = x + dn ; aux = dn (if aux)
-  OP_SMOOTH0_RESID = 3, // x0 = beta b * dinv ; y = b - A x0 ; aux = x0   (x0 gathered on the fly)
+  OP_SPMV_X0 = 3,       // y = A x ; aux = beta y * dinv  (restriction that also seeds the next level's x0)
   OP_ADD = 4,           // y = y + A x
-  OP_SUB = 5            // y = b - A x written as y = b - (A x) (same as RESID, used for A_ps)
+  OP_SUB_X0 = 5         // y = b - A x ; aux = beta y * dinv  (A_ps coupling that seeds the S~ level-0 x0)
 };
 
+// Warp-staged CSR kernel: each warp owns R = 32/G consecutive rows (G lanes per row).
+// The warp streams the contiguous nonzero range of its rows in chunks of CSR_CAP entries
+// into shared memory (coalesced streaming loads of col/val), then the G lanes of each row
+// form a_ij x_j with row-owned gathers of x (consecutive rows -> consecutive addresses for
+// stencil-like rows, few L1 wavefronts) and combine with shuffles.  G = 1 for the short fine-level rows (thread-per-row epilogue), larger G for
+// the long Galerkin rows of the coarse levels (and for small levels, so that enough
+// warps exist to fill the 148 SMs).  No padding, full coalescing, any row length.
+constexpr int CSR_WARPS = 8;
+constexpr int CSR_CAP = 256;
+
 template <int MODE, int G>
-__global__ void __launch_bounds__(256) k_csr(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                             const double *__restrict__ v, const double *__restrict__ x,
-                                             const double *__restrict__ b, const double *__restrict__ dinv,
-                                             double *__restrict__ y, double *__restrict__ aux, double alpha,
-                                             double beta, const double *__restrict__ dir) {
-  int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  int r = gid / G;
-  int lane = (G == 1) ? 0 : (threadIdx.x % G);
+__global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, const int32_t *__restrict__ rp,
+                                                        const int32_t *__restrict__ ci,
+                                                        const double *__restrict__ v, const double *__restrict__ x,
+                                                        const double *__restrict__ b,
+                                                        const double *__restrict__ dinv, double *__restrict__ y,
+                                                        double *__restrict__ aux, double alpha, double beta,
+                                                        const double *__restrict__ dir) {
+  constexpr int R = 32 / G;
+  __shared__ double sval[CSR_WARPS][CSR_CAP];
+  __shared__ int32_t scol[CSR_WARPS][CSR_CAP];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int r0 = (blockIdx.x * CSR_WARPS + warp) * R;
+  if (r0 >= n) return;  // whole warp
+  int r = r0 + lane / G;
+  int sub = lane % G;
   bool ok = r < n;
-  int a = ok ? __ldg(rp + r) : 0, e = ok ? __ldg(rp + r + 1) : 0;
-  double s = 0.0;
-  for (int q = a + lane; q < e; q += G) {
-    int col = __ldcs(ci + q);
-    double av = __ldcs(v + q);
-    double xv;
-    if (MODE == OP_SMOOTH0_RESID) xv = beta * (__ldg(b + col) * __ldg(dinv + col));
-    else xv = __ldg(x + col);
-    s += av * xv;
+  int rend = min(r0 + R, n);
+  int s = __ldg(rp + r0), e = __ldg(rp + rend);
+  int my_lo = ok ? __ldg(rp + r) : e, my_hi = ok ? __ldg(rp + r + 1) : e;
+  double acc = 0.0;
+  double *sv = sval[warp];
+  int32_t *sc = scol[warp];
+  for (int cs = s; cs < e; cs += CSR_CAP) {
+    int ce = min(cs + CSR_CAP, e);
+    // stage the warp's contiguous (col, val) range: fully coalesced streaming loads
+#pragma unroll 4
+    for (int k = cs + lane; k < ce; k += 32) {
+      sc[k - cs] = __ldcs(ci + k);
+      sv[k - cs] = __ldcs(v + k);
+    }
+    __syncwarp();
+    // row-owned products: for stencil-like rows the gathers of consecutive rows are
+    // consecutive addresses (one or two wavefronts per warp instruction)
+    int lo = max(my_lo, cs), hi = min(my_hi, ce);
+#pragma unroll 4
+    for (int k = lo + sub; k < hi; k += G) {
+      int col = sc[k - cs];
+      acc += sv[k - cs] * __ldg(x + col);
+    }
+    __syncwarp();
   }
   if (G > 1) {
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
   }
-  if (!ok || lane != 0) return;
+  if (!ok || sub != 0) return;
+  double sacc = acc;
   if (MODE == OP_SPMV) {
-    y[r] = s;
-  } else if (MODE == OP_RESID || MODE == OP_SUB) {
-    y[r] = b[r] - s;
+    y[r] = sacc;
+  } else if (MODE == OP_SPMV_X0) {
+    y[r] = sacc;
+    aux[r] = beta * (sacc * dinv[r]);
+  } else if (MODE == OP_RESID) {
+    y[r] = b[r] - sacc;
+  } else if (MODE == OP_SUB_X0) {
+    double t = b[r] - sacc;
+    y[r] = t;
+    aux[r] = beta * (t * dinv[r]);
   } else if (MODE == OP_SMOOTH) {
-    double dn = beta * ((b[r] - s) * dinv[r]);
+    double dn = beta * ((b[r] - sacc) * dinv[r]);
     if (dir) dn += alpha * dir[r];
     y[r] = x[r] + dn;
     if (aux) aux[r] = dn;
-  } else if (MODE == OP_SMOOTH0_RESID) {
-    y[r] = b[r] - s;
-    aux[r] = beta * (b[r] * dinv[r]);
   } else if (MODE == OP_ADD) {
-    y[r] += s;
+    y[r] += sacc;
   }
 }
 
-inline int lanes_for(const DCsr &A) {
+// lanes per row: keep R * (mean row length) near one chunk, and keep >= ~4 warps per SM
+inline int lanes_for(const bf_ctx *c, const DCsr &A) {
   double avg = A.n ? (double)A.nnz / A.n : 1.0;
-  int g = 1;
-  while (g < 32 && g < avg * 0.75) g <<= 1;
-  return g;
+  int G = 1;
+  while (G < 32 && (32 / G) * avg > CSR_CAP) G <<= 1;
+  while (G < 32 && (double)A.n * G / 32.0 < 4.0 * c->num_sms) G <<= 1;
+  return G;
 }
 
 template <int MODE>
 void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
             double *aux, double alpha, double beta, const double *dir) {
   if (A.n == 0) return;
-  int G = lanes_for(A);
-  int64_t threads = (int64_t)A.n * G;
-  int blocks = div_up(threads, 256);
-#define BF_CSR_CASE(g)                                                                                   \
-  case g:                                                                                                \
-    k_csr<MODE, g><<<blocks, 256, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, x, b, dinv, y, aux, alpha, beta, \
-                                                  dir);                                                  \
+  int G = lanes_for(c, A);
+  int rows_per_block = (32 / G) * CSR_WARPS;
+  int blocks = div_up(A.n, rows_per_block);
+#define BF_CSR_CASE(g)                                                                                  \
+  case g:                                                                                               \
+    k_csr<MODE, g><<<blocks, CSR_WARPS * 32, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, x, b, dinv, y, aux, alpha, \
+                                                             beta, dir);                                \
     break;
   switch (G) {
     BF_CSR_CASE(1)

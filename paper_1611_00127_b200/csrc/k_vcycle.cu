@@ -6,6 +6,8 @@
 #include "bf_internal.cuh"
 #include "k_spmv.cuh"
 
+#include <vector>
+
 namespace bf {
 
 // forward/back substitution with the LU of the coarsest matrix, one CTA, staged in smem
@@ -47,52 +49,59 @@ __global__ void k_zero(int n, double *x) {
   if (i < n) x[i] = 0.0;
 }
 
-// one smoothing pass (l1-Jacobi, or Chebyshev of degree m on [lo,1]) on level L; x in/out.
-// from_zero: x == 0 on entry.  If want_resid, also leaves r = b - A x in L.r (fused when possible).
-static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool from_zero, bool want_resid) {
+// beta of the first smoothing step from x = 0: x0 = beta b ./ dl1
+static double x0_beta(const bf_options &o) {
+  return o.smoother == 1 ? 2.0 / (1.0 + o.cheb_lo) : 1.0;  // Chebyshev: 1/theta, theta = (1+lo)/2
+}
+
+// Level invariant on entry to vcycle_level(l): L.b holds the right-hand side and L.x holds
+// x0 = beta b ./ dl1 (written by whichever kernel produced b: the split, the A_ps coupling,
+// or the restriction of the finer level), i.e. the first smoothing step from zero is already
+// done.  This keeps one gather per nonzero in every smoother kernel.
+
+// one smoothing pass (l1-Jacobi, or Chebyshev of degree m on [lo,1]); x in/out (pointer may
+// be swapped with L.t).  first: x holds x0 (the pass's first step is already applied).
+// want_resid: leave r = b - A x in L.r.
+static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool first, bool want_resid) {
   const bf_options &o = c->opt;
   int n = L.A.n;
-  if (o.smoother == 0) {  // x <- x + (b - A x) ./ dl1
-    if (from_zero) {
-      if (want_resid) {
-        csr_op<OP_SMOOTH0_RESID>(c, L.A, nullptr, L.b, L.d, L.r, x, 0.0, 1.0, nullptr);
-        return;
-      }
-      // x = b ./ d  (SMOOTH with x = 0 would read x): use the fused kernel and drop r
-      csr_op<OP_SMOOTH0_RESID>(c, L.A, nullptr, L.b, L.d, L.r, x, 0.0, 1.0, nullptr);
-      return;
-    }
-    csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, nullptr, 0.0, 1.0, nullptr);
+  auto swap_t = [&]() {
     double *tmp = x;
     x = L.t;
     L.t = tmp;
+  };
+  if (o.smoother == 0) {  // x <- x + (b - A x) ./ dl1
+    if (!first) {
+      csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, nullptr, 0.0, 1.0, nullptr);
+      swap_t();
+    }
   } else {  // Chebyshev acceleration of D^-1 A on [lo, 1] (three-term recurrence)
     double lo = o.cheb_lo, theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0, sigma = theta / delta;
     double rho = 1.0 / sigma;
     double *dir = L.r;  // direction storage (r is recomputed below when needed)
-    if (from_zero) {
-      // dir = (1/theta) b/d ; x = dir
-      csr_op<OP_SMOOTH0_RESID>(c, L.A, nullptr, L.b, L.d, L.t /*scratch r*/, x, 0.0, 1.0 / theta, nullptr);
+    if (first) {
       BF_CUDA(cudaMemcpyAsync(dir, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
     } else {
       csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, dir, 0.0, 1.0 / theta, nullptr);
-      double *tmp = x;
-      x = L.t;
-      L.t = tmp;
+      swap_t();
     }
     for (int k = 1; k < o.cheb_degree; k++) {
       double rho_new = 1.0 / (2.0 * sigma - rho);
       csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, dir, rho_new * rho, 2.0 * rho_new / delta, dir);
-      double *tmp = x;
-      x = L.t;
-      L.t = tmp;
+      swap_t();
       rho = rho_new;
     }
   }
   if (want_resid) csr_op<OP_RESID>(c, L.A, x, L.b, nullptr, L.r, nullptr, 0.0, 0.0, nullptr);
 }
 
-// V-cycle on level l with rhs in L.b; result left in L.x (pointer may be swapped with L.t)
+__global__ void k_x0(int n, double beta, const double *__restrict__ b, const double *__restrict__ dinv,
+                     double *__restrict__ x) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = beta * (b[i] * dinv[i]);
+}
+
+// V-cycle on level l (invariant above); result left in L.x (pointer may be swapped with L.t)
 static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   Level &L = h.lv[l];
   int n = L.A.n;
@@ -103,8 +112,11 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
       k_coarse_solve<<<1, 128, smem, c->stream>>>(n, h.lu, h.piv, L.b, L.x);
       BF_LAUNCH(c);
       BF_CUDA(cudaGetLastError());
-    } else {  // stalled coarsening: 4 l1-Jacobi sweeps from zero
-      csr_op<OP_SMOOTH0_RESID>(c, L.A, nullptr, L.b, L.d, L.r, L.x, 0.0, 1.0, nullptr);
+    } else {  // stalled coarsening: 4 l1-Jacobi sweeps from zero (x0 = b ./ dl1 is the first)
+      if (o.smoother == 1) {  // x0 was seeded for Chebyshev: reseed for l1-Jacobi
+        k_x0<<<div_up(n, 256), 256, 0, c->stream>>>(n, 1.0, L.b, L.d, L.x);
+        BF_LAUNCH(c);
+      }
       for (int s = 0; s < 3; s++) {
         csr_op<OP_SMOOTH>(c, L.A, L.x, L.b, L.d, L.t, nullptr, 0.0, 1.0, nullptr);
         double *tmp = L.x;
@@ -123,7 +135,8 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
     for (int s = 0; s < o.nu_pre; s++) smooth_pass(c, L, x, s == 0, s == o.nu_pre - 1);
   }
   Level &Lc = h.lv[l + 1];
-  csr_op<OP_SPMV>(c, L.R, L.r, nullptr, nullptr, Lc.b, nullptr, 0.0, 0.0, nullptr);  // b_c = R r
+  // b_c = R r, and x0_c = beta b_c ./ dl1_c for the next level
+  csr_op<OP_SPMV_X0>(c, L.R, L.r, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
   vcycle_level(c, h, l + 1);
   csr_op<OP_ADD>(c, L.P, Lc.x, nullptr, nullptr, x, nullptr, 0.0, 0.0, nullptr);  // x += P e
   for (int s = 0; s < o.nu_post; s++) smooth_pass(c, L, x, false, false);
@@ -136,19 +149,25 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
 void vcycle(bf_ctx *c, int which, const double *b, double *x) {
   Hier &h = c->h[which];
   Level &L0 = h.lv[0];
-  BF_CUDA(cudaMemcpyAsync(L0.b, b, sizeof(double) * L0.A.n, cudaMemcpyDeviceToDevice, c->stream));
+  int n = L0.A.n;
+  BF_CUDA(cudaMemcpyAsync(L0.b, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  k_x0<<<div_up(n, 256), 256, 0, c->stream>>>(n, x0_beta(c->opt), L0.b, L0.d, L0.x);
+  BF_LAUNCH(c);
   vcycle_level(c, h, 0);
-  BF_CUDA(cudaMemcpyAsync(x, L0.x, sizeof(double) * L0.A.n, cudaMemcpyDeviceToDevice, c->stream));
+  BF_CUDA(cudaMemcpyAsync(x, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
 }
 
-// R_s v -> bs, R_p v -> vp (interleaved in the caller's var_order)
+// R_p v -> vp, R_s v -> vs (interleaved in the caller's var_order); also x0 of the A_ss V-cycle
 __global__ void k_split_vec(int n, int ip, const double *__restrict__ v, double *__restrict__ vp,
-                            double *__restrict__ vs) {
+                            double *__restrict__ vs, const double *__restrict__ dinv, double beta,
+                            double *__restrict__ x0) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 a = reinterpret_cast<const double2 *>(v)[i];
+  double s = ip ? a.x : a.y;
   vp[i] = ip ? a.y : a.x;
-  vs[i] = ip ? a.x : a.y;
+  vs[i] = s;
+  x0[i] = beta * (s * dinv[i]);
 }
 
 __global__ void k_merge_vec(int n, int ip, const double *__restrict__ p, const double *__restrict__ s,
@@ -163,16 +182,95 @@ void bf_apply(bf_ctx *c, const double *v, double *z) {
   int ip = c->var_order;
   Hier &hs = c->h[0], &hS = c->h[1];
   // Alg. 3 step 2: A_ss s = R_s r_k by one V-cycle
-  k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, v, c->vp, hs.lv[0].b);
+  k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, v, c->vp, hs.lv[0].b, hs.lv[0].d,
+                                                     x0_beta(c->opt), hs.lv[0].x);
   BF_LAUNCH(c);
   vcycle_level(c, hs, 0);
   // step 3: r = R_p r_k - A_ps s
-  csr_op<OP_SUB>(c, c->blk[1], hs.lv[0].x, c->vp, nullptr, hS.lv[0].b, nullptr, 0.0, 0.0, nullptr);
+  csr_op<OP_SUB_X0>(c, c->blk[1], hs.lv[0].x, c->vp, hS.lv[0].d, hS.lv[0].b, hS.lv[0].x, 0.0, x0_beta(c->opt),
+                    nullptr);
   // step 4: S~ p = r by one V-cycle
   vcycle_level(c, hS, 0);
   k_merge_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, hS.lv[0].x, hs.lv[0].x, z);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
+}
+
+// The whole BF apply (~60 kernels, most of them small coarse-level kernels) replayed as one
+// CUDA graph: captured once per handle on a private stream, launched on the caller's stream.
+// Only the input vector changes between applies; it is patched into the split kernel node.
+void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
+  if (z != c->z) {  // the graph writes c->z; other targets take the eager path
+    bf_apply(c, v, z);
+    return;
+  }
+  if (!c->apply_exec) {
+    if (!c->cap_stream) BF_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    int64_t l0 = c->launches;
+    BF_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      bf_apply(c, v, z);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(c->cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = user;
+      throw;
+    }
+    cudaGraph_t g;
+    BF_CUDA(cudaStreamEndCapture(c->cap_stream, &g));
+    c->stream = user;
+    c->apply_graph_kernels = c->launches - l0;
+    c->launches = l0;
+    BF_CUDA(cudaGraphInstantiate(&c->apply_exec, g, 0));
+    // locate the split kernel node (the only node that reads v)
+    size_t nn = 0;
+    BF_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    BF_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+    c->apply_split_node = nullptr;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      BF_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams p;
+      BF_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
+      if (p.func == (void *)k_split_vec) {
+        c->apply_split_node = nd;
+        c->split_params = p;
+      }
+    }
+    c->apply_graph = g;
+    if (!c->apply_split_node) throw Error(BF_ERR_CUDA, "split node not found in the BF apply graph");
+  }
+  // patch the input pointer of the split kernel
+  int n = c->n, ip = c->var_order;
+  Hier &hs = c->h[0];
+  double beta = x0_beta(c->opt);
+  double *vp = c->vp, *vs = hs.lv[0].b, *x0 = hs.lv[0].x;
+  const double *dinv = hs.lv[0].d;
+  (void)vs;
+  (void)x0;
+  void *args[8];
+  // argument values as captured, with v replaced (the other buffers are fixed per handle)
+  void **cap = c->split_params.kernelParams;
+  const double *vin = v;
+  args[0] = cap[0];
+  args[1] = cap[1];
+  args[2] = (void *)&vin;
+  args[3] = cap[3];
+  args[4] = cap[4];
+  args[5] = cap[5];
+  args[6] = cap[6];
+  args[7] = cap[7];
+  (void)n; (void)ip; (void)beta; (void)vp; (void)dinv;
+  cudaKernelNodeParams p = c->split_params;
+  p.kernelParams = args;
+  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_split_node, &p));
+  BF_CUDA(cudaGraphLaunch(c->apply_exec, c->stream));
+  c->launches += c->apply_graph_kernels;
 }
 
 }  // namespace bf

@@ -440,3 +440,14 @@ def test_hash_deterministic():
     assert len(np.unique(hs)) > 4080          # no systematic collisions
     assert 0.4 < (hs / 2**32).mean() < 0.6
     assert oracle.h32(1, 2, 3) == oracle.h32(1, 2, 3) and oracle.h32(1, 2, 3) != oracle.h32(1, 3, 3)
+
+
+def test_bsr_spmv_vs_scipy():
+    """w = J z (P:L138-140 operator) against scipy's BSR product (an independent library)."""
+    prob, J, rhs = make_system(2, dims=(7, 6, 5))
+    x = seeded_vector(2 * J.n, 9)
+    y = oracle.bsr_spmv(J, x)
+    ys = J.to_scipy() @ x
+    assert np.max(np.abs(y - ys)) <= 1e-14 * (np.abs(J.to_scipy()) @ np.abs(x)).max()
+    bf = oracle.BF(J)
+    assert np.array_equal(bf.spmv(x), y)
