@@ -97,6 +97,19 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def reduce_over_ranks(dist, t_ms, units, device="cpu"):
+    """Whole-job aggregate of independent replicas: max of the per-rank device times and the
+    sum of the per-rank work units (works with NCCL on GPU tensors and gloo on CPU)."""
+    if dist is None:
+        return t_ms, units
+    import torch
+    t = torch.tensor([t_ms], dtype=torch.float64, device=device)
+    u = torch.tensor([units], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -264,12 +277,7 @@ def run_ours(args):
     ends = starts[1:] + [e1]
     solve_ms = [rec["mid"][i].elapsed_time(ends[i]) for i in range(args.steps)]
     units = float(sum(N * it for it in rec["iters"]))
-    if dist:
-        t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-        u = torch.tensor([units], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)
-        t_ms, units = float(t.item()), float(u.item())
+    t_ms, units = reduce_over_ranks(dist, t_ms, units, "cuda")
     value = units / (t_ms / 1e3)
 
     # ---- roofline of the dominant kernel class (device time share inside the timed region)
@@ -315,12 +323,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         te = f0.elapsed_time(f1)
         ue = float(N * its)
-        if dist:
-            t = torch.tensor([te], dtype=torch.float64, device="cuda")
-            u = torch.tensor([ue], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dist.all_reduce(u, op=dist.ReduceOp.SUM)
-            te, ue = float(t.item()), float(u.item())
+        te, ue = reduce_over_ranks(dist, te, ue, "cuda")
         h2d = (h_rp.numel() * 4 + h_ci.numel() * 4 + h_v.numel() * 8 + h_b.numel() * 8 + h_x.numel() * 8)
         e2e = {"value": ue / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(N * 8), "steps": k_e2e}
