@@ -1,6 +1,7 @@
 // bf_api.cu -- the C-ABI entry points of libbf.so (include/bf.h), handle and memory
 // management, error translation.  No exception crosses the ABI.
 #include <chrono>
+#include <map>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
@@ -44,17 +45,66 @@ void pinned_release(double *p) {
   g_pin_free.push_back(p);
 }
 
-void *dalloc(bf_ctx *c, size_t bytes) {
-  void *p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    throw Error(BF_ERR_OOM, "cudaMallocAsync of " + std::to_string(bytes) + " bytes failed (" +
-                                cudaGetErrorString(e) + ")");
+// Process-wide caching device allocator.  cudaMallocAsync/cudaFreeAsync were measured to
+// block the host for up to ~1.5 s per setup when the stream-ordered pool had to remap; the
+// setup allocates and frees ~2000 temporaries.  Blocks are cached by size class and never
+// returned to the driver.  A block freed by a handle is reused only after that handle's next
+// stream synchronisation (bf::sync), so queued work can never see its memory recycled.
+static std::mutex g_dev_mu;
+static std::multimap<size_t, void *> g_dev_free;  // size class -> block
+
+static size_t size_class(size_t bytes) {
+  if (bytes <= 4096) {
+    size_t s = 256;
+    while (s < bytes) s <<= 1;
+    return s;
   }
-  c->allocs.emplace_back(p, bytes);
-  c->dev_bytes += (int64_t)bytes;
+  if (bytes <= (1u << 20)) return (bytes + 4095) & ~size_t(4095);
+  return (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+}
+
+void *dalloc(bf_ctx *c, size_t bytes) {
+  size_t sc = size_class(bytes);
+  void *p = nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_dev_free.lower_bound(sc);
+    if (it != g_dev_free.end() && it->first <= sc + sc / 4) {  // accept <= 25 % slack
+      sc = it->first;
+      p = it->second;
+      g_dev_free.erase(it);
+    }
+  }
+  if (!p) {
+    cudaError_t e = cudaMalloc(&p, sc);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      {  // release the cache and retry once
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        for (auto &f : g_dev_free) cudaFree(f.second);
+        g_dev_free.clear();
+      }
+      e = cudaMalloc(&p, sc);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error(BF_ERR_OOM, "cudaMalloc of " + std::to_string(sc) + " bytes failed (" +
+                                    cudaGetErrorString(e) + ")");
+      }
+    }
+  }
+  c->alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->allocs.emplace_back(p, sc);
+  c->dev_bytes += (int64_t)sc;
   return p;
+}
+
+// blocks freed since the last sync of this handle become reusable after the sync
+static void release_pending(bf_ctx *c) {
+  if (c->pending_free.empty()) return;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  for (auto &f : c->pending_free) g_dev_free.emplace(f.second, f.first);
+  c->pending_free.clear();
 }
 
 void dfree(bf_ctx *c, void *p) {
@@ -62,9 +112,9 @@ void dfree(bf_ctx *c, void *p) {
   for (size_t i = 0; i < c->allocs.size(); i++) {
     if (c->allocs[i].first == p) {
       c->dev_bytes -= (int64_t)c->allocs[i].second;
+      c->pending_free.push_back(c->allocs[i]);
       c->allocs[i] = c->allocs.back();
       c->allocs.pop_back();
-      cudaFreeAsync(p, c->stream);
       return;
     }
   }
@@ -105,6 +155,14 @@ void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes) {
   c->timers[k].launches++;
 }
 
+void sync(bf_ctx *c) {
+  auto t0 = std::chrono::steady_clock::now();
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  release_pending(c);
+  c->sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->syncs++;
+}
+
 void timer_flush(bf_ctx *c) {
   for (auto &t : c->timers) {
     for (size_t i = 0; i + 1 < t.pending.size(); i += 2) {
@@ -129,8 +187,9 @@ static void destroy_ctx(bf_ctx *c) {
   for (auto &t : c->timers)
     for (auto e : t.pending) cudaEventDestroy(e);
   for (auto e : c->event_pool) cudaEventDestroy(e);
-  for (auto &a : c->allocs) cudaFreeAsync(a.first, c->stream);
+  for (auto &a : c->allocs) c->pending_free.push_back(a);
   c->allocs.clear();
+  bf::release_pending(c);
   if (c->hpin) bf::pinned_release(c->hpin);
   if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
   if (c->apply_graph) cudaGraphDestroy(c->apply_graph);
@@ -204,17 +263,15 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     int dev = 0;
     BF_CUDA(cudaGetDevice(&dev));
     BF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
-    cudaMemPool_t pool;
-    BF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;  // keep freed blocks cached: setup allocates/frees many temporaries
-    BF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     const char *verbose = getenv("BF_VERBOSE");
     auto t0 = std::chrono::steady_clock::now();
     auto lap = [&](const char *what) {
       if (!verbose) return;
       BF_CUDA(cudaStreamSynchronize(c->stream));
       auto t1 = std::chrono::steady_clock::now();
-      fprintf(stderr, "[bf_setup] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+      fprintf(stderr, "[bf_setup] %-12s %8.2f ms  (alloc/free %.2f ms, %lld syncs waiting %.2f ms)\n", what,
+              std::chrono::duration<double, std::milli>(t1 - t0).count(), c->alloc_ms, (long long)c->syncs,
+              c->sync_ms);
       t0 = t1;
     };
     validate_and_ingest(c, J);
@@ -223,6 +280,8 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     lap("split");
     build_schur(c);
     lap("schur");
+    tile_csr(c, c->blk[1]);
+    if (getenv("BF_NO_TMA")) c->use_tma = false;
     build_hierarchy(c, 0, c->blk[3]);
     lap("amg A_ss");
     build_hierarchy(c, 1, c->blk[4]);

@@ -23,6 +23,8 @@ namespace bf {
 struct DCsr {
   int32_t n = 0, m = 0;  // rows, cols
   int64_t nnz = 0;
+  int32_t rpt = 0, cap = 0;  // TMA tiling: rows per tile, max nonzeros per tile (0: not tiled)
+  int32_t g = 1;             // lanes per row in the TMA kernel
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
 };
@@ -83,6 +85,7 @@ struct bf_ctx {
   int red_blocks = 0;
   // bookkeeping
   std::vector<std::pair<void *, size_t>> allocs;
+  std::vector<std::pair<void *, size_t>> pending_free;  // reusable after the next sync
   int64_t dev_bytes = 0;
   int64_t launches = 0;
   bf::Timer timers[4];
@@ -95,6 +98,10 @@ struct bf_ctx {
   cudaKernelNodeParams split_params{};
   int64_t apply_graph_kernels = 0;
   int num_sms = 148;
+  bool use_tma = true;
+  double alloc_ms = 0.0;
+  int64_t syncs = 0;
+  double sync_ms = 0.0;
 };
 
 namespace bf {
@@ -114,6 +121,7 @@ void pinned_release(double *p);
 void timer_begin(bf_ctx *c, int k, cudaEvent_t *start);
 void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes = 0.0);
 void timer_flush(bf_ctx *c);
+void sync(bf_ctx *c);  // counted, timed cudaStreamSynchronize
 
 #define BF_CUDA(x) ::bf::cuda_check((x), #x)
 #define BF_LAUNCH(c) ((c)->launches++)
@@ -130,6 +138,7 @@ void build_split(bf_ctx *c);                                            // k_spl
 void build_schur(bf_ctx *c);                                            // k_split.cu
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
+void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false);                 // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
 void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu

@@ -486,7 +486,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
       BF_CUDA(cudaGetLastError());
       int nU = 0;
       BF_CUDA(cudaMemcpyAsync(&nU, nU_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      BF_CUDA(cudaStreamSynchronize(c->stream));
+      sync(c);
       if (nU == 0) break;
       if (round > 10000) throw Error(BF_ERR_LIMIT, "PMIS did not terminate");
     }
@@ -550,6 +550,11 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.x = dalloc_t<double>(c, n);
     L.r = dalloc_t<double>(c, n);
     L.t = dalloc_t<double>(c, n);
+    tile_csr(c, L.A, k == 0);
+    if (k < h.nlev - 1) {
+      tile_csr(c, L.P);
+      tile_csr(c, L.R);
+    }
   }
   BF_CUDA(cudaGetLastError());
   Level &C = h.lv[l];
@@ -567,7 +572,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     BF_CUDA(cudaGetLastError());
     int hs = -1;
     BF_CUDA(cudaMemcpyAsync(&hs, sing, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    BF_CUDA(cudaStreamSynchronize(c->stream));
+    sync(c);
     dfree(c, sing);
     if (hs >= 0)
       throw Error(BF_ERR_COARSE_SINGULAR, std::string("coarsest matrix of hierarchy ") + std::to_string(which) +

@@ -1,0 +1,186 @@
+// k_csr_tma.cuh -- TMA-pipelined CSR kernel family for the V-cycle and the A_ps coupling.
+//
+// The matrix is cut into tiles of RPT consecutive rows (RPT per matrix, chosen at setup so
+// that a tile holds at most `cap` nonzeros).  A tile's (col, val) range is contiguous in
+// HBM, so one elected thread moves it into shared memory with two 1-D bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx, the TMA engine), double-buffered: while the CTA
+// computes tile i from stage i%2, the copy of tile i+grid is already in flight.  The CTA's
+// 256 threads then form the rows with G = 256/RPT lanes per row, gathering x through L1/L2,
+// and apply the fused epilogue (residual / smoother / restriction + seeding / prolongation).
+// Persistent grid: one wave of CTAs loops over the tiles.
+#pragma once
+#include "bf_internal.cuh"
+#include "k_spmv.cuh"
+
+#include <algorithm>
+
+namespace bf {
+
+constexpr int TMA_THREADS = 256;
+constexpr int TMA_STAGES = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// byte layout of one stage: [cols: 4*(cap+8) B][vals: 8*(cap+4) B], both 16-B aligned
+// (the aligned copy of a tile of `cap` nonzeros spans at most cap+6 ints / cap+2 doubles)
+__host__ __device__ inline int tma_col_bytes(int cap) { return ((4 * (cap + 8)) + 15) & ~15; }
+__host__ __device__ inline int tma_stage_bytes(int cap) { return tma_col_bytes(cap) + (((8 * (cap + 4)) + 15) & ~15); }
+
+template <int MODE, int G>
+__global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int ntiles, int cap,
+                                                         const int32_t *__restrict__ rp,
+                                                         const int32_t *__restrict__ ci,
+                                                         const double *__restrict__ v, const double *__restrict__ x,
+                                                         const double *__restrict__ b,
+                                                         const double *__restrict__ dinv, double *__restrict__ y,
+                                                         double *__restrict__ aux, double alpha, double beta,
+                                                         const double *__restrict__ dir) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[TMA_STAGES];
+  const int stage_bytes = tma_stage_bytes(cap);
+  const int cb = tma_col_bytes(cap);
+  int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < TMA_STAGES; s++) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer: issue the bulk copies of tile t into stage s
+  auto issue = [&](int t, int s) {
+    int r0 = t * rpt, r1 = min(r0 + rpt, n);
+    int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
+    int c0 = q0 & ~3, c1 = (q1 + 3) & ~3;  // 16-B aligned int32 range
+    int v0 = q0 & ~1, v1 = (q1 + 1) & ~1;  // 16-B aligned double range
+    unsigned char *base = smem_raw + s * stage_bytes;
+    uint32_t bc = 4u * (c1 - c0), bv = 8u * (v1 - v0);
+    mbar_expect_tx(&bars[s], bc + bv);
+    if (bc) tma_bulk_g2s(base, ci + c0, bc, &bars[s]);
+    if (bv) tma_bulk_g2s(base + cb, v + v0, bv, &bars[s]);
+  };
+
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  if (tid == 0) {
+    issue(t, 0);
+    if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, 1);
+  }
+  const int sub = tid % G;
+  for (int it = 0; t < ntiles; t += gridDim.x, it++) {
+    int s = it % TMA_STAGES;
+    int r0 = t * rpt;
+    int q0 = __ldg(rp + r0);
+    mbar_wait(&bars[s], (it / TMA_STAGES) & 1);
+    const unsigned char *base = smem_raw + s * stage_bytes;
+    const int32_t *sc = reinterpret_cast<const int32_t *>(base) - (q0 & ~3);
+    const double *sv = reinterpret_cast<const double *>(base + cb) - (q0 & ~1);
+    // rows of the tile in passes of TMA_THREADS/G rows; G lanes per row
+    for (int row_in_tile = tid / G; row_in_tile < ((rpt + (TMA_THREADS / G) - 1) / (TMA_THREADS / G)) * (TMA_THREADS / G);
+         row_in_tile += TMA_THREADS / G) {
+      int r = r0 + row_in_tile;
+      bool ok = row_in_tile < rpt && r < n;
+      int lo = ok ? __ldg(rp + r) : 0, hi = ok ? __ldg(rp + r + 1) : 0;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+      if (G > 1) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+      }
+      if (!ok || sub != 0) continue;
+      if (MODE == OP_SPMV) {
+        y[r] = acc;
+      } else if (MODE == OP_SPMV_X0) {
+        y[r] = acc;
+        aux[r] = beta * (acc * dinv[r]);
+      } else if (MODE == OP_RESID) {
+        y[r] = b[r] - acc;
+      } else if (MODE == OP_SUB_X0) {
+        double tt = b[r] - acc;
+        y[r] = tt;
+        aux[r] = beta * (tt * dinv[r]);
+      } else if (MODE == OP_SMOOTH) {
+        double dn = beta * ((b[r] - acc) * dinv[r]);
+        if (dir) dn += alpha * dir[r];
+        y[r] = x[r] + dn;
+        if (aux) aux[r] = dn;
+      } else if (MODE == OP_ADD) {
+        y[r] += acc;
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0 && t + TMA_STAGES * (int)gridDim.x < ntiles) issue(t + TMA_STAGES * gridDim.x, s);
+  }
+}
+
+// per-tile nonzero count -> max (setup helper)
+static __global__ void k_tile_max(int n, int rpt, const int32_t *__restrict__ rp, int *mx) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int r0 = t * rpt;
+  if (r0 >= n) return;
+  int r1 = min(r0 + rpt, n);
+  atomicMax(mx, rp[r1] - rp[r0]);
+}
+
+template <int MODE, int G>
+void launch_csr_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                    double *aux, double alpha, double beta, const double *dir) {
+  static int configured_smem = 0;
+  int smem = TMA_STAGES * tma_stage_bytes(A.cap);
+  if (smem > configured_smem) {
+    BF_CUDA(cudaFuncSetAttribute(k_csr_tma<MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured_smem = 200 * 1024;
+  }
+  int ntiles = (A.n + A.rpt - 1) / A.rpt;
+  int per_sm = std::max(1, std::min(8, (220 * 1024) / (smem + 1024)));
+  int grid = std::min(ntiles, c->num_sms * per_sm);
+  k_csr_tma<MODE, G><<<grid, TMA_THREADS, smem, c->stream>>>(A.n, A.rpt, ntiles, A.cap, A.rp, A.ci, A.v, x, b, dinv,
+                                                             y, aux, alpha, beta, dir);
+}
+
+template <int MODE>
+bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                double *aux, double alpha, double beta, const double *dir) {
+  if (A.cap <= 0) return false;
+  switch (A.g) {
+    case 1: launch_csr_tma<MODE, 1>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 2: launch_csr_tma<MODE, 2>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 4: launch_csr_tma<MODE, 4>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 8: launch_csr_tma<MODE, 8>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 16: launch_csr_tma<MODE, 16>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 32: launch_csr_tma<MODE, 32>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    default: return false;
+  }
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  return true;
+}
+
+}  // namespace bf

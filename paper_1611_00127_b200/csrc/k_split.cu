@@ -98,7 +98,7 @@ void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J) {
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   BF_CUDA(cudaMemcpyAsync(&herr, derr, sizeof herr, cudaMemcpyDeviceToHost, c->stream));
-  BF_CUDA(cudaStreamSynchronize(c->stream));
+  sync(c);
   dfree(c, raw);
   dfree(c, derr);
   if (herr.rp_bad != INT32_MAX)
@@ -189,7 +189,7 @@ void build_split(bf_ctx *c) {
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   BF_CUDA(cudaMemcpyAsync(&hz, zd, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  BF_CUDA(cudaStreamSynchronize(c->stream));
+  sync(c);
   dfree(c, zd);
   if (hz != INT32_MAX) throw Error(BF_ERR_ZERO_DIAG, "A_ss diagonal is zero at cell " + std::to_string(hz));
 }
@@ -278,7 +278,7 @@ void build_schur(bf_ctx *c) {
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   BF_CUDA(cudaMemcpyAsync(&h, ovf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  BF_CUDA(cudaStreamSynchronize(c->stream));
+  sync(c);
   dfree(c, ovf);
   if (h != INT32_MAX)
     throw Error(BF_ERR_LIMIT, "S~ row " + std::to_string(h) + " has more than " + std::to_string(SCHUR_CAP) +

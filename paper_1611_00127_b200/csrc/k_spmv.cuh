@@ -104,9 +104,14 @@ inline int lanes_for(const bf_ctx *c, const DCsr &A) {
 }
 
 template <int MODE>
+bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                double *aux, double alpha, double beta, const double *dir);
+
+template <int MODE>
 void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
             double *aux, double alpha, double beta, const double *dir) {
   if (A.n == 0) return;
+  if (c->use_tma && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   int G = lanes_for(c, A);
   int rows_per_block = (32 / G) * CSR_WARPS;
   int blocks = div_up(A.n, rows_per_block);
@@ -129,3 +134,5 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
 }
 
 }  // namespace bf
+
+#include "k_csr_tma.cuh"

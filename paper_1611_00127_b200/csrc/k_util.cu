@@ -21,7 +21,7 @@ int64_t exclusive_scan_i32(bf_ctx *c, const int32_t *counts, int32_t *out, int32
   c->launches += 2;
   int32_t total = 0;
   BF_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-  BF_CUDA(cudaStreamSynchronize(c->stream));
+  sync(c);
   dfree(c, t);
   dfree(c, padded);
   return total;
@@ -38,7 +38,7 @@ int64_t exclusive_scan_i64(bf_ctx *c, const int64_t *counts, int64_t *out, int64
   c->launches += 2;
   int64_t total = 0;
   BF_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-  BF_CUDA(cudaStreamSynchronize(c->stream));
+  sync(c);
   dfree(c, t);
   dfree(c, padded);
   return total;

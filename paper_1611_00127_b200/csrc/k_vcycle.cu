@@ -6,6 +6,7 @@
 #include "bf_internal.cuh"
 #include "k_spmv.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace bf {
@@ -47,6 +48,43 @@ __global__ void k_coarse_solve(int n, const double *__restrict__ lu, const int32
 __global__ void k_zero(int n, double *x) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = 0.0;
+}
+
+// choose the TMA tiling of a CSR matrix: ~2048 nonzeros per tile, 8..256 rows per tile
+// lanes per row: stencil-ordered fine-level rows -> 1 (lane-per-row gathers of consecutive
+// rows hit consecutive addresses); Galerkin rows -> several lanes reading adjacent sorted
+// columns of the same row (fewer distinct sectors per gather instruction)
+void tile_csr(bf_ctx *c, DCsr &A, bool stencil) {
+  A.rpt = 0;
+  A.cap = 0;
+  if (A.n == 0 || A.nnz == 0) return;
+  double mean = (double)A.nnz / A.n;
+  int g = 1;
+  if (!stencil) {
+    const char *e = getenv("BF_TMA_G");
+    double div = e ? atof(e) : 3.0;
+    while (g < 32 && 2 * g <= mean / div) g <<= 1;
+  }
+  A.g = g;
+  int rpt = 256;
+  while (rpt > 8 && rpt * mean > 2048.0) rpt >>= 1;
+  int *mx = dalloc_t<int>(c, 1);
+  for (;; rpt >>= 1) {
+    BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
+    int ntiles = (A.n + rpt - 1) / rpt;
+    k_tile_max<<<div_up(ntiles, 256), 256, 0, c->stream>>>(A.n, rpt, A.rp, mx);
+    BF_LAUNCH(c);
+    int h = 0;
+    BF_CUDA(cudaMemcpyAsync(&h, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (TMA_STAGES * tma_stage_bytes(h) <= 96 * 1024) {
+      A.rpt = rpt;
+      A.cap = std::max(h, 1);
+      break;
+    }
+    if (rpt == 8) break;  // rows too long for a staged tile: generic warp kernel
+  }
+  dfree(c, mx);
 }
 
 // beta of the first smoothing step from x = 0: x0 = beta b ./ dl1
