@@ -100,6 +100,8 @@ struct bf_ctx {
   int num_sms = 148;
   bool use_tma = true;
   double alloc_ms = 0.0;
+  double alg_bytes = 0.0;       // running algorithmic-bytes counter (csr_op, vector kernels)
+  double apply_bytes = 0.0;     // algorithmic bytes of one BF apply (set at graph capture)
   int64_t syncs = 0;
   double sync_ms = 0.0;
 };

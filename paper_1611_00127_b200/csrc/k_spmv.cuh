@@ -107,10 +107,27 @@ template <int MODE>
 bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir);
 
+// algorithmic bytes of one csr_op (each operand once: int32 index, f64 value; x counted once
+// per column); accumulated into c->alg_bytes so a captured BF apply knows its own traffic
+template <int MODE>
+double csr_op_bytes(const DCsr &A, bool has_dir, bool has_aux) {
+  double n = A.n, base = 12.0 * A.nnz + 4.0 * (A.n + 1) + 8.0 * A.m;
+  switch (MODE) {
+    case OP_SPMV: return base + 8 * n;
+    case OP_SPMV_X0: return base + 24 * n;
+    case OP_RESID: return base + 16 * n;
+    case OP_SUB_X0: return base + 32 * n;
+    case OP_SMOOTH: return base + 24 * n + (has_dir ? 8 * n : 0) + (has_aux ? 8 * n : 0);
+    case OP_ADD: return base + 16 * n;
+  }
+  return base;
+}
+
 template <int MODE>
 void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
             double *aux, double alpha, double beta, const double *dir) {
   if (A.n == 0) return;
+  c->alg_bytes += csr_op_bytes<MODE>(A, dir != nullptr, aux != nullptr);
   if (c->use_tma && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   int G = lanes_for(c, A);
   int rows_per_block = (32 / G) * CSR_WARPS;

@@ -147,6 +147,7 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   if (l == h.nlev - 1) {
     if (h.dense) {
       size_t smem = sizeof(double) * ((size_t)n * n + n);
+      c->alg_bytes += 8.0 * n * n + 4.0 * n + 16.0 * n;
       k_coarse_solve<<<1, 128, smem, c->stream>>>(n, h.lu, h.piv, L.b, L.x);
       BF_LAUNCH(c);
       BF_CUDA(cudaGetLastError());
@@ -220,6 +221,7 @@ void bf_apply(bf_ctx *c, const double *v, double *z) {
   int ip = c->var_order;
   Hier &hs = c->h[0], &hS = c->h[1];
   // Alg. 3 step 2: A_ss s = R_s r_k by one V-cycle
+  c->alg_bytes += 48.0 * n + 32.0 * n;  // split (v in; vp, vs, x0 out; dl1 in) + merge (p, s in; z out)
   k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, v, c->vp, hs.lv[0].b, hs.lv[0].d,
                                                      x0_beta(c->opt), hs.lv[0].x);
   BF_LAUNCH(c);
@@ -247,6 +249,7 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     cudaStream_t user = c->stream;
     c->stream = c->cap_stream;
     int64_t l0 = c->launches;
+    double b0 = c->alg_bytes;
     BF_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     try {
       bf_apply(c, v, z);
@@ -261,6 +264,7 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     BF_CUDA(cudaStreamEndCapture(c->cap_stream, &g));
     c->stream = user;
     c->apply_graph_kernels = c->launches - l0;
+    c->apply_bytes = c->alg_bytes - b0;
     c->launches = l0;
     BF_CUDA(cudaGraphInstantiate(&c->apply_exec, g, 0));
     // locate the split kernel node (the only node that reads v)
@@ -307,7 +311,10 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
   cudaKernelNodeParams p = c->split_params;
   p.kernelParams = args;
   BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_split_node, &p));
+  cudaEvent_t t0;
+  timer_begin(c, 2, &t0);
   BF_CUDA(cudaGraphLaunch(c->apply_exec, c->stream));
+  timer_end(c, 2, t0, c->apply_bytes);
   c->launches += c->apply_graph_kernels;
 }
 

@@ -1,0 +1,65 @@
+"""Parity at BASELINE.json's full size, in the configuration bench.py times: C3 (128^3,
+4.19M DOF), default options, device-resident J.  Hierarchies bit-exact at every level,
+SpMV <= 1e-12, BF apply <= 1e-10, and 30 GMRES iterations (forced count) <= 1e-6 per field.
+The oracle (1 thread) needs ~1 min here."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+import oracle
+from workload import make_system, seeded_vector
+from gpu_util import torch_dev, gpu_solver, csr_equal
+
+
+@pytest.fixture(scope="module")
+def c3():
+    prob, J, rhs = make_system(3)
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    return prob, J, rhs, g, o
+
+
+def test_c3_hierarchy_bit_exact(c3):
+    prob, J, rhs, g, o = c3
+    for k, name in enumerate(("App", "Aps", "Asp", "Ass", "S")):
+        pat, val = csr_equal(g.block(k), o.matrix(name))
+        assert pat and val, name
+    for which in (0, 1):
+        assert g.num_levels(which) == o.nlev(which)
+        for l in range(o.nlev(which)):
+            G, O = g.level(which, l), o.level(which, l)
+            pat, val = csr_equal(G["A"], O["A"])
+            assert pat and val, (which, l)
+            if l < o.nlev(which) - 1:
+                assert np.array_equal(G["cf"], O["cf"]), (which, l)
+                pat, val = csr_equal(G["P"], O["P"])
+                assert pat and val, (which, l)
+
+
+def test_c3_spmv_and_apply(c3):
+    prob, J, rhs, g, o = c3
+    N = 2 * J.n
+    x = seeded_vector(N, 21)
+    y = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.spmv(torch_dev(x), y)
+    yo = o.spmv(x)
+    assert np.linalg.norm(y.cpu().numpy() - yo) <= 1e-12 * np.linalg.norm(yo)
+    z = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(x), z)
+    zo = o.apply(x)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+
+
+def test_c3_gmres_forced_iterations(c3):
+    prob, J, rhs, g, o = c3
+    k = 30
+    ro = o.gmres(rhs, tol=0.0, restart=30, maxit=k)
+    x = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=0.0, restart=30, maxit=k)
+    assert r["iters"] == ro["iters"] == k
+    xg = x.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+    assert np.allclose(r["hist"], ro["hist"], rtol=1e-6, atol=0)
