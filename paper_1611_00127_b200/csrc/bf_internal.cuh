@@ -25,6 +25,7 @@ struct DCsr {
   int64_t nnz = 0;
   int32_t rpt = 0, cap = 0;  // TMA tiling: rows per tile, max nonzeros per tile (0: not tiled)
   int32_t g = 1;             // lanes per row in the TMA kernel
+  int32_t stages = 2;        // TMA pipeline depth
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
 };
@@ -42,7 +43,9 @@ struct Hier {
   Level lv[BF_MAXL];
   double *lu = nullptr;  // nL x nL row-major LU (unit lower L below the diagonal)
   int32_t *piv = nullptr;
+  double *inv = nullptr;  // explicit inverse of the coarsest matrix (nL x nL, row-major)
   int32_t nL = 0;
+  int tail = -1;          // first level handled by the single-CTA tail kernel (-1: none)
   bool dense = false;  // coarsest level solved by LU (else 4 l1-Jacobi sweeps)
 };
 
@@ -140,6 +143,7 @@ void build_split(bf_ctx *c);                                            // k_spl
 void build_schur(bf_ctx *c);                                            // k_split.cu
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
+void plan_tail(bf_ctx *c, Hier &h);                                     // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false);                 // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------

@@ -371,7 +371,7 @@ static void spgemm(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
 // ------------------------------------------------------------------------------- coarse LU
 // dense LU with partial pivoting (tie -> lowest row index), one CTA, matrix staged in smem.
 // Singular if |pivot| <= 1e-14 max|a|: *sing = pivot index.
-__global__ void k_coarse_lu(DCsr A, double *lu, int32_t *piv, int *sing) {
+__global__ void k_coarse_lu(DCsr A, double *lu, int32_t *piv, double *inv, int *sing) {
   extern __shared__ double sm[];
   int n = A.n;
   __shared__ double amax_s;
@@ -415,6 +415,29 @@ __global__ void k_coarse_lu(DCsr A, double *lu, int32_t *piv, int *sing) {
     __syncthreads();
   }
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) lu[e] = sm[e];
+  __syncthreads();
+  // explicit inverse (column j solved by thread j) so that the solve phase is one dense
+  // matvec instead of 2n dependent substitution steps
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double *col = inv + (size_t)n * n;  // scratch column block: [n][blockDim] after inv
+    double *y = col + (size_t)j * n;
+    for (int i = 0; i < n; i++) y[i] = (i == j) ? 1.0 : 0.0;
+    for (int k = 0; k < n; k++) {
+      int p = piv[k];
+      if (p != k) {
+        double t = y[k];
+        y[k] = y[p];
+        y[p] = t;
+      }
+    }
+    for (int k = 0; k < n; k++)
+      for (int i = k + 1; i < n; i++) y[i] -= sm[i * n + k] * y[k];
+    for (int k = n - 1; k >= 0; k--) {
+      y[k] = y[k] / sm[k * n + k];
+      for (int i = 0; i < k; i++) y[i] -= sm[i * n + k] * y[k];
+    }
+    for (int i = 0; i < n; i++) inv[(size_t)i * n + j] = y[i];
+  }
 }
 
 // ------------------------------------------------------------------------------- driver
@@ -434,6 +457,7 @@ void free_hierarchy(bf_ctx *c, Hier &h) {
   }
   dfree(c, h.lu);
   dfree(c, h.piv);
+  dfree(c, h.inv);
   h = Hier();
 }
 
@@ -564,10 +588,11 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     int nL = C.A.n;
     h.lu = dalloc_t<double>(c, (size_t)nL * nL);
     h.piv = dalloc_t<int32_t>(c, nL);
+    h.inv = dalloc_t<double>(c, (size_t)2 * nL * nL);  // inverse + per-column scratch
     int *sing = dalloc_t<int>(c, 1);
     size_t smem = sizeof(double) * nL * nL;
     BF_CUDA(cudaFuncSetAttribute(k_coarse_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    k_coarse_lu<<<1, 256, smem, c->stream>>>(C.A, h.lu, h.piv, sing);
+    k_coarse_lu<<<1, 256, smem, c->stream>>>(C.A, h.lu, h.piv, h.inv, sing);
     BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
     int hs = -1;
@@ -579,6 +604,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
                                               " (n=" + std::to_string(nL) + ") singular at pivot " +
                                               std::to_string(hs));
   }
+  plan_tail(c, h);
 }
 
 }  // namespace bf

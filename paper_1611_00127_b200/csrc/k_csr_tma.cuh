@@ -17,7 +17,8 @@
 namespace bf {
 
 constexpr int TMA_THREADS = 256;
-constexpr int TMA_STAGES = 2;
+constexpr int TMA_STAGES = 2;      // stages of the tiling heuristic's smem budget
+constexpr int TMA_MAX_STAGES = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -53,7 +54,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __host__ __device__ inline int tma_col_bytes(int cap) { return ((4 * (cap + 8)) + 15) & ~15; }
 __host__ __device__ inline int tma_stage_bytes(int cap) { return tma_col_bytes(cap) + (((8 * (cap + 4)) + 15) & ~15); }
 
-template <int MODE, int G>
+template <int MODE, int G, int ST>
 __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int ntiles, int cap,
                                                          const int32_t *__restrict__ rp,
                                                          const int32_t *__restrict__ ci,
@@ -63,12 +64,12 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
                                                          double *__restrict__ aux, double alpha, double beta,
                                                          const double *__restrict__ dir) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bars[TMA_STAGES];
+  __shared__ __align__(8) uint64_t bars[ST];
   const int stage_bytes = tma_stage_bytes(cap);
   const int cb = tma_col_bytes(cap);
   int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < TMA_STAGES; s++) mbar_init(&bars[s], 1);
+    for (int s = 0; s < ST; s++) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -88,16 +89,14 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
 
   int t = blockIdx.x;
   if (t >= ntiles) return;
-  if (tid == 0) {
-    issue(t, 0);
-    if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, 1);
-  }
+  if (tid == 0)
+    for (int s = 0; s < ST && t + s * (int)gridDim.x < ntiles; s++) issue(t + s * gridDim.x, s);
   const int sub = tid % G;
   for (int it = 0; t < ntiles; t += gridDim.x, it++) {
-    int s = it % TMA_STAGES;
+    int s = it % ST;
     int r0 = t * rpt;
     int q0 = __ldg(rp + r0);
-    mbar_wait(&bars[s], (it / TMA_STAGES) & 1);
+    mbar_wait(&bars[s], (it / ST) & 1);
     const unsigned char *base = smem_raw + s * stage_bytes;
     const int32_t *sc = reinterpret_cast<const int32_t *>(base) - (q0 & ~3);
     const double *sv = reinterpret_cast<const double *>(base + cb) - (q0 & ~1);
@@ -136,7 +135,7 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
       }
     }
     __syncthreads();  // every thread is done with stage s
-    if (tid == 0 && t + TMA_STAGES * (int)gridDim.x < ntiles) issue(t + TMA_STAGES * gridDim.x, s);
+    if (tid == 0 && t + ST * (int)gridDim.x < ntiles) issue(t + ST * gridDim.x, s);
   }
 }
 
@@ -149,20 +148,30 @@ static __global__ void k_tile_max(int n, int rpt, const int32_t *__restrict__ rp
   atomicMax(mx, rp[r1] - rp[r0]);
 }
 
-template <int MODE, int G>
-void launch_csr_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
-                    double *aux, double alpha, double beta, const double *dir) {
-  static int configured_smem = 0;
-  int smem = TMA_STAGES * tma_stage_bytes(A.cap);
-  if (smem > configured_smem) {
-    BF_CUDA(cudaFuncSetAttribute(k_csr_tma<MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured_smem = 200 * 1024;
+template <int MODE, int G, int ST>
+void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                       double *aux, double alpha, double beta, const double *dir) {
+  static bool configured = false;
+  if (!configured) {
+    BF_CUDA(cudaFuncSetAttribute(k_csr_tma<MODE, G, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
   }
+  int smem = ST * tma_stage_bytes(A.cap);
   int ntiles = (A.n + A.rpt - 1) / A.rpt;
   int per_sm = std::max(1, std::min(8, (220 * 1024) / (smem + 1024)));
   int grid = std::min(ntiles, c->num_sms * per_sm);
-  k_csr_tma<MODE, G><<<grid, TMA_THREADS, smem, c->stream>>>(A.n, A.rpt, ntiles, A.cap, A.rp, A.ci, A.v, x, b, dinv,
-                                                             y, aux, alpha, beta, dir);
+  k_csr_tma<MODE, G, ST><<<grid, TMA_THREADS, smem, c->stream>>>(A.n, A.rpt, ntiles, A.cap, A.rp, A.ci, A.v, x, b,
+                                                                 dinv, y, aux, alpha, beta, dir);
+}
+
+template <int MODE, int G>
+void launch_csr_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                    double *aux, double alpha, double beta, const double *dir) {
+  switch (A.stages) {
+    case 3: launch_csr_tma_st<MODE, G, 3>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    case 4: launch_csr_tma_st<MODE, G, 4>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+    default: launch_csr_tma_st<MODE, G, 2>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
+  }
 }
 
 template <int MODE>

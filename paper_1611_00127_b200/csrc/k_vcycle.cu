@@ -11,38 +11,136 @@
 
 namespace bf {
 
-// forward/back substitution with the LU of the coarsest matrix, one CTA, staged in smem
-__global__ void k_coarse_solve(int n, const double *__restrict__ lu, const int32_t *__restrict__ piv,
-                               const double *__restrict__ b, double *__restrict__ x) {
-  extern __shared__ double sm[];
-  double *L = sm;          // n*n
-  double *y = sm + n * n;  // n
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) L[e] = lu[e];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[i];
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int k = 0; k < n; k++) {
-      int p = piv[k];
-      if (p != k) {
-        double t = y[k];
-        y[k] = y[p];
-        y[p] = t;
+// coarsest-level solve x = A_L^-1 b with the inverse formed at setup from the pivoted LU
+// (one CTA, thread per row; replaces 2 n dependent substitution steps)
+__global__ void k_coarse_inv(int n, const double *__restrict__ inv, const double *__restrict__ b,
+                             double *__restrict__ x) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < n; j++) s += inv[(size_t)i * n + j] * b[j];
+    x[i] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Single-CTA tail of the V-cycle: all levels from h.tail down to the coarsest (each with at
+// most TAIL_NNZ nonzeros, L2-resident) in ONE kernel, __syncthreads between the steps,
+// instead of ~4 launches per level (l1-Jacobi V(1,1), the default configuration).
+// ----------------------------------------------------------------------------------------
+constexpr int TAIL_MAXL = 12;
+constexpr int TAIL_NNZ = 3000;
+constexpr int TAIL_THREADS = 1024;
+
+struct TailLevel {
+  int n;
+  const int32_t *Arp, *Aci, *Prp, *Pci, *Rrp, *Rci;
+  const double *Av, *Pv, *Rv, *d;
+  double *b, *x, *r, *t;
+};
+struct TailParams {
+  int nl;  // tail levels including the coarsest
+  double beta;
+  const double *inv;
+  TailLevel lv[TAIL_MAXL];
+};
+
+// warp-per-row CSR reduction: returns sum_j a_ij x_j on lane 0 of the warp
+__device__ __forceinline__ double warp_row(const int32_t *rp, const int32_t *ci, const double *v,
+                                           const double *x, int r, int lane) {
+  double s = 0.0;
+  for (int q = rp[r] + lane; q < rp[r + 1]; q += 32) s += v[q] * x[ci[q]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = TAIL_THREADS / 32;
+  for (int l = 0; l < p.nl - 1; l++) {
+    const TailLevel &L = p.lv[l];
+    for (int r = warp; r < L.n; r += nw) {  // r = b - A x0
+      double s = warp_row(L.Arp, L.Aci, L.Av, L.x, r, lane);
+      if (lane == 0) L.r[r] = L.b[r] - s;
+    }
+    __syncthreads();
+    const TailLevel &C = p.lv[l + 1];
+    for (int r = warp; r < C.n; r += nw) {  // b_c = R r ; x0_c = beta b_c ./ dl1_c
+      double s = warp_row(L.Rrp, L.Rci, L.Rv, L.r, r, lane);
+      if (lane == 0) {
+        C.b[r] = s;
+        C.x[r] = p.beta * (s * C.d[r]);
       }
     }
-  __syncthreads();
-  for (int k = 0; k < n; k++) {  // L (unit) forward, column oriented
-    double yk = y[k];
-    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) y[i] -= L[i * n + k] * yk;
     __syncthreads();
   }
-  for (int k = n - 1; k >= 0; k--) {  // U backward
-    if (threadIdx.x == 0) y[k] = y[k] / L[k * n + k];
-    __syncthreads();
-    double yk = y[k];
-    for (int i = threadIdx.x; i < k; i += blockDim.x) y[i] -= L[i * n + k] * yk;
+  {  // coarsest: x = A_L^-1 b
+    const TailLevel &L = p.lv[p.nl - 1];
+    for (int i = threadIdx.x; i < L.n; i += TAIL_THREADS) {
+      double s = 0.0;
+      for (int j = 0; j < L.n; j++) s += p.inv[(size_t)i * L.n + j] * L.b[j];
+      L.x[i] = s;
+    }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = y[i];
+  for (int l = p.nl - 2; l >= 0; l--) {
+    const TailLevel &L = p.lv[l];
+    const TailLevel &C = p.lv[l + 1];
+    for (int r = warp; r < L.n; r += nw) {  // x += P e
+      double s = warp_row(L.Prp, L.Pci, L.Pv, C.x, r, lane);
+      if (lane == 0) L.x[r] += s;
+    }
+    __syncthreads();
+    for (int r = warp; r < L.n; r += nw) {  // t = x + (b - A x) ./ dl1
+      double s = warp_row(L.Arp, L.Aci, L.Av, L.x, r, lane);
+      if (lane == 0) L.t[r] = L.x[r] + (L.b[r] - s) * L.d[r];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < L.n; i += TAIL_THREADS) L.x[i] = L.t[i];
+    __syncthreads();
+  }
+}
+
+// decide where the tail starts (default smoother configuration only)
+void plan_tail(bf_ctx *c, Hier &h) {
+  const bf_options &o = c->opt;
+  h.tail = -1;
+  if (getenv("BF_NO_TAIL") || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  const char *e = getenv("BF_TAIL_NNZ");
+  int64_t lim = e ? atoll(e) : TAIL_NNZ;
+  int l = h.nlev - 1;
+  while (l - 1 >= 0 && h.lv[l - 1].A.nnz <= lim && h.nlev - (l - 1) <= TAIL_MAXL) l--;
+  if (l < h.nlev - 1) h.tail = l;
+}
+
+static void launch_tail(bf_ctx *c, Hier &h) {
+  TailParams p;
+  p.nl = h.nlev - h.tail;
+  p.beta = 1.0;
+  p.inv = h.inv;
+  for (int k = 0; k < p.nl; k++) {
+    Level &L = h.lv[h.tail + k];
+    TailLevel &T = p.lv[k];
+    T.n = L.A.n;
+    T.Arp = L.A.rp;
+    T.Aci = L.A.ci;
+    T.Av = L.A.v;
+    T.Prp = L.P.rp;
+    T.Pci = L.P.ci;
+    T.Pv = L.P.v;
+    T.Rrp = L.R.rp;
+    T.Rci = L.R.ci;
+    T.Rv = L.R.v;
+    T.d = L.d;
+    T.b = L.b;
+    T.x = L.x;
+    T.r = L.r;
+    T.t = L.t;
+    c->alg_bytes += 2 * (12.0 * L.A.nnz + 4.0 * L.A.n) + 2 * (12.0 * L.P.nnz + 4.0 * L.A.n) + 80.0 * L.A.n;
+  }
+  c->alg_bytes += 8.0 * h.nL * h.nL;
+  k_vcycle_tail<<<1, TAIL_THREADS, 0, c->stream>>>(p);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
 }
 
 __global__ void k_zero(int n, double *x) {
@@ -50,7 +148,7 @@ __global__ void k_zero(int n, double *x) {
   if (i < n) x[i] = 0.0;
 }
 
-// choose the TMA tiling of a CSR matrix: ~2048 nonzeros per tile, 8..256 rows per tile
+// choose the TMA tiling of a CSR matrix: ~1024 nonzeros per tile, 8..256 rows per tile
 // lanes per row: stencil-ordered fine-level rows -> 1 (lane-per-row gathers of consecutive
 // rows hit consecutive addresses); Galerkin rows -> several lanes reading adjacent sorted
 // columns of the same row (fewer distinct sectors per gather instruction)
@@ -66,8 +164,14 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil) {
     while (g < 32 && 2 * g <= mean / div) g <<= 1;
   }
   A.g = g;
+  const char *es = getenv("BF_TMA_STAGES");
+  A.stages = es ? atoi(es) : 2;
+  const char *et = getenv("BF_TMA_TILE");
+  double tile = et ? atof(et) : 1024.0;  // measured: 1024 beats 2048 (more CTAs per SM for the gathers)
   int rpt = 256;
-  while (rpt > 8 && rpt * mean > 2048.0) rpt >>= 1;
+  // ~1024 nonzeros per tile, but at least one full pass of the CTA (256/g rows) so that no
+  // thread idles (stencil rows, g = 1, always take 256-row tiles)
+  while (rpt > 8 && rpt > TMA_THREADS / g && rpt * mean > tile) rpt >>= 1;
   int *mx = dalloc_t<int>(c, 1);
   for (;; rpt >>= 1) {
     BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
@@ -77,7 +181,7 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil) {
     int h = 0;
     BF_CUDA(cudaMemcpyAsync(&h, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    if (TMA_STAGES * tma_stage_bytes(h) <= 96 * 1024) {
+    if (A.stages * tma_stage_bytes(h) <= 110 * 1024) {
       A.rpt = rpt;
       A.cap = std::max(h, 1);
       break;
@@ -144,11 +248,14 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   Level &L = h.lv[l];
   int n = L.A.n;
   const bf_options &o = c->opt;
+  if (l == h.tail) {
+    launch_tail(c, h);
+    return;
+  }
   if (l == h.nlev - 1) {
     if (h.dense) {
-      size_t smem = sizeof(double) * ((size_t)n * n + n);
-      c->alg_bytes += 8.0 * n * n + 4.0 * n + 16.0 * n;
-      k_coarse_solve<<<1, 128, smem, c->stream>>>(n, h.lu, h.piv, L.b, L.x);
+      c->alg_bytes += 8.0 * n * n + 16.0 * n;
+      k_coarse_inv<<<1, 128, 0, c->stream>>>(n, h.inv, L.b, L.x);
       BF_LAUNCH(c);
       BF_CUDA(cudaGetLastError());
     } else {  // stalled coarsening: 4 l1-Jacobi sweeps from zero (x0 = b ./ dl1 is the first)
