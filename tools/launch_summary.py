@@ -9,10 +9,11 @@ def summarise(path, top=45, title=""):
     hdr = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     H = rows[hdr]
     ki, mi, ui = H.index("Kernel Name"), H.index("Metric Value"), H.index("Metric Unit")
+    mn = H.index("Metric Name") if "Metric Name" in H else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for r in rows[hdr + 1:]:
-        if len(r) <= mi:
+        if len(r) <= mi or (mn is not None and r[mn] != "gpu__time_duration.sum"):
             continue
         v = float(r[mi].replace(",", ""))
         u = r[ui]
