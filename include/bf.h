@@ -112,6 +112,18 @@ bf_status bf_solve(bf_handle h, const double *rhs, double *x, double tol, int32_
                    int32_t maxit, int32_t vec_mem, int32_t *iters, double *res_hist,
                    int32_t *converged, double *final_true_relres, void *cuda_stream);
 
+/* New Jacobian VALUES on the setup's sparsity pattern (same row_ptr/col_idx, block_order,
+ * var_order), e.g. the next Newton iterate J(u_{k+1}).  Setup reuse (SURVEY
+ * 8(f) NEXT-1, reading R16 "frozen coarse hierarchy"): the field split, S~ and the FINEST
+ * level of both AMG hierarchies (matrix, l1 diagonal) are rebuilt from the new values; the
+ * coarse levels (C/F splits, P_l, R_l, A_l for l >= 1, the coarse LU) are kept from the last
+ * bf_setup.  A hierarchy that has a single level is rebuilt completely.
+ *   vals: [4*nnzb]; mem 0 = host pointer, 1 = device pointer.
+ * Errors as bf_setup (BF_ERR_NONFINITE, BF_ERR_ZERO_DIAG naming the cell, ...); on error the
+ * handle keeps its previous state only if the error was detected before any rebuild
+ * (validation errors), otherwise it must be destroyed. */
+bf_status bf_update(bf_handle h, const double *vals, int32_t mem, void *cuda_stream);
+
 /* Free all device memory of the handle (NULL is a no-op). */
 bf_status bf_destroy(bf_handle h);
 

@@ -54,7 +54,7 @@ class AMGs(C.Structure):
 
 
 class BFs(C.Structure):
-    _fields_ = [("n", C.c_int32), ("var_order", C.c_int32),
+    _fields_ = [("n", C.c_int32), ("var_order", C.c_int32), ("block_order", C.c_int32),
                 ("brp", C.POINTER(C.c_int64)), ("bci", C.POINTER(C.c_int32)), ("bv", C.POINTER(C.c_double)),
                 ("App", CSRs), ("Aps", CSRs), ("Asp", CSRs), ("Ass", CSRs), ("S", CSRs),
                 ("dss", C.POINTER(C.c_double)), ("hss", AMGs), ("hS", AMGs), ("opt", Options)]
@@ -91,6 +91,7 @@ def lib():
         L.or_csr_free.argtypes = [P(CSRs)]
         L.or_bf_setup.argtypes = [C.c_int32, lp, ip, dp, C.c_int32, C.c_int32, P(Options), P(P(BFs))]
         L.or_bf_free.argtypes = [P(BFs)]
+        L.or_bf_update.argtypes = [P(BFs), dp]
         L.or_bf_apply.argtypes = [P(BFs), dp, dp]
         L.or_bf_spmv.argtypes = [P(BFs), dp, dp]
         L.or_gmres.argtypes = [P(BFs), dp, dp, C.c_double, C.c_int32, C.c_int32, ip, dp, ip, dp]
@@ -352,6 +353,14 @@ class BF:
             lib().or_bf_free(self.ptr)
         except Exception:
             pass
+
+    def update(self, J, block_order=0):
+        """New values on the same pattern (frozen coarse hierarchy, reading R16)."""
+        rp, ci, v = _bsr_arrays(J, block_order)
+        self._keep_vals = v
+        st = lib().or_bf_update(self.ptr, _p(v, C.c_double))
+        if st:
+            raise RuntimeError(err())
 
     @property
     def s(self) -> BFs:

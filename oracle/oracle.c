@@ -649,6 +649,7 @@ int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
   or_bf *b = (or_bf *)xcalloc(1, sizeof(or_bf));
   b->n = n;
   b->var_order = var_order;
+  b->block_order = block_order;
   b->opt = *o;
   /* canonical copy of J for the SpMV: (p,s) row-major */
   int64_t nnzb = rp[n];
@@ -669,6 +670,41 @@ int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
   st = or_amg_setup(&b->S, o, &b->hS);
   if (st) { or_bf_free(b); return st; }
   *out = b;
+  return 0;
+}
+
+/* Setup reuse across Newton steps (reading R16 "frozen coarse
+ * hierarchy"): new Jacobian values on the same BSR pattern.  The split, S~ and the finest
+ * level of both hierarchies (A_0 and its l1 diagonal) are rebuilt from the new values; the
+ * coarse levels (C/F, P, R, A_l for l >= 1, coarse LU) are kept.  A hierarchy with a single
+ * level is set up again. */
+int or_bf_update(or_bf *b, const double *vals) {
+  int32_t n = b->n;
+  int64_t nnzb = b->brp[n];
+  for (int64_t q = 0; q < nnzb; q++)
+    for (int r = 0; r < 2; r++)
+      for (int c = 0; c < 2; c++)
+        b->bv[4 * q + 2 * r + c] = vals[4 * q + blk_index(b->block_order, b->var_order, r, c)];
+  or_csr_free(&b->App); or_csr_free(&b->Aps); or_csr_free(&b->Asp); or_csr_free(&b->Ass);
+  or_csr_free(&b->S);
+  int st = or_split(n, b->brp, b->bci, vals, b->block_order, b->var_order, &b->App, &b->Aps, &b->Asp, &b->Ass,
+                    b->dss);
+  if (st) return st;
+  or_schur(&b->App, &b->Aps, &b->Asp, b->dss, b->opt.schur_as_printed, &b->S);
+  or_amg *hs[2] = {&b->hss, &b->hS};
+  const or_csr *A0[2] = {&b->Ass, &b->S};
+  for (int k = 0; k < 2; k++) {
+    or_amg *h = hs[k];
+    if (h->nlev <= 1) {
+      or_amg_free(h);
+      st = or_amg_setup(A0[k], &b->opt, h);
+      if (st) return st;
+      continue;
+    }
+    or_csr_free(&h->A[0]);
+    csr_copy(A0[k], &h->A[0]);
+    or_l1diag(&h->A[0], h->dl1[0]);
+  }
   return 0;
 }
 

@@ -55,6 +55,7 @@ typedef struct {
 typedef struct {
   int32_t n;                      /* cells */
   int32_t var_order;
+  int32_t block_order;
   /* the input Jacobian (BSR2 in canonical row-major (p,s) order) */
   int64_t *brp; int32_t *bci; double *bv;
   or_csr App, Aps, Asp, Ass, S;   /* field split and S~ */
@@ -96,6 +97,7 @@ void or_csr_free(or_csr *A);
 int  or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
                  int32_t block_order, int32_t var_order, const or_options *o, or_bf **out);
 void or_bf_free(or_bf *b);
+int  or_bf_update(or_bf *b, const double *vals);
 void or_bf_apply(const or_bf *b, const double *v, double *z);
 void or_bf_spmv(const or_bf *b, const double *x, double *y);
 int  or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t restart,

@@ -22,7 +22,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE
           5: "BF_ERR_COARSE_SINGULAR", 6: "BF_ERR_CUDA", 7: "BF_ERR_OOM", 8: "BF_ERR_LIMIT"}
 
 # every symbol declared in include/bf.h
-EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_destroy", "bf_last_error", "bf_spmv",
+EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_update", "bf_destroy", "bf_last_error", "bf_spmv",
            "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_block",
            "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
 
@@ -58,6 +58,7 @@ def _load():
     L.bf_default_options.argtypes = [P(bf_options)]
     L.bf_setup.argtypes = [P(bf_bsr2), P(bf_options), vp, P(vp)]
     L.bf_solve.argtypes = [vp, vp, vp, C.c_double, i32, i32, i32, P(i32), dp, P(i32), dp, vp]
+    L.bf_update.argtypes = [vp, vp, i32, vp]
     L.bf_destroy.argtypes = [vp]
     L.bf_last_error.argtypes = [vp]
     L.bf_last_error.restype = C.c_char_p
@@ -132,6 +133,12 @@ def bf_setup(row_ptr, col_idx, vals, dims, block_order=0, var_order=0, opt=None,
     st = lib.bf_setup(C.byref(J), C.byref(opt) if opt is not None else None, _stream(stream), C.byref(h))
     _check(st, None)
     return h
+
+
+def bf_update(h, vals, stream=None):
+    """New Jacobian values on the setup's pattern (frozen coarse hierarchy, R16)."""
+    v, m = _ptr(vals)
+    _check(lib.bf_update(h, v, m, _stream(stream)), h)
 
 
 def bf_destroy(h):
@@ -253,6 +260,9 @@ class BFSolver:
         self.opt = bf_default_options(**opts)
         self.h = bf_setup(row_ptr, col_idx, vals, dims, block_order, var_order, self.opt, stream)
         self.n = dims[0] * dims[1] * dims[2]
+
+    def update(self, vals, stream=None):
+        bf_update(self.h, vals, stream)
 
     def solve(self, rhs, x, tol=1e-8, restart=30, maxit=500, stream=None):
         return bf_solve(self.h, rhs, x, tol, restart, maxit, True, stream)

@@ -303,6 +303,29 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
   return BF_OK;
 }
 
+bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) {
+  if (!c || !vals || (mem != 0 && mem != 1)) {
+    if (c) c->err = "bf_update: vals must be non-NULL and mem 0|1";
+    return BF_ERR_ARG;
+  }
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  c->err.clear();
+  reingest_values(c, vals, mem);  // validation first: the handle is untouched on BF_ERR_NONFINITE
+  drop_apply_graph(c);
+  for (int b = 0; b < 5; b++) free_csr(c, c->blk[b]);
+  dfree(c, c->dss);
+  c->dss = nullptr;
+  build_split(c);
+  build_schur(c);
+  tile_csr(c, c->blk[1]);
+  refresh_finest(c, 0, c->blk[3]);
+  refresh_finest(c, 1, c->blk[4]);
+  sync(c);
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
 bf_status bf_destroy(bf_handle h) {
   destroy_ctx(h);
   return BF_OK;

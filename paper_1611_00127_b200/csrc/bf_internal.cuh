@@ -72,6 +72,7 @@ struct bf_ctx {
   int32_t n = 0;  // cells
   int64_t nnzb = 0;
   int32_t var_order = 0;
+  int32_t block_order = 0;
   int32_t *brp = nullptr, *bci = nullptr;
   double *bv = nullptr;  // canonical (p,s) row-major blocks
   bf::DCsr blk[5];       // A_pp, A_ps, A_sp, A_ss, S~
@@ -140,6 +141,9 @@ void sort_pairs_u64_f64(bf_ctx *c, uint64_t *keys, double *vals, int64_t count, 
 // ---- setup kernels -----------------------------------------------------------------
 void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J);                 // k_split.cu
 void build_split(bf_ctx *c);                                            // k_split.cu
+void reingest_values(bf_ctx *c, const double *vals, int mem);            // k_split.cu
+void refresh_finest(bf_ctx *c, int which, const DCsr &A0);              // k_amg_setup.cu
+void drop_apply_graph(bf_ctx *c);                                       // k_vcycle.cu
 void build_schur(bf_ctx *c);                                            // k_split.cu
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);

@@ -607,4 +607,28 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   plan_tail(c, h);
 }
 
+// Setup reuse (bf_update, reading R16): replace the finest matrix of hierarchy `which` by
+// A0 and refresh its l1 diagonal, inverse diagonal and tiling; coarse levels are kept.
+void refresh_finest(bf_ctx *c, int which, const DCsr &A0) {
+  Hier &h = c->h[which];
+  if (h.nlev <= 1) {  // the finest level is the coarsest: rebuild (dense LU of the new matrix)
+    free_hierarchy(c, h);
+    build_hierarchy(c, which, A0);
+    return;
+  }
+  Level &L = h.lv[0];
+  free_csr(c, L.A);
+  copy_csr(c, A0, L.A);
+  int n = L.A.n;
+  double *diag = dalloc_t<double>(c, n);
+  k_diag<<<div_up(n, 256), 256, 0, c->stream>>>(L.A, diag);
+  k_l1diag<<<div_up(n, 256), 256, 0, c->stream>>>(L.A, diag, L.dl1);
+  k_recip<<<div_up(n, 256), 256, 0, c->stream>>>(n, L.dl1, L.d);
+  c->launches += 3;
+  BF_CUDA(cudaGetLastError());
+  dfree(c, diag);
+  tile_csr(c, L.A, true);
+  plan_tail(c, h);
+}
+
 }  // namespace bf

@@ -81,6 +81,7 @@ void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J) {
   c->n = n;
   c->nnzb = nnzb;
   c->var_order = J->var_order;
+  c->block_order = J->block_order;
   c->brp = dalloc_t<int32_t>(c, (size_t)n + 1);
   c->bci = dalloc_t<int32_t>(c, (size_t)nnzb);
   c->bv = dalloc_t<double>(c, (size_t)nnzb * 4);
@@ -109,6 +110,31 @@ void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J) {
     throw Error(BF_ERR_PATTERN, "diagonal block missing in row " + std::to_string(herr.diag_bad));
   if (herr.nonfinite != (long long)INT64_MAX)
     throw Error(BF_ERR_NONFINITE, "non-finite Jacobian value in block " + std::to_string(herr.nonfinite));
+}
+
+// new values on the ingested pattern (bf_update): canonicalise + finiteness check
+void reingest_values(bf_ctx *c, const double *vals, int mem) {
+  int64_t nnzb = c->nnzb;
+  double *raw = dalloc_t<double>(c, (size_t)nnzb * 4);
+  BF_CUDA(cudaMemcpyAsync(raw, vals, sizeof(double) * 4 * nnzb, mem ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          c->stream));
+  IngestErr *derr = dalloc_t<IngestErr>(c, 1);
+  IngestErr herr{INT32_MAX, INT32_MAX, INT32_MAX, (long long)INT64_MAX};
+  BF_CUDA(cudaMemcpyAsync(derr, &herr, sizeof herr, cudaMemcpyHostToDevice, c->stream));
+  double *bv = dalloc_t<double>(c, (size_t)nnzb * 4);
+  k_canon<<<div_up(nnzb, 256), 256, 0, c->stream>>>(nnzb, raw, bv, c->block_order, c->var_order, derr);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  BF_CUDA(cudaMemcpyAsync(&herr, derr, sizeof herr, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, raw);
+  dfree(c, derr);
+  if (herr.nonfinite != (long long)INT64_MAX) {
+    dfree(c, bv);
+    throw Error(BF_ERR_NONFINITE, "non-finite Jacobian value in block " + std::to_string(herr.nonfinite));
+  }
+  dfree(c, c->bv);
+  c->bv = bv;
 }
 
 // ---------------------------------------------------------------------------------------

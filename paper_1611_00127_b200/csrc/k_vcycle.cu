@@ -343,6 +343,15 @@ void bf_apply(bf_ctx *c, const double *v, double *z) {
   BF_CUDA(cudaGetLastError());
 }
 
+// forget the captured BF apply (buffers of the finest level changed)
+void drop_apply_graph(bf_ctx *c) {
+  if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
+  if (c->apply_graph) cudaGraphDestroy(c->apply_graph);
+  c->apply_exec = nullptr;
+  c->apply_graph = nullptr;
+  c->apply_split_node = nullptr;
+}
+
 // The whole BF apply (~60 kernels, most of them small coarse-level kernels) replayed as one
 // CUDA graph: captured once per handle on a private stream, launched on the caller's stream.
 // Only the input vector changes between applies; it is patched into the split kernel node.

@@ -14,9 +14,16 @@ def declared_symbols():
     return sorted(set(re.findall(r"^(?:bf_status|const char \*)\s*(bf_\w+)\s*\(", src, re.M)))
 
 
+def _build():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bf_build", os.path.join(ROOT, "paper_1611_00127_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()
+
+
 def test_library_builds_and_exports():
-    from paper_1611_00127_b200 import build
-    so = build.build()
+    so = _build()
     out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (bf_\w+)", out))
     decl = declared_symbols()
@@ -28,8 +35,7 @@ def test_library_builds_and_exports():
 
 
 def test_sm100a_code_and_no_oracle_link():
-    from paper_1611_00127_b200 import build
-    so = build.build()
+    so = _build()
     out = subprocess.run(["cuobjdump", "-lelf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     deps = subprocess.run(["ldd", so], capture_output=True, text=True).stdout

@@ -203,3 +203,45 @@ def test_determinism_repeat_setup():
     x1, x2 = np.zeros(2 * J.n), np.zeros(2 * J.n)
     r1, r2 = g1.solve(rhs, x1), g2.solve(rhs, x2)
     assert r1["iters"] == r2["iters"] and np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("config,dims", [(2, (12, 11, 9)), (3, (20, 17, 15)), (1, (14, 12, 1))])
+def test_setup_reuse_update_parity(config, dims):
+    """bf_update (NEXT-1, R16) on a Newton sequence whose states come from the ORACLE's solves:
+    finest levels bit-exact, coarse levels kept, BF apply <= 1e-10, GMRES +-1 / 1e-6."""
+    from workload import newton_sequence
+    seq = []
+    o = None
+
+    def solve(k, J, rhs):
+        return oracle.BF(J).gmres(rhs, tol=1e-8, maxit=600)["x"]
+    for k, prob, J, rhs, fn in newton_sequence(config, 3, solve, dims=dims):
+        seq.append((prob, J, rhs))
+    prob, J0, _ = seq[0]
+    g = gpu_solver(J0, prob.dims)
+    o = oracle.BF(J0)
+    coarse_before = [[g.level(w, l)["A"] for l in range(1, g.num_levels(w))] for w in (0, 1)]
+    for k in (1, 2):
+        _, Jk, rhs = seq[k]
+        g.update(torch_dev(Jk.vals.reshape(-1)))
+        o.update(Jk)
+        for b, name in enumerate(("App", "Aps", "Asp", "Ass", "S")):
+            pat, val = csr_equal(g.block(b), o.matrix(name))
+            assert pat and val, (k, name)
+        for w in (0, 1):
+            pat, val = csr_equal(g.level(w, 0)["A"], o.level(w, 0)["A"])
+            assert pat and val
+            assert np.array_equal(g.level(w, 0)["dl1"], o.level(w, 0)["dl1"])
+            for l, old in enumerate(coarse_before[w], start=1):
+                assert all(np.array_equal(u, v) for u, v in zip(g.level(w, l)["A"], old))
+        v = seeded_vector(2 * Jk.n, 30 + k)
+        z = np.zeros(2 * Jk.n)
+        g.apply_precond(v, z)
+        zo = o.apply(v)
+        assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo)
+        ro = o.gmres(rhs, tol=1e-8, maxit=600)
+        x = np.zeros(2 * Jk.n)
+        r = g.solve(rhs, x, tol=1e-8, maxit=600)
+        assert abs(r["iters"] - ro["iters"]) <= 1 and r["converged"] == ro["converged"]
+        for f in (0, 1):
+            assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])

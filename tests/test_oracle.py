@@ -451,3 +451,42 @@ def test_bsr_spmv_vs_scipy():
     assert np.max(np.abs(y - ys)) <= 1e-14 * (np.abs(J.to_scipy()) @ np.abs(x)).max()
     bf = oracle.BF(J)
     assert np.array_equal(bf.spmv(x), y)
+
+
+def test_setup_reuse_update():
+    """R16: bf_update keeps the coarse hierarchy and rebuilds the
+    split, S~ and the finest level exactly as a fresh setup would."""
+    from workload import newton_sequence
+    seqJ = []
+
+    def solve(k, J, rhs):
+        return oracle.BF(J).gmres(rhs, tol=1e-8, maxit=400)["x"]
+    for k, prob, J, rhs, fn in newton_sequence(2, 3, solve, dims=(10, 9, 8)):
+        seqJ.append((J, rhs, fn))
+    assert seqJ[2][2] < seqJ[0][2]                 # Newton reduces ||F||
+    J0, J1 = seqJ[0][0], seqJ[1][0]
+    assert np.array_equal(J0.row_ptr, J1.row_ptr) and np.array_equal(J0.col_idx, J1.col_idx)
+    bf = oracle.BF(J0)
+    coarse = [[bf.level(w, l) for l in range(1, bf.nlev(w))] for w in (0, 1)]
+    P0 = [bf.level(w, 0)["P"] for w in (0, 1)]
+    bf.update(J1)
+    fresh = oracle.BF(J1)
+    for name in ("App", "Aps", "Asp", "Ass", "S"):
+        a, b = bf.matrix(name), fresh.matrix(name)
+        assert np.array_equal(a.rp, b.rp) and np.array_equal(a.ci, b.ci) and np.array_equal(a.v, b.v)
+    for w in (0, 1):
+        L0, F0 = bf.level(w, 0), fresh.level(w, 0)
+        assert np.array_equal(L0["A"].v, F0["A"].v) and np.array_equal(L0["dl1"], F0["dl1"])
+        assert np.array_equal(L0["P"].v, P0[w].v)                 # interpolation kept
+        for l, old in enumerate(coarse[w], start=1):
+            assert np.array_equal(bf.level(w, l)["A"].v, old["A"].v)
+    # the reused preconditioner still solves J1 x = b
+    r = bf.gmres(seqJ[1][1], tol=1e-8, maxit=600)
+    assert r["converged"]
+    D = J1.to_scipy()
+    assert np.linalg.norm(seqJ[1][1] - D @ r["x"]) <= 1e-8 * np.linalg.norm(seqJ[1][1])
+    # same values -> identical to the original setup
+    bf2 = oracle.BF(J0)
+    bf2.update(J0)
+    v = seeded_vector(2 * J0.n, 4)
+    assert np.array_equal(bf2.apply(v), oracle.BF(J0).apply(v))

@@ -15,6 +15,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", type=int, default=3)
 p.add_argument("--dims", type=str, default=None)
 p.add_argument("--maxit", type=int, default=1500)
+p.add_argument("--sets", type=str, default="all")
 a = p.parse_args()
 dims = tuple(int(x) for x in a.dims.split(",")) if a.dims else None
 prob, J, rhs = make_system(a.config, dims=dims)
@@ -23,6 +24,9 @@ rp, ci, v, b = dev(J.row_ptr), dev(J.col_idx), dev(J.vals.reshape(-1)), dev(rhs)
 x = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
 SETS = [dict(), dict(nu_pre=2, nu_post=2), dict(smoother=1), dict(smoother=1, cheb_degree=3),
         dict(theta=0.5), dict(interp_norm=0), dict(orth=1), dict(smoother=1, cheb_lo=0.1)]
+if a.sets != "all":
+    SETS = [SETS[int(i)] for i in a.sets.split(",")]
+t_gen = time.perf_counter()
 for opts in SETS:
     try:
         o = bf.bf_default_options(**opts)
