@@ -80,6 +80,7 @@ struct bf_ctx {
   bf::Hier h[2];
   // solve workspace
   int32_t Vm = 0;
+  double *Z = nullptr;  // preconditioned basis z_j = M^-1 v_j (restart x N)
   double *V = nullptr, *w = nullptr, *z = nullptr, *r = nullptr, *xd = nullptr, *bd = nullptr;
   double *vp = nullptr, *vs = nullptr, *sv = nullptr, *pv = nullptr;  // BF apply split vectors
   double *red = nullptr;        // reduction partials
@@ -98,8 +99,8 @@ struct bf_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaGraph_t apply_graph = nullptr;
   cudaGraphExec_t apply_exec = nullptr;
-  cudaGraphNode_t apply_split_node = nullptr;
-  cudaKernelNodeParams split_params{};
+  cudaGraphNode_t apply_split_node = nullptr, apply_merge_node = nullptr;
+  cudaKernelNodeParams split_params{}, merge_params{};
   int64_t apply_graph_kernels = 0;
   int num_sms = 148;
   bool use_tma = true;

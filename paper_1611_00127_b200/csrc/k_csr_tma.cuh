@@ -30,11 +30,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+// L2 policy for the streamed matrix: evict-first, so that one pass over a 100+ MB operator
+// does not push the (gathered, reused) vectors out of the 126 MB L2
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                             uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -49,10 +57,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-// byte layout of one stage: [cols: 4*(cap+8) B][vals: 8*(cap+4) B], both 16-B aligned
-// (the aligned copy of a tile of `cap` nonzeros spans at most cap+6 ints / cap+2 doubles)
+// byte layout of one stage: [row_ptr: 4*(rpt+8) B][cols: 4*(cap+8) B][vals: 8*(cap+4) B], all
+// 16-B aligned (the aligned copy of a tile of `cap` nonzeros spans at most cap+6 ints /
+// cap+2 doubles; the tile's row_ptr segment rpt+1 ints, rounded up to 4).  Staging row_ptr
+// too removes the dependent global load of rp[r], rp[r+1] before each row's gathers.
+__host__ __device__ inline int tma_rp_bytes(int rpt) { return ((4 * (rpt + 8)) + 15) & ~15; }
 __host__ __device__ inline int tma_col_bytes(int cap) { return ((4 * (cap + 8)) + 15) & ~15; }
-__host__ __device__ inline int tma_stage_bytes(int cap) { return tma_col_bytes(cap) + (((8 * (cap + 4)) + 15) & ~15); }
+__host__ __device__ inline int tma_stage_bytes(int cap, int rpt) {
+  return tma_rp_bytes(rpt) + tma_col_bytes(cap) + (((8 * (cap + 4)) + 15) & ~15);
+}
 
 template <int MODE, int G, int ST>
 __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int ntiles, int cap,
@@ -65,8 +78,9 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
                                                          const double *__restrict__ dir) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[ST];
-  const int stage_bytes = tma_stage_bytes(cap);
-  const int cb = tma_col_bytes(cap);
+  const int stage_bytes = tma_stage_bytes(cap, rpt);
+  const int rb = tma_rp_bytes(rpt);
+  const int cb = rb + tma_col_bytes(cap);
   int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < ST; s++) mbar_init(&bars[s], 1);
@@ -75,16 +89,19 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
   __syncthreads();
 
   // producer: issue the bulk copies of tile t into stage s
+  const uint64_t pol = l2_evict_first_policy();
   auto issue = [&](int t, int s) {
     int r0 = t * rpt, r1 = min(r0 + rpt, n);
     int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
     int c0 = q0 & ~3, c1 = (q1 + 3) & ~3;  // 16-B aligned int32 range
     int v0 = q0 & ~1, v1 = (q1 + 1) & ~1;  // 16-B aligned double range
     unsigned char *base = smem_raw + s * stage_bytes;
+    uint32_t br = 4u * ((r1 - r0 + 1 + 3) & ~3);  // r0 is a multiple of 4 (rpt is)
     uint32_t bc = 4u * (c1 - c0), bv = 8u * (v1 - v0);
-    mbar_expect_tx(&bars[s], bc + bv);
-    if (bc) tma_bulk_g2s(base, ci + c0, bc, &bars[s]);
-    if (bv) tma_bulk_g2s(base + cb, v + v0, bv, &bars[s]);
+    mbar_expect_tx(&bars[s], br + bc + bv);
+    tma_bulk_g2s(base, rp + r0, br, &bars[s], pol);
+    if (bc) tma_bulk_g2s(base + rb, ci + c0, bc, &bars[s], pol);
+    if (bv) tma_bulk_g2s(base + cb, v + v0, bv, &bars[s], pol);
   };
 
   int t = blockIdx.x;
@@ -95,17 +112,18 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
   for (int it = 0; t < ntiles; t += gridDim.x, it++) {
     int s = it % ST;
     int r0 = t * rpt;
-    int q0 = __ldg(rp + r0);
     mbar_wait(&bars[s], (it / ST) & 1);
     const unsigned char *base = smem_raw + s * stage_bytes;
-    const int32_t *sc = reinterpret_cast<const int32_t *>(base) - (q0 & ~3);
+    const int32_t *srp = reinterpret_cast<const int32_t *>(base);
+    int q0 = srp[0];
+    const int32_t *sc = reinterpret_cast<const int32_t *>(base + rb) - (q0 & ~3);
     const double *sv = reinterpret_cast<const double *>(base + cb) - (q0 & ~1);
     // rows of the tile in passes of TMA_THREADS/G rows; G lanes per row
     for (int row_in_tile = tid / G; row_in_tile < ((rpt + (TMA_THREADS / G) - 1) / (TMA_THREADS / G)) * (TMA_THREADS / G);
          row_in_tile += TMA_THREADS / G) {
       int r = r0 + row_in_tile;
       bool ok = row_in_tile < rpt && r < n;
-      int lo = ok ? __ldg(rp + r) : 0, hi = ok ? __ldg(rp + r + 1) : 0;
+      int lo = ok ? srp[row_in_tile] : 0, hi = ok ? srp[row_in_tile + 1] : 0;
       double acc = 0.0;
 #pragma unroll 4
       for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
@@ -156,7 +174,7 @@ void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *
     BF_CUDA(cudaFuncSetAttribute(k_csr_tma<MODE, G, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
-  int smem = ST * tma_stage_bytes(A.cap);
+  int smem = ST * tma_stage_bytes(A.cap, A.rpt);
   int ntiles = (A.n + A.rpt - 1) / A.rpt;
   int per_sm = std::max(1, std::min(8, (220 * 1024) / (smem + 1024)));
   int grid = std::min(ntiles, c->num_sms * per_sm);

@@ -222,6 +222,8 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
   if (c->Vm < restart + 1) {
     dfree(c, c->V);
     c->V = dalloc_t<double>(c, (size_t)(restart + 1) * N);
+    dfree(c, c->Z);
+    c->Z = dalloc_t<double>(c, (size_t)restart * N);
     c->Vm = restart + 1;
   }
 }
@@ -295,10 +297,11 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     for (int j = 0; j < m; j++) {
       const double *vj = V + (size_t)j * N;
       double *vn = V + (size_t)(j + 1) * N;
-      bf_apply_graph(c, vj, c->z);  // z = M^-1 v_j
+      double *zj = c->Z + (size_t)j * N;
+      bf_apply_graph(c, vj, zj);  // z_j = M^-1 v_j, kept for the cycle-end update
       cudaEvent_t t0;
       timer_begin(c, 0, &t0);
-      bsr_spmv(c, c->z, c->w);  // w = J z
+      bsr_spmv(c, zj, c->w);  // w = J z_j
       timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
       int nv = j + 1;
       timer_begin(c, 1, &t0);
@@ -361,9 +364,9 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     double *yd = c->hdev + 3 * MAXNV + 4;  // distinct from dot_host's slot
     BF_CUDA(cudaMemcpyAsync(c->hdev + MAXNV, c->hpin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
     (void)yd;
-    BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, V, c->hdev + MAXNV, c->w)));
+    // x += M^-1 (V y) = Z y  (M^-1 is a fixed linear operator: no extra BF apply per cycle)
+    BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, c->Z, c->hdev + MAXNV, c->z)));
     BF_LAUNCH(c);
-    bf_apply_graph(c, c->w, c->z);
     k_add_inplace<<<G, 256, 0, c->stream>>>(N, x, c->z);
     BF_LAUNCH(c);
     // true residual at the end of the cycle (R11)

@@ -181,7 +181,7 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil) {
     int h = 0;
     BF_CUDA(cudaMemcpyAsync(&h, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    if (A.stages * tma_stage_bytes(h) <= 110 * 1024) {
+    if (A.stages * tma_stage_bytes(h, rpt) <= 110 * 1024) {
       A.rpt = rpt;
       A.cap = std::max(h, 1);
       break;
@@ -350,16 +350,13 @@ void drop_apply_graph(bf_ctx *c) {
   c->apply_exec = nullptr;
   c->apply_graph = nullptr;
   c->apply_split_node = nullptr;
+  c->apply_merge_node = nullptr;
 }
 
 // The whole BF apply (~60 kernels, most of them small coarse-level kernels) replayed as one
 // CUDA graph: captured once per handle on a private stream, launched on the caller's stream.
 // Only the input vector changes between applies; it is patched into the split kernel node.
 void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
-  if (z != c->z) {  // the graph writes c->z; other targets take the eager path
-    bf_apply(c, v, z);
-    return;
-  }
   if (!c->apply_exec) {
     if (!c->cap_stream) BF_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     cudaStream_t user = c->stream;
@@ -383,12 +380,13 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     c->apply_bytes = c->alg_bytes - b0;
     c->launches = l0;
     BF_CUDA(cudaGraphInstantiate(&c->apply_exec, g, 0));
-    // locate the split kernel node (the only node that reads v)
+    // locate the split node (the only reader of v) and the merge node (the only writer of z)
     size_t nn = 0;
     BF_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
     BF_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
     c->apply_split_node = nullptr;
+    c->apply_merge_node = nullptr;
     for (auto nd : nodes) {
       cudaGraphNodeType t;
       BF_CUDA(cudaGraphNodeGetType(nd, &t));
@@ -398,35 +396,29 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
       if (p.func == (void *)k_split_vec) {
         c->apply_split_node = nd;
         c->split_params = p;
+      } else if (p.func == (void *)k_merge_vec) {
+        c->apply_merge_node = nd;
+        c->merge_params = p;
       }
     }
     c->apply_graph = g;
-    if (!c->apply_split_node) throw Error(BF_ERR_CUDA, "split node not found in the BF apply graph");
+    if (!c->apply_split_node || !c->apply_merge_node)
+      throw Error(BF_ERR_CUDA, "split/merge node not found in the BF apply graph");
   }
-  // patch the input pointer of the split kernel
-  int n = c->n, ip = c->var_order;
-  Hier &hs = c->h[0];
-  double beta = x0_beta(c->opt);
-  double *vp = c->vp, *vs = hs.lv[0].b, *x0 = hs.lv[0].x;
-  const double *dinv = hs.lv[0].d;
-  (void)vs;
-  (void)x0;
-  void *args[8];
-  // argument values as captured, with v replaced (the other buffers are fixed per handle)
-  void **cap = c->split_params.kernelParams;
+  // patch the input pointer of the split kernel (argument 2: v) and the output pointer of the
+  // merge kernel (argument 4: z); all other arguments are the handle's fixed buffers
   const double *vin = v;
-  args[0] = cap[0];
-  args[1] = cap[1];
-  args[2] = (void *)&vin;
-  args[3] = cap[3];
-  args[4] = cap[4];
-  args[5] = cap[5];
-  args[6] = cap[6];
-  args[7] = cap[7];
-  (void)n; (void)ip; (void)beta; (void)vp; (void)dinv;
-  cudaKernelNodeParams p = c->split_params;
-  p.kernelParams = args;
-  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_split_node, &p));
+  double *zout = z;
+  void *sargs[8], *margs[5];
+  for (int k = 0; k < 8; k++) sargs[k] = c->split_params.kernelParams[k];
+  for (int k = 0; k < 5; k++) margs[k] = c->merge_params.kernelParams[k];
+  sargs[2] = (void *)&vin;
+  margs[4] = (void *)&zout;
+  cudaKernelNodeParams ps = c->split_params, pm = c->merge_params;
+  ps.kernelParams = sargs;
+  pm.kernelParams = margs;
+  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_split_node, &ps));
+  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_merge_node, &pm));
   cudaEvent_t t0;
   timer_begin(c, 2, &t0);
   BF_CUDA(cudaGraphLaunch(c->apply_exec, c->stream));
