@@ -149,7 +149,7 @@ void build_schur(bf_ctx *c);                                            // k_spl
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);                                     // k_vcycle.cu
-void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false);                 // k_vcycle.cu
+void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
 void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu

@@ -8,10 +8,17 @@
 // DESIGN.md ("Determinism contract") with explicitly rounded __dmul_rn / __dadd_rn /
 // __ddiv_rn; PMIS is integer-only with synchronous rounds.  The hierarchy is therefore
 // bit-identical run to run and to the oracle.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "bf_internal.cuh"
+
+#include <algorithm>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace bf {
 
@@ -115,6 +122,49 @@ __global__ void k_pmis_update(DCsr A, const uint8_t *__restrict__ strong, const 
   atomicAdd(nU, 1);
 }
 
+// All PMIS rounds in one cooperative kernel (grid-wide barriers between the synchronous
+// phases of a round) -- a round costs ~4 grid barriers instead of 3 launches + a host sync;
+// chains of strictly ordered keys can need hundreds of rounds (measured: 500 on a S~ level).
+__global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const uint64_t *__restrict__ key,
+                            int8_t *state, uint8_t *notmax, uint8_t *cnew, int *nU, int max_rounds, int *rounds) {
+  cg::grid_group grid = cg::this_grid();
+  const int n = A.n;
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int round = 0;
+  for (; round < max_rounds; round++) {
+    int *cnt = nU + (round & 1);
+    for (int i = t0; i < n; i += stride) notmax[i] = 0;
+    if (t0 == 0) *cnt = 0;
+    grid.sync();
+    for (int i = t0; i < n; i += stride) {
+      if (state[i] >= 0) continue;
+      for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
+        int j = A.ci[q];
+        if (!strong[q] || state[j] >= 0) continue;
+        if (greater_key(key, i, j)) notmax[j] = 1;
+        else notmax[i] = 1;
+      }
+    }
+    grid.sync();
+    for (int i = t0; i < n; i += stride) cnew[i] = (uint8_t)(state[i] < 0 && !notmax[i]);
+    grid.sync();
+    int local = 0;
+    for (int i = t0; i < n; i += stride) {
+      if (state[i] >= 0) continue;
+      if (cnew[i]) { state[i] = 1; continue; }
+      bool f = false;
+      for (int q = A.rp[i]; q < A.rp[i + 1] && !f; q++) f = strong[q] && cnew[A.ci[q]];
+      if (f) state[i] = 0;
+      else local++;
+    }
+    if (local) atomicAdd(cnt, local);
+    grid.sync();
+    if (*(volatile int *)cnt == 0) break;
+  }
+  if (t0 == 0) *rounds = round + 1;
+}
+
 __global__ void k_is_c(int n, const int8_t *__restrict__ cf, int32_t *flag) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) flag[i] = cf[i] == 1;
@@ -149,9 +199,10 @@ __device__ __forceinline__ int bsearch_pos(const int32_t *a, int lo, int hi, int
 // option.  P.ci temporarily holds fine column indices (ascending), mapped to coarse at the end.
 __global__ void k_interp_fill(DCsr A, const uint8_t *__restrict__ strong, const int8_t *__restrict__ cf,
                               const int32_t *__restrict__ cmap, const double *__restrict__ diag, int norm,
-                              DCsr P) {
+                              DCsr P, const uint8_t *__restrict__ only) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
+  if (only && !only[i]) return;
   int base = P.rp[i], end = P.rp[i + 1];
   if (cf[i] == 1) {
     P.ci[base] = cmap[i];
@@ -209,6 +260,142 @@ __global__ void k_interp_fill(DCsr A, const uint8_t *__restrict__ strong, const 
     double w = den == 0.0 ? 0.0 : (norm ? __ddiv_rn(num, den) : -__ddiv_rn(num, den));
     P.v[p] = w;
     P.ci[p] = cmap[P.ci[p]];
+  }
+}
+
+// Warp-per-row classical interpolation: the same sequence of roundings as k_interp_fill (and
+// the oracle), with the row's entries, the C_i set and the strong-F rows scanned by 32 lanes.
+// Every ordered sum (dg, D_k, the R8 denominator) is accumulated by lane 0 in ascending
+// column order from values gathered with shuffles; each num_m is updated by the one lane that
+// owns m, once per k, k ascending.  Rows with more than IW_CAP strong C or strong F
+// neighbours are flagged and done by k_interp_fill.
+constexpr int IW_WARPS = 8;
+constexpr int IW_CAP = 128;
+
+__global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uint8_t *__restrict__ strong,
+                                                               const int8_t *__restrict__ cf,
+                                                               const int32_t *__restrict__ cmap,
+                                                               const double *__restrict__ diag, int norm, DCsr P,
+                                                               uint8_t *long_rows, int *any_long) {
+  __shared__ int s_ccol[IW_WARPS][IW_CAP];
+  __shared__ double s_num[IW_WARPS][IW_CAP];
+  __shared__ int s_fk[IW_WARPS][IW_CAP];
+  __shared__ double s_fa[IW_WARPS][IW_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * IW_WARPS + warp;
+  if (i >= A.n) return;
+  const int base = P.rp[i], end = P.rp[i + 1];
+  if (cf[i] == 1) {
+    if (lane == 0) {
+      P.ci[base] = cmap[i];
+      P.v[base] = 1.0;
+    }
+    return;
+  }
+  if (end == base) return;
+  int *ccol = s_ccol[warp], *fk = s_fk[warp];
+  double *num = s_num[warp], *fa = s_fa[warp];
+  const int r0 = A.rp[i], r1 = A.rp[i + 1];
+  // pass 1: C_i (ascending) with num = a_ij; F_i^s (ascending) with a_ik; dg over the weak set
+  int nc = 0, nf = 0;
+  double dg = diag[i];
+  for (int q0 = r0; q0 < r1; q0 += 32) {
+    int q = q0 + lane;
+    bool valid = q < r1;
+    int j = valid ? A.ci[q] : -1;
+    double a = valid ? A.v[q] : 0.0;
+    bool st = valid && strong[q] && j != i;
+    int8_t cj = (valid && j >= 0) ? cf[j] : 0;
+    bool isC = st && cj == 1, isF = st && cj != 1, weak = valid && !strong[q] && j != i;
+    unsigned mc = __ballot_sync(0xffffffffu, isC), mf = __ballot_sync(0xffffffffu, isF);
+    unsigned mw = __ballot_sync(0xffffffffu, weak);
+    if (nc + __popc(mc) > IW_CAP || nf + __popc(mf) > IW_CAP) {
+      if (lane == 0) {
+        long_rows[i] = 1;
+        atomicMax(any_long, 1);
+      }
+      return;
+    }
+    unsigned below = (1u << lane) - 1;
+    if (isC) {
+      ccol[nc + __popc(mc & below)] = j;
+      num[nc + __popc(mc & below)] = a;
+    }
+    if (isF) {
+      fk[nf + __popc(mf & below)] = j;
+      fa[nf + __popc(mf & below)] = a;
+    }
+    // dg = dg + a_in over the weak entries, ascending (lane 0 walks the chunk in order)
+    for (int l = 0; l < 32; l++) {
+      double al = __shfl_sync(0xffffffffu, a, l);
+      if ((mw >> l) & 1u) dg = __dadd_rn(dg, al);
+    }
+    nc += __popc(mc);
+    nf += __popc(mf);
+  }
+  __syncwarp();
+  // pass 2: strong F neighbours k ascending
+  for (int f = 0; f < nf; f++) {
+    const int k = fk[f];
+    const double aik = fa[f];
+    const double sk = diag[k] < 0.0 ? -1.0 : 1.0;
+    const int k0 = A.rp[k], k1 = A.rp[k + 1];
+    double Dk = 0.0;
+    for (int q0 = k0; q0 < k1; q0 += 32) {  // D_k = sum over row k cap C_i of abar, ascending
+      int q = q0 + lane;
+      double abar = 0.0;
+      bool mem = false;
+      if (q < k1) {
+        int m = A.ci[q];
+        int lo = 0, hi = nc;  // binary search of m in C_i
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (ccol[mid] < m) lo = mid + 1;
+          else hi = mid;
+        }
+        mem = lo < nc && ccol[lo] == m;
+        double a = A.v[q];
+        abar = (sk * a < 0.0) ? a : 0.0;
+      }
+      unsigned mm = __ballot_sync(0xffffffffu, mem);
+      for (int l = 0; l < 32; l++) {
+        double al = __shfl_sync(0xffffffffu, abar, l);
+        if ((mm >> l) & 1u) Dk = __dadd_rn(Dk, al);
+      }
+    }
+    if (Dk == 0.0) {
+      dg = __dadd_rn(dg, aik);  // lumped into the diagonal
+      continue;
+    }
+    const double cc = __ddiv_rn(aik, Dk);
+    for (int q0 = k0; q0 < k1; q0 += 32) {  // num_m += cc * abar_km (each m owned by one lane)
+      int q = q0 + lane;
+      if (q < k1) {
+        int m = A.ci[q];
+        int lo = 0, hi = nc;
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (ccol[mid] < m) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < nc && ccol[lo] == m) {
+          double a = A.v[q];
+          double abar = (sk * a < 0.0) ? a : 0.0;
+          num[lo] = __dadd_rn(num[lo], __dmul_rn(cc, abar));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  double den = dg;
+  if (norm) {
+    den = 0.0;
+    for (int u = 0; u < nc; u++) den = __dadd_rn(den, num[u]);  // ascending (uniform per lane)
+  }
+  for (int u = lane; u < nc; u += 32) {
+    double w = den == 0.0 ? 0.0 : (norm ? __ddiv_rn(num[u], den) : -__ddiv_rn(num[u], den));
+    P.v[base + u] = w;
+    P.ci[base + u] = cmap[ccol[u]];
   }
 }
 
@@ -327,7 +514,265 @@ static int bits_for(int64_t x) {
   return b;
 }
 
+// ---- row-owned hash SpGEMM (default): one warp per row of C, shared-memory hash table.
+// For each k of row i of A in ascending order, the warp's lanes take the entries of row k of
+// B (distinct columns J within the row, so no two lanes touch the same slot), insert J and
+// apply acc[J] = acc[J] + A(i,k) * B(k,J) (separately rounded); a __syncwarp between
+// consecutive k keeps every entry's sum in ascending-k order -- the same sequence of
+// roundings as the oracle and as the expand-sort-compress path.  Rows are emitted sorted
+// (rank of each key among the row's keys).  If any row holds more than HASH_MAX distinct
+// columns the product falls back to expand-sort-compress.
+constexpr int HASH_WARPS = 4;
+constexpr int HASH_CAP = 512;        // max slots per warp (power of two)
+constexpr int HASH_MAX = 320;        // max distinct columns per row (load factor 0.625)
+
+// per-row table size: the smallest power of two >= 2 * (upper bound of the row's distinct
+// columns), at least 32, at most HASH_CAP -- small rows (most of them) touch few slots
+__device__ __forceinline__ int row_table_mask(const DCsr &A, const DCsr &B, int i, int lane) {
+  int ub = 0;
+  for (int q = A.rp[i] + lane; q < A.rp[i + 1]; q += 32) ub += B.rp[A.ci[q] + 1] - B.rp[A.ci[q]];
+  for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+  int t = 32;
+  while (t < HASH_CAP && t < 2 * ub) t <<= 1;
+  return t - 1;
+}
+
+__device__ __forceinline__ int hash_slot(int key, int mask) { return (int)(((unsigned)key * 2654435761u) >> 16) & mask; }
+
+// returns the slot of key, inserting it if absent (inserted == true for the inserting lane)
+__device__ __forceinline__ int hash_insert(int *keys, int key, int mask, bool &inserted) {
+  int s = hash_slot(key, mask);
+  inserted = false;
+  while (true) {
+    int prev = atomicCAS(&keys[s], -1, key);
+    if (prev == -1) {
+      inserted = true;
+      return s;
+    }
+    if (prev == key) return s;
+    s = (s + 1) & mask;
+  }
+}
+
+__global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, DCsr B, int32_t *cnt, int *overflow) {
+  __shared__ int skeys[HASH_WARPS][HASH_CAP];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i = blockIdx.x * HASH_WARPS + warp;
+  if (i >= A.n) return;
+  int *keys = skeys[warp];
+  int mask = row_table_mask(A, B, i, lane);
+  for (int s = lane; s <= mask; s += 32) keys[s] = -1;
+  __syncwarp();
+  int count = 0;
+  bool full = false;
+  for (int q = A.rp[i]; q < A.rp[i + 1] && !full; q++) {
+    int k = A.ci[q];
+    for (int t = B.rp[k] + lane; t < B.rp[k + 1]; t += 32) {
+      bool ins;
+      hash_insert(keys, B.ci[t], mask, ins);
+      count += ins;
+    }
+    // stop early once the row cannot fit (the product then falls back to the ESC path)
+    int tot = count;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    full = tot > HASH_MAX;
+  }
+  for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+  if (lane == 0) {
+    cnt[i] = count;
+    if (count > HASH_MAX) atomicMax(overflow, 1);
+  }
+}
+
+constexpr int HASH_WARP_BYTES = HASH_CAP * 4 + HASH_CAP * 8 + HASH_MAX * 4 + HASH_MAX * 8;
+
+__global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DCsr B, DCsr C) {
+  extern __shared__ __align__(16) unsigned char hsm[];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i = blockIdx.x * HASH_WARPS + warp;
+  if (i >= A.n) return;
+  unsigned char *wb = hsm + (size_t)warp * HASH_WARP_BYTES;
+  double *vals = reinterpret_cast<double *>(wb);
+  double *cvals = reinterpret_cast<double *>(wb + HASH_CAP * 8);
+  int *keys = reinterpret_cast<int *>(wb + HASH_CAP * 8 + HASH_MAX * 8);
+  int *ckeys = keys + HASH_CAP;
+  int mask = row_table_mask(A, B, i, lane);
+  for (int s = lane; s <= mask; s += 32) keys[s] = -1;
+  __syncwarp();
+  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {  // k ascending
+    int k = A.ci[q];
+    double a = A.v[q];
+    for (int t = B.rp[k] + lane; t < B.rp[k + 1]; t += 32) {
+      bool ins;
+      int s = hash_insert(keys, B.ci[t], mask, ins);
+      double acc = ins ? 0.0 : vals[s];
+      vals[s] = __dadd_rn(acc, __dmul_rn(a, B.v[t]));
+    }
+    __syncwarp();
+  }
+  // compact the occupied slots, then place each entry at its rank (rows are emitted sorted)
+  int n = 0;
+  for (int s0 = 0; s0 <= mask; s0 += 32) {
+    int key = keys[s0 + lane];
+    unsigned m = __ballot_sync(0xffffffffu, key >= 0);
+    if (key >= 0) {
+      int pos = n + __popc(m & ((1u << lane) - 1));
+      ckeys[pos] = key;
+      cvals[pos] = vals[s0 + lane];
+    }
+    n += __popc(m);
+  }
+  __syncwarp();
+  int base = C.rp[i];
+  for (int e = lane; e < n; e += 32) {
+    int key = ckeys[e], rank = 0;
+    for (int u = 0; u < n; u++) rank += ckeys[u] < key;
+    C.ci[base + rank] = key;
+    C.v[base + rank] = cvals[e];
+  }
+}
+
+// ---- thread-per-row SpGEMM for short rows of B (A P with P rows of ~1-6 entries): each
+// thread keeps its row's distinct columns and sums in a small local array, accumulating in
+// ascending k (same rounding sequence as above), then insertion-sorts the row.
+constexpr int TPR_CAP = 48;
+
+__global__ void k_spgemm_tpr_count(DCsr A, DCsr B, int32_t *cnt, int *overflow) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  int cols[TPR_CAP];
+  int len = 0;
+  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
+    int k = A.ci[q];
+    for (int t = B.rp[k]; t < B.rp[k + 1]; t++) {
+      int J = B.ci[t], u = 0;
+      while (u < len && cols[u] != J) u++;
+      if (u == len) {
+        if (len == TPR_CAP) {
+          atomicMax(overflow, 1);
+          cnt[i] = 0;
+          return;
+        }
+        cols[len++] = J;
+      }
+    }
+  }
+  cnt[i] = len;
+}
+
+__global__ void k_spgemm_tpr_fill(DCsr A, DCsr B, DCsr C) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  int cols[TPR_CAP];
+  double acc[TPR_CAP];
+  int len = 0;
+  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {  // k ascending
+    int k = A.ci[q];
+    double a = A.v[q];
+    for (int t = B.rp[k]; t < B.rp[k + 1]; t++) {
+      int J = B.ci[t], u = 0;
+      while (u < len && cols[u] != J) u++;
+      if (u == len) {
+        cols[len] = J;
+        acc[len] = 0.0;
+        len++;
+      }
+      acc[u] = __dadd_rn(acc[u], __dmul_rn(a, B.v[t]));
+    }
+  }
+  for (int x = 1; x < len; x++) {
+    int key = cols[x];
+    double v = acc[x];
+    int y = x - 1;
+    while (y >= 0 && cols[y] > key) {
+      cols[y + 1] = cols[y];
+      acc[y + 1] = acc[y];
+      y--;
+    }
+    cols[y + 1] = key;
+    acc[y + 1] = v;
+  }
+  int base = C.rp[i];
+  for (int x = 0; x < len; x++) {
+    C.ci[base + x] = cols[x];
+    C.v[base + x] = acc[x];
+  }
+}
+
+static void spgemm_esc(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
+static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
+
 static void spgemm(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
+  if (getenv("BF_SPGEMM_ESC")) {
+    spgemm_esc(c, A, B, C);
+    return;
+  }
+  if (B.n > 0 && (double)B.nnz / B.n <= 6.0 && A.n > 0 && (double)A.nnz / A.n <= 30.0 && !getenv("BF_SPGEMM_HASH")) {
+    C.n = A.n;
+    C.m = B.m;
+    int32_t *cnt = dalloc_t<int32_t>(c, A.n);
+    int *ovf = dalloc_t<int>(c, 1);
+    BF_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), c->stream));
+    k_spgemm_tpr_count<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, cnt, ovf);
+    BF_LAUNCH(c);
+    int h_ovf = 0;
+    BF_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    dfree(c, ovf);
+    if (!h_ovf) {
+      C.rp = dalloc_t<int32_t>(c, (size_t)C.n + 1);
+      C.nnz = exclusive_scan_i32(c, cnt, C.rp, C.n);
+      dfree(c, cnt);
+      C.ci = dalloc_t<int32_t>(c, C.nnz);
+      C.v = dalloc_t<double>(c, C.nnz);
+      k_spgemm_tpr_fill<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, C);
+      BF_LAUNCH(c);
+      BF_CUDA(cudaGetLastError());
+      return;
+    }
+    dfree(c, cnt);
+    C = DCsr();
+  }
+  spgemm_hash(c, A, B, C);
+}
+
+static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
+  C.n = A.n;
+  C.m = B.m;
+  int32_t *cnt = dalloc_t<int32_t>(c, A.n);
+  int *ovf = dalloc_t<int>(c, 1);
+  BF_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), c->stream));
+  int blocks = div_up(A.n, HASH_WARPS);
+  k_spgemm_hash_count<<<blocks, HASH_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  int h_ovf = 0;
+  BF_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, ovf);
+  if (h_ovf) {
+    dfree(c, cnt);
+    spgemm_esc(c, A, B, C);
+    return;
+  }
+  C.rp = dalloc_t<int32_t>(c, (size_t)C.n + 1);
+  C.nnz = exclusive_scan_i32(c, cnt, C.rp, C.n);
+  dfree(c, cnt);
+  C.ci = dalloc_t<int32_t>(c, C.nnz);
+  C.v = dalloc_t<double>(c, C.nnz);
+  static bool attr = false;
+  if (!attr) {
+    BF_CUDA(cudaFuncSetAttribute(k_spgemm_hash_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 HASH_WARPS * HASH_WARP_BYTES));
+    attr = true;
+  }
+  k_spgemm_hash_fill<<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES, c->stream>>>(A, B, C);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
+// ---- expand-sort-compress SpGEMM (fallback for rows with more than HASH_MAX columns)
+static void spgemm_esc(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   C.n = A.n;
   C.m = B.m;
   int64_t *ub = dalloc_t<int64_t>(c, A.n);
@@ -478,8 +923,17 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   const bf_options &o = c->opt;
   copy_csr(c, A0, h.lv[0].A);
   int l = 0;
-  int *nU_d = dalloc_t<int>(c, 1);
+  int *nU_d = dalloc_t<int>(c, 4);
+  const bool verbose = getenv("BF_VERBOSE") != nullptr;
+  auto tnow = [&]() {
+    if (verbose) sync(c);
+    return std::chrono::steady_clock::now();
+  };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
   while (h.lv[l].A.n > o.max_coarse && l < o.max_levels - 1 && l < BF_MAXL - 1) {
+    auto t0 = tnow();
     Level &L = h.lv[l];
     DCsr &A = L.A;
     int n = A.n;
@@ -492,6 +946,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     // PMIS
     int *lam = dalloc_t<int>(c, n);
     BF_CUDA(cudaMemsetAsync(lam, 0, sizeof(int) * n, c->stream));
+    auto t1 = tnow();
     k_lambda<<<div_up(n, 256), 256, 0, c->stream>>>(A, strong, lam);
     BF_LAUNCH(c);
     uint64_t *key = dalloc_t<uint64_t>(c, n);
@@ -500,19 +955,24 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     BF_LAUNCH(c);
     uint8_t *notmax = dalloc_t<uint8_t>(c, n);
     uint8_t *cnew = dalloc_t<uint8_t>(c, n);
-    for (int round = 0;; round++) {
-      BF_CUDA(cudaMemsetAsync(notmax, 0, n, c->stream));
-      BF_CUDA(cudaMemsetAsync(nU_d, 0, sizeof(int), c->stream));
-      k_pmis_edges<<<div_up(n, 256), 256, 0, c->stream>>>(A, strong, key, state, notmax);
-      k_pmis_cnew<<<div_up(n, 256), 256, 0, c->stream>>>(n, state, notmax, cnew);
-      k_pmis_update<<<div_up(n, 256), 256, 0, c->stream>>>(A, strong, cnew, state, nU_d);
-      c->launches += 3;
-      BF_CUDA(cudaGetLastError());
-      int nU = 0;
-      BF_CUDA(cudaMemcpyAsync(&nU, nU_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    {
+      static int coop_blocks = 0;
+      if (!coop_blocks) {
+        int per_sm = 0;
+        BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pmis_coop, 256, 0));
+        coop_blocks = std::max(1, per_sm) * c->num_sms;
+      }
+      int grid = std::max(1, std::min(coop_blocks, div_up(n, 256)));
+      int max_rounds = n + 1;  // each round decides at least the undecided point of largest key
+      int *rounds_d = nU_d + 2;
+      void *args[] = {(void *)&A, (void *)&strong, (void *)&key, (void *)&state, (void *)&notmax, (void *)&cnew,
+                      (void *)&nU_d, (void *)&max_rounds, (void *)&rounds_d};
+      BF_CUDA(cudaLaunchCooperativeKernel((void *)k_pmis_coop, grid, 256, args, 0, c->stream));
+      BF_LAUNCH(c);
+      int hr[3] = {0, 0, 0};
+      BF_CUDA(cudaMemcpyAsync(hr, nU_d, sizeof(hr), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
-      if (nU == 0) break;
-      if (round > 10000) throw Error(BF_ERR_LIMIT, "PMIS did not terminate");
+      if (hr[2] > max_rounds) throw Error(BF_ERR_LIMIT, "PMIS did not terminate");
     }
     dfree(c, notmax);
     dfree(c, cnew);
@@ -535,6 +995,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.cf = state;
     // interpolation
     int32_t *cnt = dalloc_t<int32_t>(c, n);
+    auto t2 = tnow();
     k_interp_count<<<div_up(n, 256), 256, 0, c->stream>>>(A, strong, state, cnt);
     BF_LAUNCH(c);
     L.P.n = n;
@@ -544,16 +1005,46 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     dfree(c, cnt);
     L.P.ci = dalloc_t<int32_t>(c, L.P.nnz);
     L.P.v = dalloc_t<double>(c, L.P.nnz);
-    k_interp_fill<<<div_up(n, 128), 128, 0, c->stream>>>(A, strong, state, cmap, diag, o.interp_norm, L.P);
+    {
+      uint8_t *long_rows = dalloc_t<uint8_t>(c, n);
+      int *any_long = dalloc_t<int>(c, 1);
+      int h_long = 1;
+      if ((double)A.nnz / n > 22.0) {  // long (Galerkin) rows: warp per row; short rows: thread per row
+        BF_CUDA(cudaMemsetAsync(long_rows, 0, n, c->stream));
+        BF_CUDA(cudaMemsetAsync(any_long, 0, sizeof(int), c->stream));
+        k_interp_warp<<<div_up(n, IW_WARPS), IW_WARPS * 32, 0, c->stream>>>(A, strong, state, cmap, diag,
+                                                                           o.interp_norm, L.P, long_rows, any_long);
+        BF_LAUNCH(c);
+        BF_CUDA(cudaMemcpyAsync(&h_long, any_long, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+      } else {
+        BF_CUDA(cudaMemsetAsync(long_rows, 1, n, c->stream));
+      }
+      if (h_long) {
+        k_interp_fill<<<div_up(n, 128), 128, 0, c->stream>>>(A, strong, state, cmap, diag, o.interp_norm, L.P,
+                                                             long_rows);
+        BF_LAUNCH(c);
+      }
+      dfree(c, long_rows);
+      dfree(c, any_long);
+    }
     BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
     dfree(c, cmap);
     dfree(c, strong);
     dfree(c, diag);
+    auto t3 = tnow();
     transpose(c, L.P, L.R);
+    auto t4 = tnow();
     DCsr AP;
     spgemm(c, A, L.P, AP);
+    auto t5 = tnow();
     spgemm(c, L.R, AP, h.lv[l + 1].A);
+    auto t6 = tnow();
+    if (verbose)
+      fprintf(stderr,
+              "[bf_setup]   h%d L%d n=%d nnz=%lld: strength %.2f pmis %.2f interp %.2f transpose %.2f AP %.2f RAP %.2f ms\n",
+              which, l, n, (long long)A.nnz, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, t6));
     free_csr(c, AP);
     l++;
   }
@@ -576,8 +1067,9 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.t = dalloc_t<double>(c, n);
     tile_csr(c, L.A, k == 0);
     if (k < h.nlev - 1) {
-      tile_csr(c, L.P);
-      tile_csr(c, L.R);
+      const char *gp = getenv("BF_TMA_G_P"), *gr = getenv("BF_TMA_G_R");
+      tile_csr(c, L.P, false, gp ? atoi(gp) : 0);
+      tile_csr(c, L.R, false, gr ? atoi(gr) : 0);
     }
   }
   BF_CUDA(cudaGetLastError());

@@ -152,13 +152,15 @@ __global__ void k_zero(int n, double *x) {
 // lanes per row: stencil-ordered fine-level rows -> 1 (lane-per-row gathers of consecutive
 // rows hit consecutive addresses); Galerkin rows -> several lanes reading adjacent sorted
 // columns of the same row (fewer distinct sectors per gather instruction)
-void tile_csr(bf_ctx *c, DCsr &A, bool stencil) {
+void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   A.rpt = 0;
   A.cap = 0;
   if (A.n == 0 || A.nnz == 0) return;
   double mean = (double)A.nnz / A.n;
   int g = 1;
-  if (!stencil) {
+  if (force_g > 0) {
+    g = force_g;
+  } else if (!stencil) {
     const char *e = getenv("BF_TMA_G");
     double div = e ? atof(e) : 3.0;
     while (g < 32 && 2 * g <= mean / div) g <<= 1;
