@@ -191,6 +191,8 @@ static void destroy_ctx(bf_ctx *c) {
   c->allocs.clear();
   bf::release_pending(c);
   if (c->hpin) bf::pinned_release(c->hpin);
+  for (auto e : c->step_ev)
+    if (e) cudaEventDestroy(e);
   if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
   if (c->apply_graph) cudaGraphDestroy(c->apply_graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);

@@ -87,6 +87,7 @@ struct bf_ctx {
   double *hdev = nullptr;       // reduced coefficients (device)
   double *hpin = nullptr;       // pinned host mirror
   unsigned int *counter = nullptr;
+  cudaEvent_t step_ev[2] = {nullptr, nullptr};  // per-Arnoldi-step completion (pipelined GMRES)
   int red_blocks = 0;
   // bookkeeping
   std::vector<std::pair<void *, size_t>> allocs;

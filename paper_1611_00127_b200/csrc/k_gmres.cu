@@ -217,7 +217,8 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
     c->hdev = dalloc_t<double>(c, 4 * MAXNV + 8);
     c->counter = dalloc_t<unsigned int>(c, 4);
     BF_CUDA(cudaMemsetAsync(c->counter, 0, 4 * sizeof(unsigned int), c->stream));
-    c->hpin = pinned_acquire();  // >= (4 MAXNV + 8) doubles
+    c->hpin = pinned_acquire();  // 2 step slots of (2 MAXNV + 8) doubles + y staging
+    for (int s = 0; s < 2; s++) BF_CUDA(cudaEventCreateWithFlags(&c->step_ev[s], cudaEventDisableTiming));
   }
   if (c->Vm < restart + 1) {
     dfree(c, c->V);
@@ -287,6 +288,42 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     return;
   }
   double *hd1 = c->hdev, *hd2 = c->hdev + MAXNV, *hdn = c->hdev + 2 * MAXNV;
+  // Arnoldi step j, enqueued without waiting for the host: z_j = M^-1 v_j, w = J z_j, CGS2,
+  // v_{j+1} = w / ||w|| (norm taken on the device), then an async copy of (h, h2, ||w||^2)
+  // into pinned slot j%2 and an event.  The host processes step j (Givens, convergence) while
+  // step j+1 already runs; a step enqueued past the stopping point is simply discarded.
+  const int SLOT = 2 * MAXNV + 8;
+  auto enqueue = [&](int j) {
+    const double *vj = V + (size_t)j * N;
+    double *vn = V + (size_t)(j + 1) * N;
+    double *zj = c->Z + (size_t)j * N;
+    bf_apply_graph(c, vj, zj);  // z_j = M^-1 v_j, kept for the cycle-end update
+    cudaEvent_t t0;
+    timer_begin(c, 0, &t0);
+    bsr_spmv(c, zj, c->w);  // w = J z_j
+    timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
+    int nv = j + 1;
+    timer_begin(c, 1, &t0);
+    BF_NV_SWITCH(nv, (k_dots<NV><<<wave_grid(c, k_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1,
+                                                                                          c->counter)));
+    if (c->opt.orth == 0) {
+      BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<wave_grid(c, k_axpy_dots<NV>), RED_THREADS, 0, c->stream>>>(
+                           N, V, c->w, hd1, c->red, hd2, c->counter)));
+      BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(
+                           N, V, c->w, hd2, vn, c->red, hdn, c->counter)));
+    } else {
+      BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(
+                           N, V, c->w, hd1, vn, c->red, hdn, c->counter)));
+    }
+    c->launches += c->opt.orth == 0 ? 3 : 2;
+    timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));
+    k_scale<<<G, 256, 0, c->stream>>>(N, vn, hdn, 0.0, vn);  // 1/sqrt(||w||^2) read on the device
+    BF_LAUNCH(c);
+    BF_CUDA(cudaGetLastError());
+    BF_CUDA(cudaMemcpyAsync(c->hpin + (j & 1) * SLOT, c->hdev, sizeof(double) * (2 * MAXNV + 1),
+                            cudaMemcpyDeviceToHost, c->stream));
+    BF_CUDA(cudaEventRecord(c->step_ev[j & 1], c->stream));
+  };
   for (;;) {
     k_scale<<<G, 256, 0, c->stream>>>(N, c->r, nullptr, 1.0 / beta, V);
     BF_LAUNCH(c);
@@ -294,41 +331,14 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     g[0] = beta;
     int k = 0;
     bool breakdown = false;
+    enqueue(0);
     for (int j = 0; j < m; j++) {
-      const double *vj = V + (size_t)j * N;
-      double *vn = V + (size_t)(j + 1) * N;
-      double *zj = c->Z + (size_t)j * N;
-      bf_apply_graph(c, vj, zj);  // z_j = M^-1 v_j, kept for the cycle-end update
-      cudaEvent_t t0;
-      timer_begin(c, 0, &t0);
-      bsr_spmv(c, zj, c->w);  // w = J z_j
-      timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
-      int nv = j + 1;
-      timer_begin(c, 1, &t0);
-      BF_NV_SWITCH(nv, (k_dots<NV><<<wave_grid(c, k_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1, c->counter)));
-      if (c->opt.orth == 0) {
-        BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<wave_grid(c, k_axpy_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, c->red, hd2,
-                                                                            c->counter)));
-        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd2, vn, c->red, hdn,
-                                                                            c->counter)));
-      } else {
-        BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, hd1, vn, c->red, hdn,
-                                                                            c->counter)));
-      }
-      c->launches += c->opt.orth == 0 ? 3 : 2;
-      timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));
-      BF_CUDA(cudaGetLastError());
-      BF_CUDA(cudaMemcpyAsync(c->hpin, c->hdev, sizeof(double) * (2 * MAXNV + 1), cudaMemcpyDeviceToHost,
-                              c->stream));
-      BF_CUDA(cudaStreamSynchronize(c->stream));
-      double hn = std::sqrt(c->hpin[2 * MAXNV]);
-      for (int i = 0; i <= j; i++) hcol[i] = c->hpin[i] + (c->opt.orth == 0 ? c->hpin[MAXNV + i] : 0.0);
-      if (hn != 0.0) {
-        k_scale<<<G, 256, 0, c->stream>>>(N, vn, nullptr, 1.0 / hn, vn);
-        BF_LAUNCH(c);
-      } else {
-        breakdown = true;
-      }
+      if (j + 1 < m && *iters + 1 < maxit) enqueue(j + 1);  // speculative next step
+      BF_CUDA(cudaEventSynchronize(c->step_ev[j & 1]));
+      const double *hp = c->hpin + (j & 1) * SLOT;
+      double hn = std::sqrt(hp[2 * MAXNV]);
+      for (int i = 0; i <= j; i++) hcol[i] = hp[i] + (c->opt.orth == 0 ? hp[MAXNV + i] : 0.0);
+      if (hn == 0.0) breakdown = true;  // (happy) breakdown: the speculative step is discarded
       for (int i = 0; i <= j; i++) H[(size_t)i * m + j] = hcol[i];
       H[(size_t)(j + 1) * m + j] = hn;
       for (int i = 0; i < j; i++) {  // previous Givens rotations
@@ -360,10 +370,9 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
       for (int jj = i + 1; jj < k; jj++) s -= H[(size_t)i * m + jj] * y[jj];
       y[i] = H[(size_t)i * m + i] != 0.0 ? s / H[(size_t)i * m + i] : 0.0;
     }
-    for (int i = 0; i < k; i++) c->hpin[i] = y[i];
-    double *yd = c->hdev + 3 * MAXNV + 4;  // distinct from dot_host's slot
-    BF_CUDA(cudaMemcpyAsync(c->hdev + MAXNV, c->hpin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
-    (void)yd;
+    double *ypin = c->hpin + 2 * SLOT;
+    for (int i = 0; i < k; i++) ypin[i] = y[i];
+    BF_CUDA(cudaMemcpyAsync(c->hdev + MAXNV, ypin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
     // x += M^-1 (V y) = Z y  (M^-1 is a fixed linear operator: no extra BF apply per cycle)
     BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, c->Z, c->hdev + MAXNV, c->z)));
     BF_LAUNCH(c);
