@@ -124,6 +124,43 @@ bf_status bf_solve(bf_handle h, const double *rhs, double *x, double tol, int32_
  * (validation errors), otherwise it must be destroyed. */
 bf_status bf_update(bf_handle h, const double *vals, int32_t mem, void *cuda_stream);
 
+/* ---- NEXT-2: device assembly of the two-phase residual and Jacobian ------------------
+ * The fully implicit (p_w, S_n) TPFA discretisation of P:L43-83 with the readings of
+ * DESIGN.md R2 (the same model as the seeded generator workload/twophase.py): uniform
+ * grid of cell size h, isotropic per-cell permeability, quadratic k_r, P_c model
+ * (pc_kind 0 none, 1 Brooks-Corey (a = P_d, b = lambda), 2 van Genuchten (a = n,
+ * b = alpha), 3 linear (a = P_0)), gravity along gravity_axis (-1: none), Dirichlet faces
+ * (axis, side 0 = low / 1 = high, pressure; S_n of the boundary state = S_n^n of the cell),
+ * optional water mass source [kg/s]. All array pointers are DEVICE pointers. */
+typedef struct {
+  int32_t nx, ny, nz;
+  double h, phi, rho_w, rho_n, mu_w, mu_n, g, dt;
+  int32_t gravity_axis;
+  int32_t pc_kind;
+  double pc_a, pc_b;
+  int32_t n_dirichlet;
+  int32_t dir_axis[6], dir_side[6];
+  double dir_p[6];
+  const double *perm;      /* [n] m^2 */
+  const double *sn_old;    /* [n] S_n^n */
+  const double *source_w;  /* [n] kg/s or NULL */
+} bf_twophase;
+
+/* Number of 2x2 blocks of the assembled Jacobian: n + 2 * (interior faces). */
+int64_t bf_assemble_nnzb(int32_t nx, int32_t ny, int32_t nz);
+
+/* Assemble R(u) and J(u) at the state (p, S_n) (device arrays of n): writes row_ptr[n+1],
+ * col_idx[nnzb] (ascending, all grid-adjacency blocks), vals[4 nnzb] (row-major,
+ * var_order 0) and residual[2n] interleaved (R_w, R_n) (mass form).  The
+ * Jacobian is exact with frozen upwind directions.  Device buffers. */
+bf_status bf_assemble(const bf_twophase *prob, const double *p, const double *sn, int32_t *row_ptr,
+                      int32_t *col_idx, double *vals, double *residual, void *cuda_stream);
+
+/* Newton state update u <- u + delta (delta interleaved, device arrays): p += dp;
+ * S_n += clip(dS, -chop, chop) then clipped to [0, 1] when chop > 0 (reading R17). */
+bf_status bf_newton_update(int32_t n, double *p, double *sn, const double *delta, double chop,
+                           void *cuda_stream);
+
 /* Free all device memory of the handle (NULL is a no-op). */
 bf_status bf_destroy(bf_handle h);
 

@@ -23,6 +23,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE
 
 # every symbol declared in include/bf.h
 EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_update", "bf_destroy", "bf_last_error", "bf_spmv",
+           "bf_assemble", "bf_assemble_nnzb", "bf_newton_update",
            "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_block",
            "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
 
@@ -48,6 +49,15 @@ class bf_options(C.Structure):
                 ("timing", C.c_int32)]
 
 
+class bf_twophase(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("h", C.c_double), ("phi", C.c_double),
+                ("rho_w", C.c_double), ("rho_n", C.c_double), ("mu_w", C.c_double), ("mu_n", C.c_double),
+                ("g", C.c_double), ("dt", C.c_double), ("gravity_axis", C.c_int32), ("pc_kind", C.c_int32),
+                ("pc_a", C.c_double), ("pc_b", C.c_double), ("n_dirichlet", C.c_int32),
+                ("dir_axis", C.c_int32 * 6), ("dir_side", C.c_int32 * 6), ("dir_p", C.c_double * 6),
+                ("perm", C.c_void_p), ("sn_old", C.c_void_p), ("source_w", C.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1611_00127_b200.build` "
@@ -59,6 +69,9 @@ def _load():
     L.bf_setup.argtypes = [P(bf_bsr2), P(bf_options), vp, P(vp)]
     L.bf_solve.argtypes = [vp, vp, vp, C.c_double, i32, i32, i32, P(i32), dp, P(i32), dp, vp]
     L.bf_update.argtypes = [vp, vp, i32, vp]
+    L.bf_assemble.argtypes = [P(bf_twophase), vp, vp, vp, vp, vp, vp, vp]
+    L.bf_assemble_nnzb.argtypes = [i32, i32, i32]
+    L.bf_newton_update.argtypes = [i32, vp, vp, vp, C.c_double, vp]
     L.bf_destroy.argtypes = [vp]
     L.bf_last_error.argtypes = [vp]
     L.bf_last_error.restype = C.c_char_p
@@ -72,8 +85,9 @@ def _load():
     L.bf_launch_count.argtypes = [vp, P(i64)]
     L.bf_device_bytes.argtypes = [vp, P(i64)]
     for name in EXPORTS:
-        L[name].restype = L[name].restype if name == "bf_last_error" else C.c_int
+        L[name].restype = C.c_int
     L.bf_last_error.restype = C.c_char_p
+    L.bf_assemble_nnzb.restype = C.c_int64
     return L
 
 
@@ -139,6 +153,25 @@ def bf_update(h, vals, stream=None):
     """New Jacobian values on the setup's pattern (frozen coarse hierarchy, R16)."""
     v, m = _ptr(vals)
     _check(lib.bf_update(h, v, m, _stream(stream)), h)
+
+
+def bf_assemble_nnzb(nx, ny, nz) -> int:
+    return int(lib.bf_assemble_nnzb(nx, ny, nz))
+
+
+def bf_assemble(prob: bf_twophase, p, sn, row_ptr, col_idx, vals, residual, stream=None):
+    """Device assembly of R(u) and J(u) (NEXT-2); every array a CUDA tensor."""
+    args = [_ptr(a) for a in (p, sn, row_ptr, col_idx, vals, residual)]
+    if any(m != 1 for _, m in args):
+        raise ValueError("bf_assemble takes device arrays")
+    _check(lib.bf_assemble(C.byref(prob), *[a for a, _ in args], _stream(stream)), None)
+
+
+def bf_newton_update(p, sn, delta, chop=0.2, stream=None):
+    (pp, m0), (sp, m1), (dp, m2) = _ptr(p), _ptr(sn), _ptr(delta)
+    if (m0, m1, m2) != (1, 1, 1):
+        raise ValueError("bf_newton_update takes device arrays")
+    _check(lib.bf_newton_update(int(p.shape[0]), pp, sp, dp, chop, _stream(stream)), None)
 
 
 def bf_destroy(h):

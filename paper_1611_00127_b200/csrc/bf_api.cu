@@ -1,6 +1,7 @@
 // bf_api.cu -- the C-ABI entry points of libbf.so (include/bf.h), handle and memory
 // management, error translation.  No exception crosses the ABI.
 #include <chrono>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <cstdio>
@@ -97,6 +98,16 @@ void *dalloc(bf_ctx *c, size_t bytes) {
   c->allocs.emplace_back(p, sc);
   c->dev_bytes += (int64_t)sc;
   return p;
+}
+
+void release_all(bf_ctx *c) {  // caller has synchronised
+  for (auto &a : c->allocs) c->pending_free.push_back(a);
+  c->allocs.clear();
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    for (auto &f : c->pending_free) g_dev_free.emplace(f.second, f.first);
+  }
+  c->pending_free.clear();
 }
 
 // blocks freed since the last sync of this handle become reusable after the sync
@@ -326,6 +337,47 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
   sync(c);
   return BF_OK;
   BF_GUARD_END(c)
+}
+
+int64_t bf_assemble_nnzb(int32_t nx, int32_t ny, int32_t nz) {
+  int64_t n = (int64_t)nx * ny * nz;
+  int64_t faces = (int64_t)(nx - 1) * ny * nz + (int64_t)nx * (ny - 1) * nz + (int64_t)nx * ny * (nz - 1);
+  return n + 2 * faces;
+}
+
+// stand-alone calls (no handle): a transient context for the stream, scratch memory and errors
+static bf_status run_transient(void *stream, const std::function<void(bf_ctx *)> &fn) {
+  g_setup_err.clear();
+  bf_ctx c;
+  c.stream = (cudaStream_t)stream;
+  try {
+    fn(&c);
+    bf::sync(&c);
+  } catch (const Error &e) {
+    g_setup_err = e.msg;
+    cudaStreamSynchronize(c.stream);
+    bf::release_all(&c);
+    return e.st;
+  }
+  bf::release_all(&c);
+  return BF_OK;
+}
+
+bf_status bf_assemble(const bf_twophase *P, const double *p, const double *sn, int32_t *row_ptr, int32_t *col_idx,
+                      double *vals, double *residual, void *stream) {
+  if (!P) {
+    g_setup_err = "bf_assemble: prob must be non-NULL";
+    return BF_ERR_ARG;
+  }
+  return run_transient(stream, [&](bf_ctx *c) { assemble(c, P, p, sn, row_ptr, col_idx, vals, residual); });
+}
+
+bf_status bf_newton_update(int32_t n, double *p, double *sn, const double *delta, double chop, void *stream) {
+  if (n < 1 || !p || !sn || !delta) {
+    g_setup_err = "bf_newton_update: bad argument";
+    return BF_ERR_ARG;
+  }
+  return run_transient(stream, [&](bf_ctx *c) { newton_update(c, n, p, sn, delta, chop); });
 }
 
 bf_status bf_destroy(bf_handle h) {

@@ -130,6 +130,7 @@ void timer_begin(bf_ctx *c, int k, cudaEvent_t *start);
 void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes = 0.0);
 void timer_flush(bf_ctx *c);
 void sync(bf_ctx *c);  // counted, timed cudaStreamSynchronize
+void release_all(bf_ctx *c);  // return every block of c to the cache (after a sync)
 
 #define BF_CUDA(x) ::bf::cuda_check((x), #x)
 #define BF_LAUNCH(c) ((c)->launches++)
@@ -159,6 +160,9 @@ void vcycle(bf_ctx *c, int which, const double *b, double *x);          // k_vcy
 void bf_apply(bf_ctx *c, const double *v, double *z);                   // k_vcycle.cu
 void bf_apply_graph(bf_ctx *c, const double *v, double *z);             // k_vcycle.cu
 void alloc_solve_workspace(bf_ctx *c, int restart);                     // k_gmres.cu
+void assemble(bf_ctx *c, const bf_twophase *P, const double *p, const double *sn, int32_t *rp, int32_t *ci,
+              double *vals, double *R);                                   // k_assemble.cu
+void newton_update(bf_ctx *c, int n, double *p, double *sn, const double *delta, double chop);
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
 

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "bf.h")).read()
-    return sorted(set(re.findall(r"^(?:bf_status|const char \*)\s*(bf_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:bf_status|const char \*|int64_t)\s*(bf_\w+)\s*\(", src, re.M)))
 
 
 def _build():
@@ -40,12 +40,13 @@ def test_sm100a_code_and_no_oracle_link():
     assert "sm_100a" in out
     deps = subprocess.run(["ldd", so], capture_output=True, text=True).stdout
     assert "oracle" not in deps
-    # the product path never imports the oracle
+    # the product path never imports, includes or loads the oracle
     pkg = os.path.join(ROOT, "paper_1611_00127_b200")
+    bad = re.compile(r"(^\s*(import|from)\s+oracle\b)|liboracle|oracle\.h|oracle/|import_module\(.oracle", re.M)
     for dp, _, files in os.walk(pkg):
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
-                assert "oracle" not in open(os.path.join(dp, f)).read().replace("oracle.", ""), f
+                assert not bad.search(open(os.path.join(dp, f)).read()), f
 
 
 def test_default_options_without_gpu():
