@@ -160,7 +160,13 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   int g = 1;
   if (force_g > 0) {
     g = force_g;
-  } else if (!stencil) {
+  } else if (stencil) {
+    // lane-per-row gathers are ideal for stencil rows, but a 256-row tile of long rows (S~:
+    // ~12/row) needs ~100 KB for two stages -> 2 CTAs/SM; two lanes per row keep 128-row tiles
+    const char *e = getenv("BF_STENCIL_G2");
+    double lim = e ? atof(e) : 8.0;
+    if (mean > lim) g = 2;
+  } else {
     const char *e = getenv("BF_TMA_G");
     double div = e ? atof(e) : 3.0;
     while (g < 32 && 2 * g <= mean / div) g <<= 1;
