@@ -135,6 +135,9 @@ void free_csr(bf_ctx *c, DCsr &A) {
   dfree(c, A.rp);
   dfree(c, A.ci);
   dfree(c, A.v);
+  dfree(c, A.lidx);
+  dfree(c, A.ucol);
+  dfree(c, A.uoff);
   A = DCsr();
 }
 

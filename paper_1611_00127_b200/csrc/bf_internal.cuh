@@ -26,6 +26,9 @@ struct DCsr {
   int32_t rpt = 0, cap = 0;  // TMA tiling: rows per tile, max nonzeros per tile (0: not tiled)
   int32_t g = 1;             // lanes per row in the TMA kernel
   int32_t stages = 2;        // TMA pipeline depth
+  int16_t *lidx = nullptr;   // local-index variant (k_csr_lx.cuh): per-nonzero index into its tile's U_t
+  int32_t *ucol = nullptr, *uoff = nullptr;  // concatenated U_t, tile offsets
+  int32_t ucap = 0;
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
 };
@@ -152,6 +155,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);                                     // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
+void setup_lx(bf_ctx *c, DCsr &A);                                      // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
 void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu

@@ -1066,10 +1066,13 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.r = dalloc_t<double>(c, n);
     L.t = dalloc_t<double>(c, n);
     tile_csr(c, L.A, k == 0);
+    if (k > 0) setup_lx(c, L.A);
     if (k < h.nlev - 1) {
       const char *gp = getenv("BF_TMA_G_P"), *gr = getenv("BF_TMA_G_R");
       tile_csr(c, L.P, false, gp ? atoi(gp) : 0);
       tile_csr(c, L.R, false, gr ? atoi(gr) : 0);
+      setup_lx(c, L.P);
+      setup_lx(c, L.R);
     }
   }
   BF_CUDA(cudaGetLastError());

@@ -193,9 +193,14 @@ void launch_csr_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, 
 }
 
 template <int MODE>
+bool csr_op_lx(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+               double *aux, double alpha, double beta, const double *dir);
+
+template <int MODE>
 bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir) {
   if (A.cap <= 0) return false;
+  if (csr_op_lx<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return true;
   switch (A.g) {
     case 1: launch_csr_tma<MODE, 1>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
     case 2: launch_csr_tma<MODE, 2>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
@@ -211,3 +216,5 @@ bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, cons
 }
 
 }  // namespace bf
+
+#include "k_csr_lx.cuh"

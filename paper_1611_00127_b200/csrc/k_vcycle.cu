@@ -6,6 +6,7 @@
 #include "bf_internal.cuh"
 #include "k_spmv.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -197,6 +198,52 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
     if (rpt == 8) break;  // rows too long for a staged tile: generic warp kernel
   }
   dfree(c, mx);
+}
+
+__global__ void k_imax(int n, const int32_t *__restrict__ a, int *mx) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicMax(mx, a[i]);
+}
+
+// local-index (per-tile unique column) form of a tiled Galerkin / transfer matrix, used when
+// a tile's nonzeros reuse their x entries at least 1.5 times on average (k_csr_lx.cuh)
+void setup_lx(bf_ctx *c, DCsr &A) {
+  // opt-in (BF_LX=1): measured on C3, tile reuse is only 1.3-2.1 at the 32-64-row tiles the
+  // smem budget allows, and the extra gather phase made the V-cycle 1.5 % slower overall
+  if (!getenv("BF_LX") || A.cap <= 0 || A.cap > LX_SORT || A.nnz == 0) return;
+  int ntiles = (A.n + A.rpt - 1) / A.rpt;
+  int32_t *ucnt = dalloc_t<int32_t>(c, ntiles);
+  int grid = std::min(ntiles, c->num_sms * 8);
+  k_lx_count<<<grid, 256, 0, c->stream>>>(A, A.rpt, ntiles, ucnt);
+  BF_LAUNCH(c);
+  int *mx = dalloc_t<int>(c, 1);
+  BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
+  k_imax<<<div_up(ntiles, 256), 256, 0, c->stream>>>(ntiles, ucnt, mx);
+  BF_LAUNCH(c);
+  int32_t *uoff = dalloc_t<int32_t>(c, (size_t)ntiles + 1);
+  int64_t total = exclusive_scan_i32(c, ucnt, uoff, ntiles);
+  int ucap = 0;
+  BF_CUDA(cudaMemcpyAsync(&ucap, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, ucnt);
+  dfree(c, mx);
+  double reuse = total > 0 ? (double)A.nnz / total : 0.0;
+  if (getenv("BF_VERBOSE"))
+    fprintf(stderr, "[bf_setup]   lx candidate n=%d nnz=%lld rpt=%d g=%d cap=%d ucap=%d reuse=%.2f\n", A.n,
+            (long long)A.nnz, A.rpt, A.g, A.cap, ucap, reuse);
+  int smem = 2 * lx_stage_bytes(A.cap, A.rpt, ucap) + 8 * (ucap + 8);
+  const char *er = getenv("BF_LX_REUSE");
+  if (reuse < (er ? atof(er) : 1.5) || smem > 110 * 1024) {
+    dfree(c, uoff);
+    return;
+  }
+  A.uoff = uoff;
+  A.ucap = ucap;
+  A.ucol = dalloc_t<int32_t>(c, (size_t)total + 8);
+  A.lidx = dalloc_t<int16_t>(c, (size_t)A.nnz + 16);
+  k_lx_fill<<<grid, 256, 0, c->stream>>>(A, A.rpt, ntiles, A.uoff, A.ucol, A.lidx);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
 }
 
 // beta of the first smoothing step from x = 0: x0 = beta b ./ dl1
