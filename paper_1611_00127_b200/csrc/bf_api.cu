@@ -298,6 +298,7 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     lap("schur");
     tile_csr(c, c->blk[1]);
     if (getenv("BF_NO_TMA")) c->use_tma = false;
+    if (getenv("BF_NO_PDL")) c->use_pdl = false;
     build_hierarchy(c, 0, c->blk[3]);
     lap("amg A_ss");
     build_hierarchy(c, 1, c->blk[4]);

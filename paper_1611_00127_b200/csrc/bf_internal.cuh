@@ -108,6 +108,7 @@ struct bf_ctx {
   int64_t apply_graph_kernels = 0;
   int num_sms = 148;
   bool use_tma = true;
+  bool use_pdl = true;  // programmatic dependent launch for the TMA CSR kernels
   double alloc_ms = 0.0;
   double alg_bytes = 0.0;       // running algorithmic-bytes counter (csr_op, vector kernels)
   double apply_bytes = 0.0;     // algorithmic bytes of one BF apply (set at graph capture)

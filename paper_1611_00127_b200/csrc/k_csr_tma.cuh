@@ -45,6 +45,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// programmatic dependent launch (PDL): wait for the preceding kernel's memory / allow the next
+// kernel to begin launching.  No-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -105,9 +112,15 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
   };
 
   int t = blockIdx.x;
-  if (t >= ntiles) return;
+  if (t >= ntiles) {
+    pdl_wait();
+    return;
+  }
+  // the matrix is setup data: its first tiles are fetched BEFORE waiting for the previous
+  // kernel of the V-cycle (programmatic dependent launch), overlapping that kernel's tail
   if (tid == 0)
     for (int s = 0; s < ST && t + s * (int)gridDim.x < ntiles; s++) issue(t + s * gridDim.x, s);
+  pdl_wait();  // x, b, dinv, dir and the outputs are touched only after this
   const int sub = tid % G;
   for (int it = 0; t < ntiles; t += gridDim.x, it++) {
     int s = it % ST;
@@ -155,6 +168,7 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
     __syncthreads();  // every thread is done with stage s
     if (tid == 0 && t + ST * (int)gridDim.x < ntiles) issue(t + ST * gridDim.x, s);
   }
+  pdl_launch_dependents();  // this CTA is done: the next kernel may start its prologue
 }
 
 // per-tile nonzero count -> max (setup helper)
@@ -178,8 +192,18 @@ void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *
   int ntiles = (A.n + A.rpt - 1) / A.rpt;
   int per_sm = std::max(1, std::min(8, (220 * 1024) / (smem + 1024)));
   int grid = std::min(ntiles, c->num_sms * per_sm);
-  k_csr_tma<MODE, G, ST><<<grid, TMA_THREADS, smem, c->stream>>>(A.n, A.rpt, ntiles, A.cap, A.rp, A.ci, A.v, x, b,
-                                                                 dinv, y, aux, alpha, beta, dir);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TMA_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, k_csr_tma<MODE, G, ST>, A.n, A.rpt, ntiles, A.cap, (const int32_t *)A.rp,
+                             (const int32_t *)A.ci, (const double *)A.v, x, b, dinv, y, aux, alpha, beta, dir));
 }
 
 template <int MODE, int G>
