@@ -245,3 +245,43 @@ def test_setup_reuse_update_parity(config, dims):
         assert abs(r["iters"] - ro["iters"]) <= 1 and r["converged"] == ro["converged"]
         for f in (0, 1):
             assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+
+
+@pytest.mark.parametrize("opts", [dict(max_levels=1), dict(max_levels=2), dict(max_levels=2, smoother=1),
+                                  dict(max_coarse=128), dict(theta=0.9), dict(nu_pre=3, nu_post=0),
+                                  dict(nu_pre=0, nu_post=2), dict(smoother=1, cheb_degree=3, cheb_lo=0.1),
+                                  dict(seed=12345)])
+def test_option_edge_cases(opts):
+    """Less common option combinations: single-level and stalled hierarchies (4 l1-Jacobi sweeps
+    on a non-dense coarsest level), the largest dense coarse solve, asymmetric smoothing."""
+    prob, J, rhs = make_system(2, dims=(13, 12, 11))
+    o = oracle.BF(J, **opts)
+    g = gpu_solver(J, prob.dims, **opts)
+    for which in (0, 1):
+        assert g.num_levels(which) == o.nlev(which)
+    v = seeded_vector(2 * J.n, 8)
+    z = np.zeros(2 * J.n)
+    g.apply_precond(v, z)
+    zo = o.apply(v)
+    assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo), opts
+    k = 40
+    ro = o.gmres(rhs, tol=0.0, maxit=k)
+    x = np.zeros(2 * J.n)
+    r = g.solve(rhs, x, tol=0.0, maxit=k)
+    assert r["iters"] == ro["iters"] == k
+    for f in (0, 1):
+        assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2]), opts
+
+
+@pytest.mark.parametrize("restart", [1, 7, 32])
+def test_restart_lengths(restart):
+    prob, J, rhs = make_system(1, dims=(20, 18, 1))
+    o = oracle.BF(J)
+    g = gpu_solver(J, prob.dims)
+    ro = o.gmres(rhs, tol=1e-8, restart=restart, maxit=400)
+    x = np.zeros(2 * J.n)
+    r = g.solve(rhs, x, tol=1e-8, restart=restart, maxit=400)
+    assert abs(r["iters"] - ro["iters"]) <= 1 and r["converged"] == ro["converged"]
+    if ro["converged"]:
+        for f in (0, 1):
+            assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
