@@ -136,6 +136,7 @@ void free_csr(bf_ctx *c, DCsr &A) {
   dfree(c, A.ci);
   dfree(c, A.v);
   dfree(c, A.lidx);
+  dfree(c, A.dia_v);
   dfree(c, A.ucol);
   dfree(c, A.uoff);
   A = DCsr();
@@ -297,6 +298,7 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     build_schur(c);
     lap("schur");
     tile_csr(c, c->blk[1]);
+    setup_dia(c, c->blk[1]);
     if (getenv("BF_NO_TMA")) c->use_tma = false;
     if (getenv("BF_NO_PDL")) c->use_pdl = false;
     build_hierarchy(c, 0, c->blk[3]);
@@ -336,6 +338,7 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
   build_split(c);
   build_schur(c);
   tile_csr(c, c->blk[1]);
+  setup_dia(c, c->blk[1]);
   refresh_finest(c, 0, c->blk[3]);
   refresh_finest(c, 1, c->blk[4]);
   sync(c);

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,9 @@ struct DCsr {
   int16_t *lidx = nullptr;   // local-index variant (k_csr_lx.cuh): per-nonzero index into its tile's U_t
   int32_t *ucol = nullptr, *uoff = nullptr;  // concatenated U_t, tile offsets
   int32_t ucap = 0;
+  double *dia_v = nullptr;   // DIA storage of a grid-structured finest-level matrix (k_dia.cuh)
+  int32_t dia_k = 0;
+  int32_t *dia_off = nullptr;  // host array of dia_k offsets (kept out of the by-value kernel struct)
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
 };
@@ -73,6 +77,7 @@ struct bf_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int32_t n = 0;  // cells
+  int32_t nx = 0, ny = 0, nz = 0;
   int64_t nnzb = 0;
   int32_t var_order = 0;
   int32_t block_order = 0;
@@ -109,6 +114,7 @@ struct bf_ctx {
   int num_sms = 148;
   bool use_tma = true;
   bool use_pdl = true;  // programmatic dependent launch for the TMA CSR kernels
+  std::deque<std::vector<int32_t>> dia_offsets;  // storage behind DCsr::dia_off
   double alloc_ms = 0.0;
   double alg_bytes = 0.0;       // running algorithmic-bytes counter (csr_op, vector kernels)
   double apply_bytes = 0.0;     // algorithmic bytes of one BF apply (set at graph capture)
@@ -157,6 +163,7 @@ void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);                                     // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
 void setup_lx(bf_ctx *c, DCsr &A);                                      // k_vcycle.cu
+void setup_dia(bf_ctx *c, DCsr &A);                                     // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
 void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu

@@ -1066,6 +1066,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.r = dalloc_t<double>(c, n);
     L.t = dalloc_t<double>(c, n);
     tile_csr(c, L.A, k == 0);
+    if (k == 0) setup_dia(c, L.A);
     if (k > 0) setup_lx(c, L.A);
     if (k < h.nlev - 1) {
       const char *gp = getenv("BF_TMA_G_P"), *gr = getenv("BF_TMA_G_R");
@@ -1123,6 +1124,7 @@ void refresh_finest(bf_ctx *c, int which, const DCsr &A0) {
   BF_CUDA(cudaGetLastError());
   dfree(c, diag);
   tile_csr(c, L.A, true);
+  setup_dia(c, L.A);
   plan_tail(c, h);
 }
 

@@ -79,6 +79,9 @@ void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J) {
   int n = J->n_cells;
   int64_t nnzb = J->nnzb;
   c->n = n;
+  c->nx = J->nx;
+  c->ny = J->ny;
+  c->nz = J->nz;
   c->nnzb = nnzb;
   c->var_order = J->var_order;
   c->block_order = J->block_order;

@@ -106,6 +106,9 @@ inline int lanes_for(const bf_ctx *c, const DCsr &A) {
 template <int MODE>
 bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir);
+template <int MODE>
+bool csr_op_dia(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                double *aux, double alpha, double beta, const double *dir);
 
 // algorithmic bytes of one csr_op (each operand once: int32 index, f64 value; x counted once
 // per column); accumulated into c->alg_bytes so a captured BF apply knows its own traffic
@@ -128,6 +131,7 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
             double *aux, double alpha, double beta, const double *dir) {
   if (A.n == 0) return;
   c->alg_bytes += csr_op_bytes<MODE>(A, dir != nullptr, aux != nullptr);
+  if (csr_op_dia<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (c->use_tma && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   int G = lanes_for(c, A);
   int rows_per_block = (32 / G) * CSR_WARPS;
@@ -153,3 +157,4 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
 }  // namespace bf
 
 #include "k_csr_tma.cuh"
+#include "k_dia.cuh"

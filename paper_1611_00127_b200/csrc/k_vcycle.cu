@@ -5,6 +5,9 @@
 //   s = V_Ass(R_s v);  r' = R_p v - A_ps s;  p = V_S~(r');  z = R_p^T p + R_s^T s.
 #include "bf_internal.cuh"
 #include "k_spmv.cuh"
+#include "k_dia.cuh"
+
+#include <algorithm>
 
 #include <cstdio>
 #include <cstdlib>
@@ -242,6 +245,49 @@ void setup_lx(bf_ctx *c, DCsr &A) {
   A.ucol = dalloc_t<int32_t>(c, (size_t)total + 8);
   A.lidx = dalloc_t<int16_t>(c, (size_t)A.nnz + 16);
   k_lx_fill<<<grid, 256, 0, c->stream>>>(A, A.rpt, ntiles, A.uoff, A.ucol, A.lidx);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
+// DIA form of a finest-level matrix whose nonzeros all sit on a few grid-stencil offsets
+void setup_dia(bf_ctx *c, DCsr &A) {
+  if (getenv("BF_NO_DIA") || A.n == 0 || A.n != A.m || c->nx <= 0) return;
+  std::vector<int> cand;
+  int64_t sx = 1, sy = c->nx, sz = (int64_t)c->nx * c->ny;
+  for (int cz = -2; cz <= 2; cz++)
+    for (int cy = -2; cy <= 2; cy++)
+      for (int cx = -2; cx <= 2; cx++) {
+        int64_t o = cx * sx + cy * sy + cz * sz;
+        if (o > -(int64_t)A.n && o < A.n) cand.push_back((int)o);
+      }
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  int nc = (int)cand.size();
+  int *dcand = dalloc_t<int>(c, nc), *pres = dalloc_t<int>(c, nc + 1);
+  BF_CUDA(cudaMemcpyAsync(dcand, cand.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, c->stream));
+  BF_CUDA(cudaMemsetAsync(pres, 0, sizeof(int) * (nc + 1), c->stream));
+  k_dia_mark<<<div_up(A.n, 256), 256, 0, c->stream>>>(A, dcand, nc, pres, pres + nc);
+  BF_LAUNCH(c);
+  std::vector<int> hp(nc + 1);
+  BF_CUDA(cudaMemcpyAsync(hp.data(), pres, sizeof(int) * (nc + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, dcand);
+  dfree(c, pres);
+  if (hp[nc]) return;  // an offset outside the candidate stencil
+  DiaOffsets o;
+  o.k = 0;
+  for (int q = 0; q < nc; q++)
+    if (hp[q]) {
+      if (o.k == DIA_MAXK) return;
+      o.off[o.k++] = cand[q];
+    }
+  double fill = (double)A.nnz / ((double)o.k * A.n);
+  if (fill < 0.75) return;
+  A.dia_v = dalloc_t<double>(c, (size_t)o.k * A.n);
+  A.dia_k = o.k;
+  c->dia_offsets.emplace_back(o.off, o.off + o.k);
+  A.dia_off = c->dia_offsets.back().data();
+  k_dia_fill<<<div_up(A.n, 256), 256, 0, c->stream>>>(A, o, A.dia_v);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
 }
