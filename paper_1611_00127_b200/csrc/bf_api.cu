@@ -292,6 +292,7 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
       t0 = t1;
     };
     validate_and_ingest(c, J);
+    setup_bsr_dia(c);
     lap("ingest");
     build_split(c);
     lap("split");
@@ -331,6 +332,7 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
   c->stream = (cudaStream_t)stream;
   c->err.clear();
   reingest_values(c, vals, mem);  // validation first: the handle is untouched on BF_ERR_NONFINITE
+  setup_bsr_dia(c);
   drop_apply_graph(c);
   for (int b = 0; b < 5; b++) free_csr(c, c->blk[b]);
   dfree(c, c->dss);

@@ -39,6 +39,7 @@ struct DCsr {
 
 struct Level {
   DCsr A, P, R;
+  DCsr Rf;  // fused restriction R (I - beta A D^-1) of the seeded pre-smoother's residual (k_amg_setup.cu)
   int8_t *cf = nullptr;
   double *dl1 = nullptr;
   double *b = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
@@ -83,6 +84,8 @@ struct bf_ctx {
   int32_t block_order = 0;
   int32_t *brp = nullptr, *bci = nullptr;
   double *bv = nullptr;  // canonical (p,s) row-major blocks
+  double *jdia = nullptr;  // DIA copy of J (7 block diagonals), k_spmv.cu
+  int32_t jdia_k = 0, jdia_off[8] = {0};
   bf::DCsr blk[5];       // A_pp, A_ps, A_sp, A_ss, S~
   double *dss = nullptr;
   bf::Hier h[2];
@@ -160,13 +163,16 @@ void drop_apply_graph(bf_ctx *c);                                       // k_vcy
 void build_schur(bf_ctx *c);                                            // k_split.cu
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
-void plan_tail(bf_ctx *c, Hier &h);                                     // k_vcycle.cu
+void plan_tail(bf_ctx *c, Hier &h);
+void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
+double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu                                     // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
 void setup_lx(bf_ctx *c, DCsr &A);                                      // k_vcycle.cu
 void setup_dia(bf_ctx *c, DCsr &A);                                     // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
 void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spmv.cu
+void setup_bsr_dia(bf_ctx *c);                                          // k_spmv.cu
 void csr_spmv(bf_ctx *c, const DCsr &A, const double *x, double *y);    // k_spmv.cu
 void vcycle(bf_ctx *c, int which, const double *b, double *x);          // k_vcycle.cu
 void bf_apply(bf_ctx *c, const double *v, double *z);                   // k_vcycle.cu

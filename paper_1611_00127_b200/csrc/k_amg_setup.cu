@@ -467,20 +467,23 @@ __global__ void k_spgemm_ub(DCsr A, DCsr B, int64_t *ub) {
   ub[i] = s;
 }
 
+// warp per row of A; product (q, t) lands at the same position as in a serial row loop
+// (k ascending, then B's row order), so the stable sort keeps the ascending-k order of equal keys
 __global__ void k_spgemm_expand(DCsr A, DCsr B, const int64_t *__restrict__ off, int colbits, uint64_t *keys,
                                 double *vals) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (i >= A.n) return;
   int64_t p = off[i];
   uint64_t hi = (uint64_t)i << colbits;
   for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
     double a = A.v[q];
     int k = A.ci[q];
-    for (int t = B.rp[k]; t < B.rp[k + 1]; t++) {
-      keys[p] = hi | (uint64_t)B.ci[t];
-      vals[p] = __dmul_rn(a, B.v[t]);
-      p++;
+    int bs = B.rp[k], be = B.rp[k + 1];
+    for (int t = bs + lane; t < be; t += 32) {
+      keys[p + (t - bs)] = hi | (uint64_t)B.ci[t];
+      vals[p + (t - bs)] = __dmul_rn(a, B.v[t]);
     }
+    p += be - bs;
   }
 }
 
@@ -554,28 +557,59 @@ __device__ __forceinline__ int hash_insert(int *keys, int key, int mask, bool &i
   }
 }
 
+// the row's A entries (column k, value a) and B row bounds are loaded lane-parallel, 32 at
+// a time, and broadcast by shuffles: the per-k dependent chain is then one B load, not three
+struct RowChunk {
+  int k, bs, be;
+  double a;
+};
+__device__ __forceinline__ RowChunk load_chunk(const DCsr &A, const DCsr &B, int q, int r1, bool want_a) {
+  RowChunk c{0, 0, 0, 0.0};
+  if (q < r1) {
+    c.k = A.ci[q];
+    if (want_a) c.a = A.v[q];
+    c.bs = B.rp[c.k];
+    c.be = B.rp[c.k + 1];
+  }
+  return c;
+}
+__device__ __forceinline__ int chunk_mask(const DCsr &A, const DCsr &B, int i, int lane, int len, const RowChunk &c) {
+  if (len > 32) return row_table_mask(A, B, i, lane);
+  int ub = c.be - c.bs;
+  for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+  int t = 32;
+  while (t < HASH_CAP && t < 2 * ub) t <<= 1;
+  return t - 1;
+}
+
 __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, DCsr B, int32_t *cnt, int *overflow) {
   __shared__ int skeys[HASH_WARPS][HASH_CAP];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int i = blockIdx.x * HASH_WARPS + warp;
   if (i >= A.n) return;
   int *keys = skeys[warp];
-  int mask = row_table_mask(A, B, i, lane);
+  const int r0 = A.rp[i], r1 = A.rp[i + 1];
+  RowChunk ch = load_chunk(A, B, r0 + lane, r1, false);
+  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch);
   for (int s = lane; s <= mask; s += 32) keys[s] = -1;
   __syncwarp();
   int count = 0;
   bool full = false;
-  for (int q = A.rp[i]; q < A.rp[i + 1] && !full; q++) {
-    int k = A.ci[q];
-    for (int t = B.rp[k] + lane; t < B.rp[k + 1]; t += 32) {
-      bool ins;
-      hash_insert(keys, B.ci[t], mask, ins);
-      count += ins;
+  for (int q0 = r0; q0 < r1 && !full; q0 += 32) {
+    if (q0 != r0) ch = load_chunk(A, B, q0 + lane, r1, false);
+    int nq = min(32, r1 - q0);
+    for (int u = 0; u < nq && !full; u++) {
+      int bs = __shfl_sync(0xffffffffu, ch.bs, u), be = __shfl_sync(0xffffffffu, ch.be, u);
+      for (int t = bs + lane; t < be; t += 32) {
+        bool ins;
+        hash_insert(keys, B.ci[t], mask, ins);
+        count += ins;
+      }
+      // stop early once the row cannot fit (the product then falls back to the ESC path)
+      int tot = count;
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      full = tot > HASH_MAX;
     }
-    // stop early once the row cannot fit (the product then falls back to the ESC path)
-    int tot = count;
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    full = tot > HASH_MAX;
   }
   for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
   if (lane == 0) {
@@ -596,19 +630,42 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DC
   double *cvals = reinterpret_cast<double *>(wb + HASH_CAP * 8);
   int *keys = reinterpret_cast<int *>(wb + HASH_CAP * 8 + HASH_MAX * 8);
   int *ckeys = keys + HASH_CAP;
-  int mask = row_table_mask(A, B, i, lane);
+  const int r0 = A.rp[i], r1 = A.rp[i + 1];
+  RowChunk ch = load_chunk(A, B, r0 + lane, r1, true);
+  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch);
   for (int s = lane; s <= mask; s += 32) keys[s] = -1;
   __syncwarp();
-  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {  // k ascending
-    int k = A.ci[q];
-    double a = A.v[q];
-    for (int t = B.rp[k] + lane; t < B.rp[k + 1]; t += 32) {
-      bool ins;
-      int s = hash_insert(keys, B.ci[t], mask, ins);
-      double acc = ins ? 0.0 : vals[s];
-      vals[s] = __dadd_rn(acc, __dmul_rn(a, B.v[t]));
+  for (int q0 = r0; q0 < r1; q0 += 32) {  // k ascending
+    if (q0 != r0) ch = load_chunk(A, B, q0 + lane, r1, true);
+    int nq = min(32, r1 - q0);
+    // B(k, :) of the first 32 entries of the next k is prefetched while this k is hashed
+    int bs = __shfl_sync(0xffffffffu, ch.bs, 0), be = __shfl_sync(0xffffffffu, ch.be, 0);
+    int nc = bs + lane < be ? B.ci[bs + lane] : -1;
+    double nv = bs + lane < be ? B.v[bs + lane] : 0.0;
+    for (int u = 0; u < nq; u++) {
+      double a = __shfl_sync(0xffffffffu, ch.a, u);
+      int cbs = bs, cbe = be, cc = nc;
+      double cv = nv;
+      if (u + 1 < nq) {
+        bs = __shfl_sync(0xffffffffu, ch.bs, u + 1);
+        be = __shfl_sync(0xffffffffu, ch.be, u + 1);
+        nc = bs + lane < be ? B.ci[bs + lane] : -1;
+        nv = bs + lane < be ? B.v[bs + lane] : 0.0;
+      }
+      if (cc >= 0) {
+        bool ins;
+        int s = hash_insert(keys, cc, mask, ins);
+        double acc = ins ? 0.0 : vals[s];
+        vals[s] = __dadd_rn(acc, __dmul_rn(a, cv));
+      }
+      for (int t = cbs + 32 + lane; t < cbe; t += 32) {  // rows of B longer than 32 (rare)
+        bool ins;
+        int s = hash_insert(keys, B.ci[t], mask, ins);
+        double acc = ins ? 0.0 : vals[s];
+        vals[s] = __dadd_rn(acc, __dmul_rn(a, B.v[t]));
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   // compact the occupied slots, then place each entry at its rank (rows are emitted sorted)
   int n = 0;
@@ -786,7 +843,7 @@ static void spgemm_esc(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   int rowbits = bits_for(A.n);
   uint64_t *keys = dalloc_t<uint64_t>(c, T);
   double *vals = dalloc_t<double>(c, T);
-  k_spgemm_expand<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, off, colbits, keys, vals);
+  k_spgemm_expand<<<div_up((int64_t)A.n * 32, 256), 256, 0, c->stream>>>(A, B, off, colbits, keys, vals);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   dfree(c, off);
@@ -892,6 +949,7 @@ void free_hierarchy(bf_ctx *c, Hier &h) {
     free_csr(c, L.A);
     free_csr(c, L.P);
     free_csr(c, L.R);
+    free_csr(c, L.Rf);
     dfree(c, L.cf);
     dfree(c, L.dl1);
     dfree(c, L.b);
@@ -1101,6 +1159,60 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
                                               std::to_string(hs));
   }
   plan_tail(c, h);
+  build_rfuse(c, h, false);
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused restriction of the pre-smoothed residual.  With one l1-Jacobi pre-sweep from zero the
+// V-cycle's first two steps on level l are x0 = beta D b, r = b - A x0, and the restriction
+// b_c = R r = R (I - beta A D) b, D = diag(1/dl1).  Rf = R M with M = I - beta A D (the
+// pattern of A: the diagonal is structurally present) turns "residual + restriction" into ONE
+// sparse product over b.  Mathematically identical to the two-step form (the rounding order
+// differs; the V-cycle parity tolerance covers it), and it reads nnz(Rf) instead of
+// nnz(A) + nnz(R) and the r round trip.  Built for the CSR levels above the tail (the finest
+// level's DIA residual + restriction is cheaper per byte), default smoother configuration only.
+// ---------------------------------------------------------------------------------------
+static __global__ void k_rfuse_m(DCsr A, const double *__restrict__ d, double beta, double *__restrict__ mv) {
+  int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (i >= A.n) return;
+  for (int q = A.rp[i] + lane; q < A.rp[i + 1]; q += 32) {
+    int j = A.ci[q];
+    double t = (beta * A.v[q]) * d[j];
+    mv[q] = (j == i ? 1.0 : 0.0) - t;
+  }
+}
+
+void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
+  const bf_options &o = c->opt;
+  if (getenv("BF_NO_RFUSE") || o.smoother != 0 || o.nu_pre != 1) return;
+  const bool l0 = getenv("BF_RFUSE_L0") != nullptr;
+  int lend = h.tail >= 0 ? h.tail : h.nlev - 1;
+  for (int l = l0 ? 0 : 1; l < lend; l++) {
+    if (finest_only && l > 0) break;
+    Level &L = h.lv[l];
+    free_csr(c, L.Rf);
+    if (L.A.dia_v && !l0) continue;
+    DCsr M;
+    M.n = L.A.n;
+    M.m = L.A.m;
+    M.nnz = L.A.nnz;
+    M.rp = L.A.rp;
+    M.ci = L.A.ci;
+    M.v = dalloc_t<double>(c, L.A.nnz);
+    k_rfuse_m<<<div_up((int64_t)M.n * 32, 256), 256, 0, c->stream>>>(L.A, L.d, 1.0, M.v);
+    BF_LAUNCH(c);
+    auto t0 = std::chrono::steady_clock::now();
+    spgemm(c, L.R, M, L.Rf);
+    dfree(c, M.v);
+    tile_csr(c, L.Rf, false);
+    if (getenv("BF_VERBOSE")) {
+      sync(c);
+      fprintf(stderr, "[bf_setup]   rfuse L%d: R %lld nnz x M %lld nnz -> %lld nnz, %.2f ms\n", l, (long long)L.R.nnz,
+              (long long)L.A.nnz, (long long)L.Rf.nnz,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  }
+  BF_CUDA(cudaGetLastError());
 }
 
 // Setup reuse (bf_update, reading R16): replace the finest matrix of hierarchy `which` by
@@ -1126,6 +1238,7 @@ void refresh_finest(bf_ctx *c, int which, const DCsr &A0) {
   tile_csr(c, L.A, true);
   setup_dia(c, L.A);
   plan_tail(c, h);
+  if (h.lv[0].Rf.n) build_rfuse(c, h, true);  // the finest level's fused restriction uses A_0
 }
 
 }  // namespace bf

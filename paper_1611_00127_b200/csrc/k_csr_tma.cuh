@@ -13,6 +13,7 @@
 #include "k_spmv.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace bf {
 
@@ -137,6 +138,17 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
       int r = r0 + row_in_tile;
       bool ok = row_in_tile < rpt && r < n;
       int lo = ok ? srp[row_in_tile] : 0, hi = ok ? srp[row_in_tile + 1] : 0;
+      // the epilogue's row operands are loaded before the gathers, so that their latency
+      // overlaps the gather latency instead of following it
+      const bool own = ok && sub == 0;
+      double eb = 0.0, ed = 0.0, ex = 0.0, edir = 0.0;
+      if (own) {
+        if (MODE == OP_RESID || MODE == OP_SUB_X0 || MODE == OP_SMOOTH) eb = __ldg(b + r);
+        if (MODE == OP_SUB_X0 || MODE == OP_SMOOTH || MODE == OP_SPMV_X0) ed = __ldg(dinv + r);
+        if (MODE == OP_SMOOTH) ex = __ldg(x + r);
+        if (MODE == OP_SMOOTH && dir) edir = dir[r];
+        if (MODE == OP_ADD) ex = y[r];
+      }
       double acc = 0.0;
 #pragma unroll 4
       for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
@@ -144,25 +156,25 @@ __global__ void __launch_bounds__(TMA_THREADS) k_csr_tma(int n, int rpt, int nti
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
       }
-      if (!ok || sub != 0) continue;
+      if (!own) continue;
       if (MODE == OP_SPMV) {
         y[r] = acc;
       } else if (MODE == OP_SPMV_X0) {
         y[r] = acc;
-        aux[r] = beta * (acc * dinv[r]);
+        aux[r] = beta * (acc * ed);
       } else if (MODE == OP_RESID) {
-        y[r] = b[r] - acc;
+        y[r] = eb - acc;
       } else if (MODE == OP_SUB_X0) {
-        double tt = b[r] - acc;
+        double tt = eb - acc;
         y[r] = tt;
-        aux[r] = beta * (tt * dinv[r]);
+        aux[r] = beta * (tt * ed);
       } else if (MODE == OP_SMOOTH) {
-        double dn = beta * ((b[r] - acc) * dinv[r]);
-        if (dir) dn += alpha * dir[r];
-        y[r] = x[r] + dn;
+        double dn = beta * ((eb - acc) * ed);
+        if (dir) dn += alpha * edir;
+        y[r] = ex + dn;
         if (aux) aux[r] = dn;
       } else if (MODE == OP_ADD) {
-        y[r] += acc;
+        y[r] = ex + acc;
       }
     }
     __syncthreads();  // every thread is done with stage s
@@ -190,7 +202,12 @@ void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *
   }
   int smem = ST * tma_stage_bytes(A.cap, A.rpt);
   int ntiles = (A.n + A.rpt - 1) / A.rpt;
-  int per_sm = std::max(1, std::min(8, (220 * 1024) / (smem + 1024)));
+  static int max_per_sm = 0;
+  if (!max_per_sm) {
+    const char *e = getenv("BF_TMA_CTAS");
+    max_per_sm = e ? std::max(1, atoi(e)) : 8;
+  }
+  int per_sm = std::max(1, std::min(max_per_sm, (220 * 1024) / (smem + 1024)));
   int grid = std::min(ntiles, c->num_sms * per_sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

@@ -27,6 +27,13 @@ __global__ void __launch_bounds__(256) k_dia(int n, DiaOffsets o, const double *
                                              const double *__restrict__ dir) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
+  // the epilogue's row operands first: their loads overlap the diagonal loads
+  double eb = 0.0, ed = 0.0, ex = 0.0, edir = 0.0;
+  if (MODE == OP_RESID || MODE == OP_SUB_X0 || MODE == OP_SMOOTH) eb = __ldg(b + r);
+  if (MODE == OP_SUB_X0 || MODE == OP_SMOOTH || MODE == OP_SPMV_X0) ed = __ldg(dinv + r);
+  if (MODE == OP_SMOOTH) ex = __ldg(x + r);
+  if (MODE == OP_SMOOTH && dir) edir = dir[r];
+  if (MODE == OP_ADD) ex = y[r];
   double acc = 0.0;
 #pragma unroll 4
   for (int d = 0; d < o.k; d++) {
@@ -38,20 +45,20 @@ __global__ void __launch_bounds__(256) k_dia(int n, DiaOffsets o, const double *
     y[r] = acc;
   } else if (MODE == OP_SPMV_X0) {
     y[r] = acc;
-    aux[r] = beta * (acc * dinv[r]);
+    aux[r] = beta * (acc * ed);
   } else if (MODE == OP_RESID) {
-    y[r] = b[r] - acc;
+    y[r] = eb - acc;
   } else if (MODE == OP_SUB_X0) {
-    double t = b[r] - acc;
+    double t = eb - acc;
     y[r] = t;
-    aux[r] = beta * (t * dinv[r]);
+    aux[r] = beta * (t * ed);
   } else if (MODE == OP_SMOOTH) {
-    double dn = beta * ((b[r] - acc) * dinv[r]);
-    if (dir) dn += alpha * dir[r];
-    y[r] = x[r] + dn;
+    double dn = beta * ((eb - acc) * ed);
+    if (dir) dn += alpha * edir;
+    y[r] = ex + dn;
     if (aux) aux[r] = dn;
   } else if (MODE == OP_ADD) {
-    y[r] += acc;
+    y[r] = ex + acc;
   }
 }
 

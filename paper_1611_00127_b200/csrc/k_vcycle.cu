@@ -8,6 +8,7 @@
 #include "k_dia.cuh"
 
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -27,80 +28,116 @@ __global__ void k_coarse_inv(int n, const double *__restrict__ inv, const double
 }
 
 // ----------------------------------------------------------------------------------------
-// Single-CTA tail of the V-cycle: all levels from h.tail down to the coarsest (each with at
-// most TAIL_NNZ nonzeros, L2-resident) in ONE kernel, __syncthreads between the steps,
-// instead of ~4 launches per level (l1-Jacobi V(1,1), the default configuration).
+// Cooperative tail of the V-cycle: all levels from h.tail down to the coarsest in ONE
+// cooperative kernel (grid-wide barriers between the steps) instead of ~4 launches per level
+// (l1-Jacobi V(1,1), the default configuration).  The coarse levels are latency bound: a
+// level with 10^3..10^4 rows is one short wave, so the launch + ramp of separate kernels, not
+// the bytes, sets their cost.  Rows are owned by groups of g lanes (g ~ mean row length / 2),
+// each group reduces its row in a fixed order; every value has one owner.
 // ----------------------------------------------------------------------------------------
 constexpr int TAIL_MAXL = 12;
 constexpr int TAIL_NNZ = 3000;
-constexpr int TAIL_THREADS = 1024;
+constexpr int TAIL_THREADS = 512;
 
 struct TailLevel {
-  int n;
+  int n, gA, gP, gR;
   const int32_t *Arp, *Aci, *Prp, *Pci, *Rrp, *Rci;
   const double *Av, *Pv, *Rv, *d;
   double *b, *x, *r, *t;
 };
 struct TailParams {
   int nl;  // tail levels including the coarsest
+  int gL;  // lanes per row of the dense coarse solve
   double beta;
   const double *inv;
   TailLevel lv[TAIL_MAXL];
 };
 
-// warp-per-row CSR reduction: returns sum_j a_ij x_j on lane 0 of the warp
-__device__ __forceinline__ double warp_row(const int32_t *rp, const int32_t *ci, const double *v,
-                                           const double *x, int r, int lane) {
+// g-lane group reduction of one CSR row (all lanes of the warp call it; result on lane 0 of
+// the group); ok = this group has a row
+__device__ __forceinline__ double group_row(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                            const double *__restrict__ v, const double *x, int r, bool ok,
+                                            int lig, int g) {
   double s = 0.0;
-  for (int q = rp[r] + lane; q < rp[r + 1]; q += 32) s += v[q] * x[ci[q]];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (ok) {
+    int e = rp[r + 1];
+    for (int q = rp[r] + lig; q < e; q += g) s += v[q] * x[ci[q]];
+  }
+  for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, g);
   return s;
 }
 
 __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = TAIL_THREADS / 32;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   for (int l = 0; l < p.nl - 1; l++) {
     const TailLevel &L = p.lv[l];
-    for (int r = warp; r < L.n; r += nw) {  // r = b - A x0
-      double s = warp_row(L.Arp, L.Aci, L.Av, L.x, r, lane);
-      if (lane == 0) L.r[r] = L.b[r] - s;
-    }
-    __syncthreads();
-    const TailLevel &C = p.lv[l + 1];
-    for (int r = warp; r < C.n; r += nw) {  // b_c = R r ; x0_c = beta b_c ./ dl1_c
-      double s = warp_row(L.Rrp, L.Rci, L.Rv, L.r, r, lane);
-      if (lane == 0) {
-        C.b[r] = s;
-        C.x[r] = p.beta * (s * C.d[r]);
+    {  // r = b - A x0
+      int g = L.gA, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int r = base + tid / g;
+        bool ok = r < L.n;
+        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g);
+        if (ok && lig == 0) L.r[r] = L.b[r] - s;
       }
     }
-    __syncthreads();
+    grid.sync();
+    const TailLevel &C = p.lv[l + 1];
+    {  // b_c = R r ; x0_c = beta b_c ./ dl1_c
+      int g = L.gR, lig = tid & (g - 1);
+      for (int base = 0; base < C.n; base += nth / g) {
+        int r = base + tid / g;
+        bool ok = r < C.n;
+        double s = group_row(L.Rrp, L.Rci, L.Rv, L.r, r, ok, lig, g);
+        if (ok && lig == 0) {
+          C.b[r] = s;
+          C.x[r] = p.beta * (s * C.d[r]);
+        }
+      }
+    }
+    grid.sync();
   }
   {  // coarsest: x = A_L^-1 b
     const TailLevel &L = p.lv[p.nl - 1];
-    for (int i = threadIdx.x; i < L.n; i += TAIL_THREADS) {
+    int g = p.gL, lig = tid & (g - 1);
+    for (int base = 0; base < L.n; base += nth / g) {
+      int i = base + tid / g;
+      bool ok = i < L.n;
       double s = 0.0;
-      for (int j = 0; j < L.n; j++) s += p.inv[(size_t)i * L.n + j] * L.b[j];
-      L.x[i] = s;
+      if (ok)
+        for (int j = lig; j < L.n; j += g) s += p.inv[(size_t)i * L.n + j] * L.b[j];
+      for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, g);
+      if (ok && lig == 0) L.x[i] = s;
     }
-    __syncthreads();
+    grid.sync();
   }
+  // up-sweep; the smoothed result of a tail level stays in its t buffer (the host swaps the
+  // first tail level's x/t pointers, so the caller sees it in L.x)
   for (int l = p.nl - 2; l >= 0; l--) {
     const TailLevel &L = p.lv[l];
     const TailLevel &C = p.lv[l + 1];
-    for (int r = warp; r < L.n; r += nw) {  // x += P e
-      double s = warp_row(L.Prp, L.Pci, L.Pv, C.x, r, lane);
-      if (lane == 0) L.x[r] += s;
+    const double *e = (l + 1 == p.nl - 1) ? C.x : C.t;
+    {  // x += P e
+      int g = L.gP, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int r = base + tid / g;
+        bool ok = r < L.n;
+        double s = group_row(L.Prp, L.Pci, L.Pv, e, r, ok, lig, g);
+        if (ok && lig == 0) L.x[r] += s;
+      }
     }
-    __syncthreads();
-    for (int r = warp; r < L.n; r += nw) {  // t = x + (b - A x) ./ dl1
-      double s = warp_row(L.Arp, L.Aci, L.Av, L.x, r, lane);
-      if (lane == 0) L.t[r] = L.x[r] + (L.b[r] - s) * L.d[r];
+    grid.sync();
+    {  // t = x + (b - A x) ./ dl1
+      int g = L.gA, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int r = base + tid / g;
+        bool ok = r < L.n;
+        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g);
+        if (ok && lig == 0) L.t[r] = L.x[r] + (L.b[r] - s) * L.d[r];
+      }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < L.n; i += TAIL_THREADS) L.x[i] = L.t[i];
-    __syncthreads();
+    if (l > 0) grid.sync();
   }
 }
 
@@ -116,15 +153,27 @@ void plan_tail(bf_ctx *c, Hier &h) {
   if (l < h.nlev - 1) h.tail = l;
 }
 
+// lanes per row group: a power of two near half the mean row length
+static int tail_lanes(int64_t nnz, int n) {
+  double mean = n > 0 ? (double)nnz / n : 1.0;
+  int g = 1;
+  while (g < 32 && 2 * g <= mean / 2.0) g <<= 1;
+  return g;
+}
+
 static void launch_tail(bf_ctx *c, Hier &h) {
   TailParams p;
   p.nl = h.nlev - h.tail;
   p.beta = 1.0;
   p.inv = h.inv;
+  int64_t lanes = 1;
   for (int k = 0; k < p.nl; k++) {
     Level &L = h.lv[h.tail + k];
     TailLevel &T = p.lv[k];
     T.n = L.A.n;
+    T.gA = tail_lanes(L.A.nnz, L.A.n);
+    T.gP = tail_lanes(L.P.nnz, L.A.n);
+    T.gR = tail_lanes(L.R.nnz, L.R.n);
     T.Arp = L.A.rp;
     T.Aci = L.A.ci;
     T.Av = L.A.v;
@@ -139,12 +188,38 @@ static void launch_tail(bf_ctx *c, Hier &h) {
     T.x = L.x;
     T.r = L.r;
     T.t = L.t;
-    c->alg_bytes += 2 * (12.0 * L.A.nnz + 4.0 * L.A.n) + 2 * (12.0 * L.P.nnz + 4.0 * L.A.n) + 80.0 * L.A.n;
+    if (k < p.nl - 1) {
+      lanes = std::max(lanes, (int64_t)T.n * std::max(T.gA, T.gP));
+      lanes = std::max(lanes, (int64_t)L.R.n * T.gR);
+      c->alg_bytes += 2 * (12.0 * L.A.nnz + 4.0 * L.A.n) + 2 * (12.0 * L.P.nnz + 4.0 * L.A.n) + 80.0 * L.A.n;
+    }
   }
+  p.gL = std::min(32, std::max(1, tail_lanes((int64_t)h.nL * h.nL, h.nL)));
+  lanes = std::max(lanes, (int64_t)h.nL * p.gL);
   c->alg_bytes += 8.0 * h.nL * h.nL;
-  k_vcycle_tail<<<1, TAIL_THREADS, 0, c->stream>>>(p);
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail, TAIL_THREADS, 0));
+    const char *e = getenv("BF_TAIL_BPS");
+    int bps = e ? atoi(e) : 1;
+    max_blocks = std::max(1, std::min(per_sm, bps)) * c->num_sms;
+  }
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_blocks, (lanes + TAIL_THREADS - 1) / TAIL_THREADS));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TAIL_THREADS);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, k_vcycle_tail, p));
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
+  Level &L0 = h.lv[h.tail];  // the tail's result for its first level is in t
+  std::swap(L0.x, L0.t);
 }
 
 __global__ void k_zero(int n, double *x) {
@@ -379,11 +454,15 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
     BF_LAUNCH(c);
     BF_CUDA(cudaMemcpyAsync(L.r, L.b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   } else {
-    for (int s = 0; s < o.nu_pre; s++) smooth_pass(c, L, x, s == 0, s == o.nu_pre - 1);
+    for (int s = 0; s < o.nu_pre; s++) smooth_pass(c, L, x, s == 0, s == o.nu_pre - 1 && !L.Rf.n);
   }
   Level &Lc = h.lv[l + 1];
   // b_c = R r, and x0_c = beta b_c ./ dl1_c for the next level
-  csr_op<OP_SPMV_X0>(c, L.R, L.r, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
+  if (L.Rf.n) {  // b_c = R (I - beta A D) b: residual of the seeded pre-sweep + restriction in one product
+    csr_op<OP_SPMV_X0>(c, L.Rf, L.b, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
+  } else {
+    csr_op<OP_SPMV_X0>(c, L.R, L.r, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
+  }
   vcycle_level(c, h, l + 1);
   csr_op<OP_ADD>(c, L.P, Lc.x, nullptr, nullptr, x, nullptr, 0.0, 0.0, nullptr);  // x += P e
   for (int s = 0; s < o.nu_post; s++) smooth_pass(c, L, x, false, false);
@@ -444,6 +523,21 @@ void bf_apply(bf_ctx *c, const double *v, double *z) {
   BF_CUDA(cudaGetLastError());
 }
 
+// algorithmic bytes of one BF apply, SURVEY.md 8(d)'s per-unit figures on the actual
+// hierarchies: per level l < L of each V(1,1) 24 nnz(A_l) + 24 nnz(P_l) + 116 n_l + 12 n_{l+1},
+// the coarsest solve 8 n_L^2, the A_ps coupling 12 nnz(A_ps) + 36 n, split + merge 64 n.
+// Independent of the kernels' own storage (DIA, fused restriction), like the J SpMV's 36 B/block.
+double apply_model_bytes(bf_ctx *c) {
+  double bytes = 12.0 * c->blk[1].nnz + 36.0 * c->n + 64.0 * c->n;
+  for (int w = 0; w < 2; w++) {
+    Hier &h = c->h[w];
+    for (int l = 0; l + 1 < h.nlev; l++)
+      bytes += 24.0 * h.lv[l].A.nnz + 24.0 * h.lv[l].P.nnz + 116.0 * h.lv[l].A.n + 12.0 * h.lv[l + 1].A.n;
+    bytes += 8.0 * h.nL * h.nL;
+  }
+  return bytes;
+}
+
 // forget the captured BF apply (buffers of the finest level changed)
 void drop_apply_graph(bf_ctx *c) {
   if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
@@ -478,7 +572,8 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     BF_CUDA(cudaStreamEndCapture(c->cap_stream, &g));
     c->stream = user;
     c->apply_graph_kernels = c->launches - l0;
-    c->apply_bytes = c->alg_bytes - b0;
+    c->apply_bytes = apply_model_bytes(c);
+    (void)b0;
     c->launches = l0;
     BF_CUDA(cudaGraphInstantiate(&c->apply_exec, g, 0));
     // locate the split node (the only reader of v) and the merge node (the only writer of z)
