@@ -175,8 +175,8 @@ void bsr_spmv(bf_ctx *c, const double *x, double *y);                   // k_spm
 void setup_bsr_dia(bf_ctx *c);                                          // k_spmv.cu
 void csr_spmv(bf_ctx *c, const DCsr &A, const double *x, double *y);    // k_spmv.cu
 void vcycle(bf_ctx *c, int which, const double *b, double *x);          // k_vcycle.cu
-void bf_apply(bf_ctx *c, const double *v, double *z);                   // k_vcycle.cu
-void bf_apply_graph(bf_ctx *c, const double *v, double *z);             // k_vcycle.cu
+void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2 = nullptr);                   // k_vcycle.cu
+void bf_apply_graph(bf_ctx *c, const double *v, double *z, const double *nrm2 = nullptr);             // k_vcycle.cu
 void alloc_solve_workspace(bf_ctx *c, int restart);                     // k_gmres.cu
 void assemble(bf_ctx *c, const bf_twophase *P, const double *p, const double *sn, int32_t *rp, int32_t *ci,
               double *vals, double *R);                                   // k_assemble.cu

@@ -248,13 +248,14 @@ static int wave_grid(bf_ctx *c, K kernel) {
   return c->num_sms * per_sm;
 }
 
-// out = a . b  (host value, synchronises)
-static double dot_host(bf_ctx *c, const double *a, const double *b) {
+// out = a . b  (host value, synchronises); the device copy lands in `dst` (default scratch)
+static double dot_host(bf_ctx *c, const double *a, const double *b, double *dst = nullptr) {
   int64_t N = 2 * (int64_t)c->n;
-  k_dots<1><<<wave_grid(c, k_dots<1>), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, c->hdev + 3 * MAXNV, c->counter);
+  if (!dst) dst = c->hdev + 3 * MAXNV;
+  k_dots<1><<<wave_grid(c, k_dots<1>), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, dst, c->counter);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
-  BF_CUDA(cudaMemcpyAsync(c->hpin, c->hdev + 3 * MAXNV, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaMemcpyAsync(c->hpin, dst, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
   return c->hpin[0];
 }
@@ -276,20 +277,20 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     *relres = 0.0;
     return;
   }
-  // r = b - J x
+  double *hd1 = c->hdev, *hd2 = c->hdev + MAXNV, *hdn = c->hdev + 2 * MAXNV;
+  // r = b - J x, written straight into the basis slot v_0 (normalised by the first split)
   bsr_spmv(c, x, c->w);
-  k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, c->r);
+  k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, V);
   BF_LAUNCH(c);
-  double beta = std::sqrt(dot_host(c, c->r, c->r));
+  double beta = std::sqrt(dot_host(c, V, V, hdn));
   if (hist) hist[0] = beta / bnorm;
   *relres = beta / bnorm;
   if (beta <= tol * bnorm) {
     *converged = 1;
     return;
   }
-  double *hd1 = c->hdev, *hd2 = c->hdev + MAXNV, *hdn = c->hdev + 2 * MAXNV;
   // Arnoldi step j, enqueued without waiting for the host: z_j = M^-1 v_j, w = J z_j, CGS2,
-  // v_{j+1} = w / ||w|| (norm taken on the device), then an async copy of (h, h2, ||w||^2)
+  // v_{j+1} = w / ||w|| (norm taken on the device, applied by the next step's split kernel), then an async copy of (h, h2, ||w||^2)
   // into pinned slot j%2 and an event.  The host processes step j (Givens, convergence) while
   // step j+1 already runs; a step enqueued past the stopping point is simply discarded.
   const int SLOT = 2 * MAXNV + 8;
@@ -297,7 +298,10 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     const double *vj = V + (size_t)j * N;
     double *vn = V + (size_t)(j + 1) * N;
     double *zj = c->Z + (size_t)j * N;
-    bf_apply_graph(c, vj, zj);  // z_j = M^-1 v_j, kept for the cycle-end update
+    // z_j = M^-1 v_j, kept for the cycle-end update; the split kernel first normalises the
+    // slot v_j in place by 1/sqrt(*hdn) (||v_j||^2 from the previous step's pass 3, or the
+    // restart residual's norm)
+    bf_apply_graph(c, vj, zj, hdn);
     cudaEvent_t t0;
     timer_begin(c, 0, &t0);
     bsr_spmv(c, zj, c->w);  // w = J z_j
@@ -317,16 +321,12 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     }
     c->launches += c->opt.orth == 0 ? 3 : 2;
     timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));
-    k_scale<<<G, 256, 0, c->stream>>>(N, vn, hdn, 0.0, vn);  // 1/sqrt(||w||^2) read on the device
-    BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
     BF_CUDA(cudaMemcpyAsync(c->hpin + (j & 1) * SLOT, c->hdev, sizeof(double) * (2 * MAXNV + 1),
                             cudaMemcpyDeviceToHost, c->stream));
     BF_CUDA(cudaEventRecord(c->step_ev[j & 1], c->stream));
   };
   for (;;) {
-    k_scale<<<G, 256, 0, c->stream>>>(N, c->r, nullptr, 1.0 / beta, V);
-    BF_LAUNCH(c);
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int k = 0;
@@ -380,9 +380,9 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     BF_LAUNCH(c);
     // true residual at the end of the cycle (R11)
     bsr_spmv(c, x, c->w);
-    k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, c->r);
+    k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, V);
     BF_LAUNCH(c);
-    beta = std::sqrt(dot_host(c, c->r, c->r));
+    beta = std::sqrt(dot_host(c, V, V, hdn));
     *relres = beta / bnorm;
     if (beta <= tol * bnorm) {
       *converged = 1;

@@ -483,13 +483,22 @@ void vcycle(bf_ctx *c, int which, const double *b, double *x) {
   BF_CUDA(cudaMemcpyAsync(x, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
 }
 
-// R_p v -> vp, R_s v -> vs (interleaved in the caller's var_order); also x0 of the A_ss V-cycle
-__global__ void k_split_vec(int n, int ip, const double *__restrict__ v, double *__restrict__ vp,
+// R_p v -> vp, R_s v -> vs (interleaved in the caller's var_order); also x0 of the A_ss V-cycle.
+// nrm2 != null: v is an unnormalised GMRES basis slot with ||v||^2 = *nrm2 (computed by the
+// last CGS2 pass); v is normalised here, in place, by the same 1/sqrt(||v||^2) scaling the
+// separate scaling pass applied (one read + one write of v saved per Arnoldi step).
+__global__ void k_split_vec(int n, int ip, double *__restrict__ v, double *__restrict__ vp,
                             double *__restrict__ vs, const double *__restrict__ dinv, double beta,
-                            double *__restrict__ x0) {
+                            double *__restrict__ x0, const double *__restrict__ nrm2) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 a = reinterpret_cast<const double2 *>(v)[i];
+  if (nrm2) {
+    double sc = 1.0 / sqrt(*nrm2);
+    a.x = a.x * sc;
+    a.y = a.y * sc;
+    reinterpret_cast<double2 *>(v)[i] = a;
+  }
   double s = ip ? a.x : a.y;
   vp[i] = ip ? a.y : a.x;
   vs[i] = s;
@@ -503,14 +512,14 @@ __global__ void k_merge_vec(int n, int ip, const double *__restrict__ p, const d
   reinterpret_cast<double2 *>(z)[i] = ip ? make_double2(s[i], p[i]) : make_double2(p[i], s[i]);
 }
 
-void bf_apply(bf_ctx *c, const double *v, double *z) {
+void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   int n = c->n;
   int ip = c->var_order;
   Hier &hs = c->h[0], &hS = c->h[1];
   // Alg. 3 step 2: A_ss s = R_s r_k by one V-cycle
   c->alg_bytes += 48.0 * n + 32.0 * n;  // split (v in; vp, vs, x0 out; dl1 in) + merge (p, s in; z out)
-  k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, v, c->vp, hs.lv[0].b, hs.lv[0].d,
-                                                     x0_beta(c->opt), hs.lv[0].x);
+  k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, const_cast<double *>(v), c->vp, hs.lv[0].b,
+                                                     hs.lv[0].d, x0_beta(c->opt), hs.lv[0].x, nrm2);
   BF_LAUNCH(c);
   vcycle_level(c, hs, 0);
   // step 3: r = R_p r_k - A_ps s
@@ -551,7 +560,7 @@ void drop_apply_graph(bf_ctx *c) {
 // The whole BF apply (~60 kernels, most of them small coarse-level kernels) replayed as one
 // CUDA graph: captured once per handle on a private stream, launched on the caller's stream.
 // Only the input vector changes between applies; it is patched into the split kernel node.
-void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
+void bf_apply_graph(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   if (!c->apply_exec) {
     if (!c->cap_stream) BF_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     cudaStream_t user = c->stream;
@@ -560,7 +569,7 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     double b0 = c->alg_bytes;
     BF_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     try {
-      bf_apply(c, v, z);
+      bf_apply(c, v, z, nrm2);
     } catch (...) {
       cudaGraph_t g;
       cudaStreamEndCapture(c->cap_stream, &g);
@@ -601,14 +610,16 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z) {
     if (!c->apply_split_node || !c->apply_merge_node)
       throw Error(BF_ERR_CUDA, "split/merge node not found in the BF apply graph");
   }
-  // patch the input pointer of the split kernel (argument 2: v) and the output pointer of the
+  // patch the input pointer of the split kernel (argument 2: v; argument 8: the norm for in-place normalisation) and the output pointer of the
   // merge kernel (argument 4: z); all other arguments are the handle's fixed buffers
-  const double *vin = v;
+  double *vin = const_cast<double *>(v);
+  const double *nin = nrm2;
   double *zout = z;
-  void *sargs[8], *margs[5];
-  for (int k = 0; k < 8; k++) sargs[k] = c->split_params.kernelParams[k];
+  void *sargs[9], *margs[5];
+  for (int k = 0; k < 9; k++) sargs[k] = c->split_params.kernelParams[k];
   for (int k = 0; k < 5; k++) margs[k] = c->merge_params.kernelParams[k];
   sargs[2] = (void *)&vin;
+  sargs[8] = (void *)&nin;
   margs[4] = (void *)&zout;
   cudaKernelNodeParams ps = c->split_params, pm = c->merge_params;
   ps.kernelParams = sargs;
