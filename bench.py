@@ -284,9 +284,10 @@ def run_ours(args):
     # ---- roofline of the dominant kernel class (device time share inside the timed region)
     peak, peak_src = peaks()
     kt = rec["kt"]
-    cls = {0: "bsr2_spmv (J SpMV, one kernel)",
-           1: "gmres_cgs2 (3 fused orthogonalisation passes per Arnoldi step)",
-           2: "bf_apply (Algorithm 3: two V-cycles + A_ps coupling, ~60 TMA CSR kernels in one CUDA graph)"}
+    cls = {0: "bsr2_spmv (J SpMV, one DIA-BSR kernel; bytes: SURVEY 8(d) 36 B/block + 36 B/row)",
+           1: "gmres_cgs2 (3 fused orthogonalisation passes per Arnoldi step; bytes: 8N(3j+5))",
+           2: "bf_apply (Algorithm 3: two V-cycles + A_ps coupling, ~43 DIA/TMA-CSR kernels in one CUDA graph; "
+              "bytes: SURVEY 8(d) per-level V(1,1) model on the actual hierarchies)"}
 
     def roof(k):
         ms, launches, by = kt[k]
