@@ -251,6 +251,16 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
     while (g < 32 && 2 * g <= mean / div) g <<= 1;
   }
   A.g = g;
+  // CTA size: 256 threads, or 128 when a 256-thread tile (256/g rows) of these rows would hold
+  // far more than the target nonzeros (long Galerkin rows at g = mean/4): smaller tiles, twice
+  // the CTAs per SM, the same threads per SM
+  {
+    const char *en = getenv("BF_TMA_NT");
+    int nt = TMA_THREADS;  // 128 measured slower on C3 (72.6/68.5 vs 67.5 ms): opt-in only
+    if (en) nt = atoi(en) == 128 ? 128 : TMA_THREADS;
+    if (nt / g < 1) nt = TMA_THREADS;
+    A.nt = nt;
+  }
   const char *es = getenv("BF_TMA_STAGES");
   A.stages = es ? atoi(es) : 2;
   const char *et = getenv("BF_TMA_TILE");
@@ -258,7 +268,7 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   int rpt = 256;
   // ~1024 nonzeros per tile, but at least one full pass of the CTA (256/g rows) so that no
   // thread idles (stencil rows, g = 1, always take 256-row tiles)
-  while (rpt > 8 && rpt > TMA_THREADS / g && rpt * mean > tile) rpt >>= 1;
+  while (rpt > 8 && rpt > A.nt / g && rpt * mean > tile) rpt >>= 1;
   int *mx = dalloc_t<int>(c, 1);
   for (;; rpt >>= 1) {
     BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
