@@ -54,7 +54,9 @@ struct Hier {
   int32_t *piv = nullptr;
   double *inv = nullptr;  // explicit inverse of the coarsest matrix (nL x nL, row-major)
   int32_t nL = 0;
-  int tail = -1;          // first level handled by the single-CTA tail kernel (-1: none)
+  int tail = -1;          // first level handled by the cooperative tail kernel (-1: none)
+  int dtail = -1;         // first level whose whole sub-V-cycle is applied as a dense operator T (-1: none)
+  double *tmat = nullptr; // T (n_dtail x n_dtail, row-major): the exact linear map b -> x of that sub-V-cycle
   bool dense = false;  // coarsest level solved by LU (else 4 l1-Jacobi sweeps)
 };
 
@@ -165,6 +167,7 @@ void build_schur(bf_ctx *c);                                            // k_spl
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);
+void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vcycle.cu
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
 double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu                                     // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu

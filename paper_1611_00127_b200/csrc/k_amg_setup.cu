@@ -961,6 +961,7 @@ void free_hierarchy(bf_ctx *c, Hier &h) {
   dfree(c, h.lu);
   dfree(c, h.piv);
   dfree(c, h.inv);
+  dfree(c, h.tmat);
   h = Hier();
 }
 
@@ -1159,6 +1160,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
                                               std::to_string(hs));
   }
   plan_tail(c, h);
+  build_dense_tail(c, h);
   build_rfuse(c, h, false);
 }
 
@@ -1186,7 +1188,7 @@ void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
   const bf_options &o = c->opt;
   if (getenv("BF_NO_RFUSE") || o.smoother != 0 || o.nu_pre != 1) return;
   const bool l0 = getenv("BF_RFUSE_L0") != nullptr;
-  int lend = h.tail >= 0 ? h.tail : h.nlev - 1;
+  int lend = h.dtail >= 0 ? h.dtail : (h.tail >= 0 ? h.tail : h.nlev - 1);
   for (int l = l0 ? 0 : 1; l < lend; l++) {
     if (finest_only && l > 0) break;
     Level &L = h.lv[l];

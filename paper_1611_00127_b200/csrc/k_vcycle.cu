@@ -153,6 +153,194 @@ void plan_tail(bf_ctx *c, Hier &h) {
   if (l < h.nlev - 1) h.tail = l;
 }
 
+// ----------------------------------------------------------------------------------------
+// Dense tail operator.  Below the first level l_T with at most DTAIL_N rows, the V(1,1) cycle
+// (seeded l1-Jacobi pre-sweep, residual, restriction, recursion, exact coarse solve,
+// prolongation, post-sweep) is a FIXED linear map b_{l_T} -> x_{l_T}: nothing in it depends on
+// the right-hand side except linearly.  Its matrix T (n x n, n <= DTAIL_N) is formed at setup
+// by running exactly those steps on the n unit vectors (one CTA per column, k_tail_columns),
+// and the solve applies it as one dense matvec (k_dense_tail): the same operator as the
+// level-by-level cycle (rounding order differs; the V-cycle parity tolerance covers it),
+// ~10 latency-bound launches per hierarchy replaced by one bandwidth-bound read of T
+// (C3: 950^2 and 606^2 doubles, 7.2 + 2.9 MB).  Default smoother configuration only; frozen
+// with the coarse levels by bf_update (R16).
+// ----------------------------------------------------------------------------------------
+constexpr int DTAIL_N = 2048;
+constexpr int DTAIL_THREADS = 256;
+
+// one CTA per column `col` of T; per-column level vectors are the TailParams buffers offset by
+// col * n_k (allocated [n0 columns][n_k] per level by build_dense_tail)
+__global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, double *__restrict__ T) {
+  const int col = blockIdx.x, n0 = p.lv[0].n;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  auto vb = [&](int k) { return p.lv[k].b + (size_t)col * p.lv[k].n; };
+  auto vx = [&](int k) { return p.lv[k].x + (size_t)col * p.lv[k].n; };
+  auto vr = [&](int k) { return p.lv[k].r + (size_t)col * p.lv[k].n; };
+  auto vt = [&](int k) { return p.lv[k].t + (size_t)col * p.lv[k].n; };
+  {  // b_0 = e_col, x_0 = beta b_0 ./ dl1_0 (the seeded pre-sweep)
+    double *b = vb(0), *x = vx(0);
+    for (int i = tid; i < n0; i += nth) {
+      double bi = i == col ? 1.0 : 0.0;
+      b[i] = bi;
+      x[i] = p.beta * (bi * p.lv[0].d[i]);
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < p.nl - 1; l++) {
+    const TailLevel &L = p.lv[l];
+    const TailLevel &C = p.lv[l + 1];
+    {  // r = b - A x0
+      double *b = vb(l), *x = vx(l), *r = vr(l);
+      int g = L.gA, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int i = base + tid / g;
+        bool ok = i < L.n;
+        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
+        if (ok && lig == 0) r[i] = b[i] - s;
+      }
+    }
+    __syncthreads();
+    {  // b_c = R r ; x0_c = beta b_c ./ dl1_c
+      double *r = vr(l), *bc = vb(l + 1), *xc = vx(l + 1);
+      int g = L.gR, lig = tid & (g - 1);
+      for (int base = 0; base < C.n; base += nth / g) {
+        int i = base + tid / g;
+        bool ok = i < C.n;
+        double s = group_row(L.Rrp, L.Rci, L.Rv, r, i, ok, lig, g);
+        if (ok && lig == 0) {
+          bc[i] = s;
+          xc[i] = p.beta * (s * C.d[i]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  {  // coarsest: x = A_L^-1 b
+    const TailLevel &L = p.lv[p.nl - 1];
+    double *b = vb(p.nl - 1), *x = vx(p.nl - 1);
+    for (int i = tid; i < L.n; i += nth) {
+      double s = 0.0;
+      for (int j = 0; j < L.n; j++) s += p.inv[(size_t)i * L.n + j] * b[j];
+      x[i] = s;
+    }
+  }
+  __syncthreads();
+  for (int l = p.nl - 2; l >= 0; l--) {
+    const TailLevel &L = p.lv[l];
+    const double *e = (l + 1 == p.nl - 1) ? vx(l + 1) : vt(l + 1);
+    double *b = vb(l), *x = vx(l), *t = vt(l);
+    {  // x += P e
+      int g = L.gP, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int i = base + tid / g;
+        bool ok = i < L.n;
+        double s = group_row(L.Prp, L.Pci, L.Pv, e, i, ok, lig, g);
+        if (ok && lig == 0) x[i] += s;
+      }
+    }
+    __syncthreads();
+    {  // t = x + (b - A x) ./ dl1
+      int g = L.gA, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int i = base + tid / g;
+        bool ok = i < L.n;
+        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
+        if (ok && lig == 0) t[i] = x[i] + (b[i] - s) * L.d[i];
+      }
+    }
+    __syncthreads();
+  }
+  const double *t0 = vt(0);
+  for (int i = tid; i < n0; i += nth) T[(size_t)i * n0 + col] = t0[i];
+}
+
+// x = T b: warp per row of T, b staged in shared memory
+__global__ void __launch_bounds__(DTAIL_THREADS) k_dense_tail(int n, const double *__restrict__ T,
+                                                               const double *__restrict__ b, double *__restrict__ x) {
+  extern __shared__ double bs[];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) bs[j] = b[j];
+  __syncthreads();
+  int lane = threadIdx.x & 31;
+  int row = blockIdx.x * (DTAIL_THREADS / 32) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const double *tr = T + (size_t)row * n;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s += tr[j] * bs[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[row] = s;
+}
+
+static int tail_lanes(int64_t nnz, int n);
+
+void build_dense_tail(bf_ctx *c, Hier &h) {
+  const bf_options &o = c->opt;
+  dfree(c, h.tmat);
+  h.tmat = nullptr;
+  h.dtail = -1;
+  if (getenv("BF_NO_DTAIL") || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  const char *e = getenv("BF_DTAIL_N");
+  int lim = e ? atoi(e) : DTAIL_N;
+  int lt = -1;
+  for (int l = 1; l < h.nlev - 1; l++)
+    if (h.lv[l].A.n <= lim && h.nlev - l <= TAIL_MAXL) {
+      lt = l;
+      break;
+    }
+  if (lt < 0) return;
+  int n0 = h.lv[lt].A.n;
+  TailParams p;
+  p.nl = h.nlev - lt;
+  p.beta = 1.0;
+  p.inv = h.inv;
+  std::vector<double *> bufs;
+  for (int k = 0; k < p.nl; k++) {
+    Level &L = h.lv[lt + k];
+    TailLevel &Tl = p.lv[k];
+    Tl.n = L.A.n;
+    Tl.gA = tail_lanes(L.A.nnz, L.A.n);
+    Tl.gP = tail_lanes(L.P.nnz, L.A.n);
+    Tl.gR = tail_lanes(L.R.nnz, L.R.n);
+    Tl.Arp = L.A.rp;
+    Tl.Aci = L.A.ci;
+    Tl.Av = L.A.v;
+    Tl.Prp = L.P.rp;
+    Tl.Pci = L.P.ci;
+    Tl.Pv = L.P.v;
+    Tl.Rrp = L.R.rp;
+    Tl.Rci = L.R.ci;
+    Tl.Rv = L.R.v;
+    Tl.d = L.d;
+    double *w = dalloc_t<double>(c, (size_t)4 * n0 * L.A.n);  // [b | x | r | t] x n0 columns
+    bufs.push_back(w);
+    Tl.b = w;
+    Tl.x = w + (size_t)n0 * L.A.n;
+    Tl.r = w + (size_t)2 * n0 * L.A.n;
+    Tl.t = w + (size_t)3 * n0 * L.A.n;
+  }
+  h.tmat = dalloc_t<double>(c, (size_t)n0 * n0);
+  k_tail_columns<<<n0, DTAIL_THREADS, 0, c->stream>>>(p, h.tmat);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  for (double *w : bufs) dfree(c, w);
+  h.dtail = lt;
+}
+
+static void launch_dense_tail(bf_ctx *c, Hier &h) {
+  Level &L = h.lv[h.dtail];
+  int n = L.A.n;
+  c->alg_bytes += 8.0 * n * n + 16.0 * n;
+  static bool attr = false;
+  if (!attr) {
+    BF_CUDA(cudaFuncSetAttribute(k_dense_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, DTAIL_N * 8 + 1024));
+    attr = true;
+  }
+  k_dense_tail<<<div_up(n, DTAIL_THREADS / 32), DTAIL_THREADS, sizeof(double) * n, c->stream>>>(n, h.tmat, L.b,
+                                                                                               L.x);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
 // lanes per row group: a power of two near half the mean row length
 static int tail_lanes(int64_t nnz, int n) {
   double mean = n > 0 ? (double)nnz / n : 1.0;
@@ -434,6 +622,10 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   Level &L = h.lv[l];
   int n = L.A.n;
   const bf_options &o = c->opt;
+  if (l == h.dtail) {  // the whole sub-cycle from here down as one dense operator
+    launch_dense_tail(c, h);
+    return;
+  }
   if (l == h.tail) {
     launch_tail(c, h);
     return;

@@ -285,3 +285,47 @@ def test_restart_lengths(restart):
     if ro["converged"]:
         for f in (0, 1):
             assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+
+
+# The solve-phase storage / fusion choices (DIA finest levels, fused restriction Rf, dense
+# tail operator, cooperative tail, TMA tiles) are all the same linear operators as the
+# oracle's level-by-level V-cycle; each variant must meet the same bounds.  The choices are
+# read at bf_setup time from the environment.
+VARIANTS = {
+    "default": {},
+    "no-dtail": {"BF_NO_DTAIL": "1"},
+    "no-rfuse": {"BF_NO_RFUSE": "1"},
+    "rfuse-l0": {"BF_RFUSE_L0": "1"},
+    "plain": {"BF_NO_DTAIL": "1", "BF_NO_RFUSE": "1", "BF_NO_TAIL": "1", "BF_NO_DIA": "1", "BF_NO_TMA": "1"},
+    "coop-tail-big": {"BF_NO_DTAIL": "1", "BF_TAIL_NNZ": "200000"},
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+@pytest.mark.parametrize("config,dims", [(2, (33, 30, 31)), (3, (20, 17, 15))])
+def test_solve_path_variants(variant, config, dims, monkeypatch):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    prob, J, rhs = make_system(config, dims=dims)
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    n = J.n
+    for which in (0, 1):
+        b = seeded_vector(n, 20 + which)
+        xo = o.vcycle(which, b)
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.vcycle(which, torch_dev(b), x)
+        assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo), (variant, which)
+    v = seeded_vector(2 * n, 8)
+    zo = o.apply(v)
+    z = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(v), z)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo), variant
+    ro = o.gmres(rhs, tol=1e-8, restart=30, maxit=500)
+    x = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=1e-8, restart=30, maxit=500)
+    assert r["converged"] == ro["converged"] and abs(r["iters"] - ro["iters"]) <= 1, (variant, r["iters"], ro["iters"])
+    xg = x.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2]), variant
+    g.close()
