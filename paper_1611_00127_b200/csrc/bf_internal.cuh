@@ -169,7 +169,7 @@ void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);
 void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vcycle.cu
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
-double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu                                     // k_vcycle.cu
+double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
 void setup_lx(bf_ctx *c, DCsr &A);                                      // k_vcycle.cu
 void setup_dia(bf_ctx *c, DCsr &A);                                     // k_vcycle.cu
@@ -189,5 +189,27 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int m
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
 
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// programmatic dependent launch (PDL): the kernel may begin while its stream predecessor is
+// still running; it touches that predecessor's outputs only after pdl_wait().  Data written
+// before the predecessor started (setup matrices, older Krylov vectors) may be read earlier.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(bf_ctx *c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...));
+}
 
 }  // namespace bf

@@ -55,6 +55,10 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double *pa
   }
 }
 
+// The three passes are launched with programmatic dependent launch: the first grid-stride
+// iteration's basis loads (V_0..V_j are complete before the predecessor kernel started) are
+// issued before pdl_wait(); w and h (the predecessor's outputs) are read after it.
+
 // pass 1: out[i] = V_i . w, i < NV
 template <int NV>
 __global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double *__restrict__ V,
@@ -63,10 +67,19 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; i++) acc[i] = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
-    double v[NV];  // all NV loads in flight before the FMAs (memory-level parallelism)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[NV];  // all NV loads in flight before the FMAs (memory-level parallelism)
+  if (t < N) {
 #pragma unroll
     for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
+  }
+  pdl_wait();
+  for (; t < N; t += stride) {
+    if (t != (int64_t)blockIdx.x * blockDim.x + threadIdx.x) {
+#pragma unroll
+      for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
+    }
     double wt = __ldcs(w + t);
 #pragma unroll
     for (int i = 0; i < NV; i++) acc[i] += v[i] * wt;
@@ -80,19 +93,27 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_dots(int64_t N, const d
                                                            const double *__restrict__ h, double *partial,
                                                            double *out, unsigned int *counter) {
   __shared__ double hs[NV];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[NV];
+  if (t0 < N) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t0);
+  }
+  pdl_wait();
   if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
   __syncthreads();
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; i++) acc[i] = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
-    double v[NV];
+  for (int64_t t = t0; t < N; t += stride) {
     double wt = w[t];
+    if (t != t0) {
 #pragma unroll
-    for (int i = 0; i < NV; i++) {
-      v[i] = __ldcs(V + (size_t)i * N + t);
-      wt -= hs[i] * v[i];
+      for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
     }
+#pragma unroll
+    for (int i = 0; i < NV; i++) wt -= hs[i] * v[i];
     w[t] = wt;
 #pragma unroll
     for (int i = 0; i < NV; i++) acc[i] += v[i] * wt;
@@ -107,13 +128,22 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const d
                                                            const double *__restrict__ h, double *__restrict__ y,
                                                            double *partial, double *out, unsigned int *counter) {
   __shared__ double hs[NV];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v[NV];
+  if (t0 < N) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t0);
+  }
+  pdl_wait();
   if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
   __syncthreads();
   double acc[1] = {0.0};
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
-    double v[NV];
+  for (int64_t t = t0; t < N; t += stride) {
+    if (t != t0) {
 #pragma unroll
-    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
+      for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
+    }
     double wt = __ldcs(w + t);
 #pragma unroll
     for (int i = 0; i < NV; i++) wt -= hs[i] * v[i];
@@ -308,16 +338,17 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
     int nv = j + 1;
     timer_begin(c, 1, &t0);
-    BF_NV_SWITCH(nv, (k_dots<NV><<<wave_grid(c, k_dots<NV>), RED_THREADS, 0, c->stream>>>(N, V, c->w, c->red, hd1,
-                                                                                          c->counter)));
+    const double *Vc = V;
+    BF_NV_SWITCH(nv, (launch_pdl(c, k_dots<NV>, dim3(wave_grid(c, k_dots<NV>)), dim3(RED_THREADS), 0, N, Vc,
+                                 (const double *)c->w, c->red, hd1, c->counter)));
     if (c->opt.orth == 0) {
-      BF_NV_SWITCH(nv, (k_axpy_dots<NV><<<wave_grid(c, k_axpy_dots<NV>), RED_THREADS, 0, c->stream>>>(
-                           N, V, c->w, hd1, c->red, hd2, c->counter)));
-      BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(
-                           N, V, c->w, hd2, vn, c->red, hdn, c->counter)));
+      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_dots<NV>, dim3(wave_grid(c, k_axpy_dots<NV>)), dim3(RED_THREADS), 0, N,
+                                   Vc, c->w, (const double *)hd1, c->red, hd2, c->counter)));
+      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_norm<NV>, dim3(wave_grid(c, k_axpy_norm<NV>)), dim3(RED_THREADS), 0, N,
+                                   Vc, (const double *)c->w, (const double *)hd2, vn, c->red, hdn, c->counter)));
     } else {
-      BF_NV_SWITCH(nv, (k_axpy_norm<NV><<<wave_grid(c, k_axpy_norm<NV>), RED_THREADS, 0, c->stream>>>(
-                           N, V, c->w, hd1, vn, c->red, hdn, c->counter)));
+      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_norm<NV>, dim3(wave_grid(c, k_axpy_norm<NV>)), dim3(RED_THREADS), 0, N,
+                                   Vc, (const double *)c->w, (const double *)hd1, vn, c->red, hdn, c->counter)));
     }
     c->launches += c->opt.orth == 0 ? 3 : 2;
     timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));

@@ -73,18 +73,27 @@ struct BsrDia {
 __global__ void __launch_bounds__(256) k_bsr2_dia(int n, BsrDia o, const double2 *__restrict__ jd,
                                                   const double2 *__restrict__ x, double2 *__restrict__ y, int ip) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
+  // J's diagonals are setup data: loaded before waiting for the kernel that produced x (PDL)
+  double2 v[14];
+#pragma unroll
+  for (int d = 0; d < 7; d++) {
+    if (d < o.k && r < n) {
+      size_t e = ((size_t)d * n + r) * 2;
+      v[2 * d] = __ldcs(jd + e);
+      v[2 * d + 1] = __ldcs(jd + e + 1);
+    }
+  }
+  pdl_wait();
   if (r >= n) return;
   double y0 = 0.0, y1 = 0.0;
-#pragma unroll 7
-  for (int d = 0; d < o.k; d++) {
+#pragma unroll
+  for (int d = 0; d < 7; d++) {
     int col = r + o.off[d];
-    size_t e = ((size_t)d * n + r) * 2;
-    double2 v01 = __ldcs(jd + e), v23 = __ldcs(jd + e + 1);
-    if (col >= 0 && col < n) {
+    if (d < o.k && col >= 0 && col < n) {
       double2 xc = __ldg(x + col);
       double xp = ip ? xc.y : xc.x, xs = ip ? xc.x : xc.y;
-      y0 += v01.x * xp + v01.y * xs;
-      y1 += v23.x * xp + v23.y * xs;
+      y0 += v[2 * d].x * xp + v[2 * d].y * xs;
+      y1 += v[2 * d + 1].x * xp + v[2 * d + 1].y * xs;
     }
   }
   y[r] = ip ? make_double2(y1, y0) : make_double2(y0, y1);
@@ -154,9 +163,9 @@ void bsr_spmv(bf_ctx *c, const double *x, double *y) {
     BsrDia o;
     o.k = c->jdia_k;
     for (int d = 0; d < o.k; d++) o.off[d] = c->jdia_off[d];
-    k_bsr2_dia<<<div_up(c->n, 256), 256, 0, c->stream>>>(c->n, o, reinterpret_cast<const double2 *>(c->jdia),
-                                                        reinterpret_cast<const double2 *>(x),
-                                                        reinterpret_cast<double2 *>(y), c->var_order);
+    launch_pdl(c, k_bsr2_dia, dim3(div_up(c->n, 256)), dim3(256), 0, c->n, o,
+               reinterpret_cast<const double2 *>(c->jdia), reinterpret_cast<const double2 *>(x),
+               reinterpret_cast<double2 *>(y), c->var_order);
     BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
     return;
