@@ -254,21 +254,40 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
   for (int i = tid; i < n0; i += nth) T[(size_t)i * n0 + col] = t0[i];
 }
 
-// x = T b: warp per row of T, b staged in shared memory
+// x = T b: DTAIL_SPLIT warps per row of T (each a contiguous quarter of the row, 8 loads in
+// flight per lane), b staged in shared memory; partial sums combined in a fixed order
+constexpr int DTAIL_SPLIT = 4;
 __global__ void __launch_bounds__(DTAIL_THREADS) k_dense_tail(int n, const double *__restrict__ T,
                                                                const double *__restrict__ b, double *__restrict__ x) {
   extern __shared__ double bs[];
+  __shared__ double part[DTAIL_THREADS / 32];
+  // T is setup data: the first loads of this CTA's rows are issued before the wait (PDL)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * (DTAIL_THREADS / 32 / DTAIL_SPLIT) + warp / DTAIL_SPLIT;
+  const int q = warp % DTAIL_SPLIT;
+  const int seg = (n + DTAIL_SPLIT - 1) / DTAIL_SPLIT;
+  const int j0 = q * seg, j1 = min(n, j0 + seg);
+  pdl_wait();
   for (int j = threadIdx.x; j < n; j += blockDim.x) bs[j] = b[j];
   __syncthreads();
-  int lane = threadIdx.x & 31;
-  int row = blockIdx.x * (DTAIL_THREADS / 32) + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const double *tr = T + (size_t)row * n;
   double s = 0.0;
-  for (int j = lane; j < n; j += 32) s += tr[j] * bs[j];
+  if (row < n) {
+    const double *tr = T + (size_t)row * n;
+#pragma unroll 8
+    for (int j = j0 + lane; j < j1; j += 32) s += __ldcs(tr + j) * bs[j];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) x[row] = s;
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  if (threadIdx.x < DTAIL_THREADS / 32 / DTAIL_SPLIT) {
+    int r = blockIdx.x * (DTAIL_THREADS / 32 / DTAIL_SPLIT) + threadIdx.x;
+    if (r < n) {
+      double t = 0.0;
+      for (int k = 0; k < DTAIL_SPLIT; k++) t += part[threadIdx.x * DTAIL_SPLIT + k];
+      x[r] = t;
+    }
+  }
 }
 
 static int tail_lanes(int64_t nnz, int n);
@@ -335,8 +354,8 @@ static void launch_dense_tail(bf_ctx *c, Hier &h) {
     BF_CUDA(cudaFuncSetAttribute(k_dense_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, DTAIL_N * 8 + 1024));
     attr = true;
   }
-  k_dense_tail<<<div_up(n, DTAIL_THREADS / 32), DTAIL_THREADS, sizeof(double) * n, c->stream>>>(n, h.tmat, L.b,
-                                                                                               L.x);
+  launch_pdl(c, k_dense_tail, dim3(div_up(n, DTAIL_THREADS / 32 / DTAIL_SPLIT)), dim3(DTAIL_THREADS),
+             sizeof(double) * n, n, (const double *)h.tmat, (const double *)L.b, L.x);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
 }
