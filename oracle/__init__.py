@@ -40,7 +40,8 @@ class Options(C.Structure):
     _fields_ = [("theta", C.c_double), ("max_levels", C.c_int32), ("max_coarse", C.c_int32),
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
-                ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32)]
+                ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
+                ("precond", C.c_int32)]
 
 
 MAXL = 64
@@ -57,7 +58,8 @@ class BFs(C.Structure):
     _fields_ = [("n", C.c_int32), ("var_order", C.c_int32), ("block_order", C.c_int32),
                 ("brp", C.POINTER(C.c_int64)), ("bci", C.POINTER(C.c_int32)), ("bv", C.POINTER(C.c_double)),
                 ("App", CSRs), ("Aps", CSRs), ("Asp", CSRs), ("Ass", CSRs), ("S", CSRs),
-                ("dss", C.POINTER(C.c_double)), ("hss", AMGs), ("hS", AMGs), ("opt", Options)]
+                ("dss", C.POINTER(C.c_double)), ("hss", AMGs), ("hS", AMGs), ("opt", Options),
+                ("hpp", AMGs), ("ilu", C.POINTER(C.c_double)), ("ilu_dinv", C.POINTER(C.c_double))]
 
 
 _lib = None
@@ -89,6 +91,8 @@ def lib():
         L.or_amg_free.argtypes = [P(AMGs)]
         L.or_vcycle.argtypes = [P(AMGs), dp, dp]
         L.or_csr_free.argtypes = [P(CSRs)]
+        L.or_ilu0.argtypes = [C.c_int32, lp, ip, dp, dp, dp]
+        L.or_ilu0_solve.argtypes = [C.c_int32, lp, ip, dp, dp, dp, dp]
         L.or_bf_setup.argtypes = [C.c_int32, lp, ip, dp, C.c_int32, C.c_int32, P(Options), P(P(BFs))]
         L.or_bf_free.argtypes = [P(BFs)]
         L.or_bf_update.argtypes = [P(BFs), dp]
@@ -280,6 +284,31 @@ def l1diag(A: CSR):
     return d
 
 
+def ilu0(J):
+    """Block ILU(0) of the 2x2 BSR J (canonical row-major blocks) on its own block pattern
+    (reading R18).  Returns (lu [nnzb,2,2], dinv [n,2,2])."""
+    rp, ci, v = _bsr_arrays(J)
+    lu = np.empty_like(v)
+    dinv = np.empty(4 * J.n)
+    st = lib().or_ilu0(J.n, _p(rp, C.c_int64), _p(ci, C.c_int32), _p(v, C.c_double), _p(lu, C.c_double),
+                       _p(dinv, C.c_double))
+    if st:
+        raise RuntimeError(err())
+    return lu.reshape(-1, 2, 2), dinv.reshape(-1, 2, 2)
+
+
+def ilu0_solve(J, lu, dinv, r):
+    """x = (L U)^-1 r, canonical interleaved vectors."""
+    rp, ci, _ = _bsr_arrays(J)
+    lu = np.ascontiguousarray(lu, np.float64).reshape(-1)
+    dinv = np.ascontiguousarray(dinv, np.float64).reshape(-1)
+    r = np.ascontiguousarray(r, np.float64)
+    x = np.empty_like(r)
+    lib().or_ilu0_solve(J.n, _p(rp, C.c_int64), _p(ci, C.c_int32), _p(lu, C.c_double), _p(dinv, C.c_double),
+                        _p(r, C.c_double), _p(x, C.c_double))
+    return x
+
+
 def smooth(A: CSR, d, b, x, kind=0, degree=2, lo=0.3):
     s = A.cstruct()
     d = np.ascontiguousarray(d, np.float64)
@@ -373,8 +402,14 @@ class BF:
         return np.ctypeslib.as_array(self.s.dss, (self.n,)).copy()
 
     def hierarchy(self, which):
-        """which: 0 -> A_ss, 1 -> S~"""
-        return self.s.hss if which == 0 else self.s.hS
+        """which: 0 -> A_ss, 1 -> S~, 2 -> A_pp (CPR)"""
+        return (self.s.hss, self.s.hS, self.s.hpp)[which]
+
+    def ilu(self):
+        """(lu [nnzb,2,2], dinv [n,2,2]) of the CPR preconditioner's block ILU(0)."""
+        nnzb = int(self.s.brp[self.n])
+        return (np.ctypeslib.as_array(self.s.ilu, (4 * nnzb,)).copy().reshape(-1, 2, 2),
+                np.ctypeslib.as_array(self.s.ilu_dinv, (4 * self.n,)).copy().reshape(-1, 2, 2))
 
     def nlev(self, which):
         return self.hierarchy(which).nlev

@@ -47,6 +47,7 @@ void or_default_options(or_options *o) {
   o->orth = 0;            /* Q30: CGS2 */
   o->schur_as_printed = 0;/* Q21 */
   o->interp_norm = 1;     /* R8 */
+  o->precond = 0;         /* BF, Algorithm 3 */
 }
 
 void or_csr_free(or_csr *A) {
@@ -643,9 +644,117 @@ void or_vcycle(const or_amg *h, const double *b, double *x) { vcycle_rec(h, 0, b
 /* ------------------------------------------------------------------------ */
 /* BF preconditioner (Algorithm 3; matrix form `m_bf` P:L252-257) */
 /* ------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------ */
+/* Block ILU(0) of J ("For the preconditioner P_1 in step 2 of both     */
+/* algorithms, we use the incomplete factorization with no fill ILU(0)").       */
+/* Reading R18: the factorization is kept on J's stored 2x2 block pattern in   */
+/* the point ordering of P:L145-153 (scalar ILU(0) on a pattern of full 2x2    */
+/* blocks is the same factorization up to rounding).  IKJ form of Gaussian     */
+/* elimination restricted to the pattern [Saad, ILU(0)]:                       */
+/*   for i: for k < i in pattern(i), ascending:                                */
+/*            a_ik <- a_ik a_kk^-1                                             */
+/*            a_ij <- a_ij - a_ik a_kj   for j > k, (i,j) and (k,j) in pattern  */
+/*          a_ii^-1 kept for the backward substitution.                        */
+/* 2x2 products: entry (r,c) = A_r0 B_0c + A_r1 B_1c, multiplies and the add   */
+/* rounded separately (c.4); inverse by the adjugate: det = a00 a11 - a01 a10. */
+/* ------------------------------------------------------------------------ */
+static void blk_mul(const double *A, const double *B, double *C) {
+  C[0] = A[0] * B[0] + A[1] * B[2];
+  C[1] = A[0] * B[1] + A[1] * B[3];
+  C[2] = A[2] * B[0] + A[3] * B[2];
+  C[3] = A[2] * B[1] + A[3] * B[3];
+}
+
+static int blk_inv(const double *A, double *Ai) {
+  double det = A[0] * A[3] - A[1] * A[2];
+  if (det == 0.0 || !isfinite(det)) return 1;
+  Ai[0] = A[3] / det;
+  Ai[1] = -A[1] / det;
+  Ai[2] = -A[2] / det;
+  Ai[3] = A[0] / det;
+  return 0;
+}
+
+int or_ilu0(int32_t n, const int64_t *rp, const int32_t *ci, const double *v, double *lu, double *dinv) {
+  memcpy(lu, v, (size_t)rp[n] * 4 * sizeof(double));
+  for (int32_t i = 0; i < n; i++) {
+    int64_t d = -1;
+    for (int64_t q = rp[i]; q < rp[i + 1]; q++) {
+      int32_t k = ci[q];
+      if (k == i) d = q;
+      if (k >= i) continue;
+      double L[4];
+      blk_mul(lu + 4 * q, dinv + 4 * (int64_t)k, L);          /* a_ik <- a_ik a_kk^-1 */
+      memcpy(lu + 4 * q, L, sizeof L);
+      for (int64_t t = q + 1; t < rp[i + 1]; t++) {             /* j > k, (i,j) in pattern */
+        int32_t j = ci[t];
+        int64_t u = -1;
+        for (int64_t w = rp[k]; w < rp[k + 1]; w++)
+          if (ci[w] == j) { u = w; break; }
+        if (u < 0) continue;                                    /* (k,j) not in pattern: dropped fill */
+        double P[4];
+        blk_mul(lu + 4 * q, lu + 4 * u, P);                     /* a_ij <- a_ij - a_ik a_kj */
+        for (int e = 0; e < 4; e++) lu[4 * t + e] = lu[4 * t + e] - P[e];
+      }
+    }
+    if (d < 0 || blk_inv(lu + 4 * d, dinv + 4 * (int64_t)i)) {
+      set_err("ILU(0) pivot block singular (or missing) at cell %d", i);
+      return -1 - i;
+    }
+  }
+  return 0;
+}
+
+void or_ilu0_solve(int32_t n, const int64_t *rp, const int32_t *ci, const double *lu, const double *dinv,
+                   const double *r, double *x) {
+  double *y = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
+  for (int32_t i = 0; i < n; i++) {                             /* L y = r, L unit block-lower */
+    double y0 = r[2 * i], y1 = r[2 * i + 1];
+    for (int64_t q = rp[i]; q < rp[i + 1]; q++) {
+      int32_t k = ci[q];
+      if (k >= i) break;
+      const double *L = lu + 4 * q;
+      y0 = y0 - (L[0] * y[2 * k] + L[1] * y[2 * k + 1]);
+      y1 = y1 - (L[2] * y[2 * k] + L[3] * y[2 * k + 1]);
+    }
+    y[2 * i] = y0;
+    y[2 * i + 1] = y1;
+  }
+  for (int32_t i = n - 1; i >= 0; i--) {                        /* U x = y */
+    double t0 = y[2 * i], t1 = y[2 * i + 1];
+    for (int64_t q = rp[i]; q < rp[i + 1]; q++) {
+      int32_t j = ci[q];
+      if (j <= i) continue;
+      const double *U = lu + 4 * q;
+      t0 = t0 - (U[0] * x[2 * j] + U[1] * x[2 * j + 1]);
+      t1 = t1 - (U[2] * x[2 * j] + U[3] * x[2 * j + 1]);
+    }
+    const double *D = dinv + 4 * (int64_t)i;
+    x[2 * i] = D[0] * t0 + D[1] * t1;
+    x[2 * i + 1] = D[2] * t0 + D[3] * t1;
+  }
+  free(y);
+}
+
+/* hierarchies the chosen preconditioner uses: BF (Alg. 3) A_ss and S~; CPR-AMG(1) (Alg. 1)
+ * A_pp; CPR-AMG(2) (Alg. 2) A_pp and A_ss */
+static int build_precond(or_bf *b) {
+  const or_options *o = &b->opt;
+  int st = 0;
+  if (o->precond == 0 || o->precond == 2) {
+    st = or_amg_setup(&b->Ass, o, &b->hss);
+    if (st) return st;
+  }
+  if (o->precond == 0) return or_amg_setup(&b->S, o, &b->hS);
+  st = or_amg_setup(&b->App, o, &b->hpp);
+  if (st) return st;
+  return or_ilu0(b->n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv) ? 4 : 0;
+}
+
 int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
                 int32_t block_order, int32_t var_order, const or_options *o, or_bf **out) {
   *out = NULL;
+  if (o->precond < 0 || o->precond > 2) { set_err("precond must be 0, 1 or 2"); return 1; }
   or_bf *b = (or_bf *)xcalloc(1, sizeof(or_bf));
   b->n = n;
   b->var_order = var_order;
@@ -662,12 +771,14 @@ int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
     for (int r = 0; r < 2; r++)
       for (int c = 0; c < 2; c++) b->bv[4 * q + 2 * r + c] = vals[4 * q + blk_index(block_order, var_order, r, c)];
   b->dss = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+  if (o->precond) {
+    b->ilu = (double *)xmalloc((size_t)nnzb * 4 * sizeof(double) + 8);
+    b->ilu_dinv = (double *)xmalloc((size_t)n * 4 * sizeof(double) + 8);
+  }
   int st = or_split(n, rp, ci, vals, block_order, var_order, &b->App, &b->Aps, &b->Asp, &b->Ass, b->dss);
   if (st) { or_bf_free(b); return st; }
   or_schur(&b->App, &b->Aps, &b->Asp, b->dss, o->schur_as_printed, &b->S);
-  st = or_amg_setup(&b->Ass, o, &b->hss);
-  if (st) { or_bf_free(b); return st; }
-  st = or_amg_setup(&b->S, o, &b->hS);
+  st = build_precond(b);
   if (st) { or_bf_free(b); return st; }
   *out = b;
   return 0;
@@ -675,9 +786,9 @@ int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
 
 /* Setup reuse across Newton steps (reading R16 "frozen coarse
  * hierarchy"): new Jacobian values on the same BSR pattern.  The split, S~ and the finest
- * level of both hierarchies (A_0 and its l1 diagonal) are rebuilt from the new values; the
+ * level of every hierarchy (A_0 and its l1 diagonal) are rebuilt from the new values; the
  * coarse levels (C/F, P, R, A_l for l >= 1, coarse LU) are kept.  A hierarchy with a single
- * level is set up again. */
+ * level is set up again.  CPR: the ILU(0) of J is recomputed. */
 int or_bf_update(or_bf *b, const double *vals) {
   int32_t n = b->n;
   int64_t nnzb = b->brp[n];
@@ -691,10 +802,11 @@ int or_bf_update(or_bf *b, const double *vals) {
                     b->dss);
   if (st) return st;
   or_schur(&b->App, &b->Aps, &b->Asp, b->dss, b->opt.schur_as_printed, &b->S);
-  or_amg *hs[2] = {&b->hss, &b->hS};
-  const or_csr *A0[2] = {&b->Ass, &b->S};
-  for (int k = 0; k < 2; k++) {
+  or_amg *hs[3] = {&b->hss, &b->hS, &b->hpp};
+  const or_csr *A0[3] = {&b->Ass, &b->S, &b->App};
+  for (int k = 0; k < 3; k++) {
     or_amg *h = hs[k];
+    if (h->nlev == 0) continue;                      /* not used by this preconditioner */
     if (h->nlev <= 1) {
       or_amg_free(h);
       st = or_amg_setup(A0[k], &b->opt, h);
@@ -705,6 +817,7 @@ int or_bf_update(or_bf *b, const double *vals) {
     csr_copy(A0[k], &h->A[0]);
     or_l1diag(&h->A[0], h->dl1[0]);
   }
+  if (b->opt.precond && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv)) return 4;
   return 0;
 }
 
@@ -713,7 +826,8 @@ void or_bf_free(or_bf *b) {
   free(b->brp); free(b->bci); free(b->bv); free(b->dss);
   or_csr_free(&b->App); or_csr_free(&b->Aps); or_csr_free(&b->Asp); or_csr_free(&b->Ass);
   or_csr_free(&b->S);
-  or_amg_free(&b->hss); or_amg_free(&b->hS);
+  or_amg_free(&b->hss); or_amg_free(&b->hS); or_amg_free(&b->hpp);
+  free(b->ilu); free(b->ilu_dinv);
   free(b);
 }
 
@@ -728,8 +842,47 @@ void or_bf_spmv(const or_bf *b, const double *x, double *y) {
   free(xc); free(yc);
 }
 
+/* Two-stage CPR preconditioners, on the canonical interleaved vector r:
+ *   Algorithm 1 (CPR-AMG(1), combinative)        Algorithm 2 (CPR-AMG(2), additive)
+ *   u = P_1^-1 r            (step 2, ILU(0))     same
+ *   t = r - J u             (step 3)             same
+ *   A_pp dp = R_p t         (step 4, one V-cycle) same
+ *                                                 A_ss ds = R_s t (step 5, one V-cycle)
+ *   u <- u + R_p^T dp       (step 5)             u <- u + R_p^T dp + R_s^T ds (step 6)
+ * i.e. M_comb^-1 / M_add^-1 of `m_comb`, `m_add` with V-cycles for A_pp^-1, A_ss^-1. */
+static void cpr_apply(const or_bf *b, const double *r, double *u) {
+  int32_t n = b->n;
+  double *t = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
+  double *tp = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+  double *dp = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+  or_ilu0_solve(n, b->brp, b->bci, b->ilu, b->ilu_dinv, r, u);            /* step 2 */
+  or_bsr_spmv(n, b->brp, b->bci, b->bv, u, t);                             /* step 3 */
+  for (int64_t i = 0; i < 2 * (int64_t)n; i++) t[i] = r[i] - t[i];
+  for (int32_t c = 0; c < n; c++) tp[c] = t[2 * c];
+  or_vcycle(&b->hpp, tp, dp);                                              /* step 4 */
+  if (b->opt.precond == 2) {
+    double *ts = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+    double *ds = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+    for (int32_t c = 0; c < n; c++) ts[c] = t[2 * c + 1];
+    or_vcycle(&b->hss, ts, ds);                                            /* Alg. 2 step 5 */
+    for (int32_t c = 0; c < n; c++) u[2 * c + 1] = u[2 * c + 1] + ds[c];
+    free(ts); free(ds);
+  }
+  for (int32_t c = 0; c < n; c++) u[2 * c] = u[2 * c] + dp[c];            /* u + R_p^T dp */
+  free(t); free(tp); free(dp);
+}
+
 void or_bf_apply(const or_bf *b, const double *v, double *z) {
   int32_t n = b->n, ip = b->var_order ? 1 : 0, is = 1 - ip;
+  if (b->opt.precond) {
+    double *rc = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
+    double *uc = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
+    for (int32_t c = 0; c < n; c++) { rc[2 * c] = v[2 * c + ip]; rc[2 * c + 1] = v[2 * c + is]; }
+    cpr_apply(b, rc, uc);
+    for (int32_t c = 0; c < n; c++) { z[2 * c + ip] = uc[2 * c]; z[2 * c + is] = uc[2 * c + 1]; }
+    free(rc); free(uc);
+    return;
+  }
   double *rp = (double *)xmalloc((size_t)n * sizeof(double) + 8);
   double *rs = (double *)xmalloc((size_t)n * sizeof(double) + 8);
   double *s = (double *)xmalloc((size_t)n * sizeof(double) + 8);

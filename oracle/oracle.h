@@ -35,6 +35,8 @@ typedef struct {
   int32_t  orth;           /* 0 CGS2, 1 CGS1 (Q30) */
   int32_t  schur_as_printed; /* 0: A_sp (Q21); 1: literal P:L239 (A_pp) */
   int32_t  interp_norm;    /* 1: weights normalised to P 1 = 1 (R8, default); 0: Q26 denominators */
+  int32_t  precond;        /* 0: BF (Algorithm 3, default); 1: CPR-AMG(1) combinative (Algorithm 1);
+                              2: CPR-AMG(2) additive (Algorithm 2) -- P:L159-193 */
 } or_options;
 
 #define OR_MAX_LEVELS 64
@@ -62,6 +64,11 @@ typedef struct {
   double *dss;                    /* diag(A_ss) */
   or_amg hss, hS;                 /* hierarchies for A_ss and S~ */
   or_options opt;
+  /* CPR-AMG(1)/(2): AMG on A_pp and the block ILU(0) P_1 of J */
+  or_amg hpp;                     /* hierarchy for A_pp (precond 1, 2) */
+  double *ilu;                    /* [4 nnzb] block ILU(0) factors on J's block pattern: strictly lower
+                                     blocks hold L_ik (unit block-lower L), the rest hold U_ij */
+  double *ilu_dinv;               /* [4 n] inverse of U's diagonal (pivot) blocks */
 } or_bf;
 
 #ifdef __cplusplus
@@ -94,6 +101,13 @@ void or_amg_free(or_amg *h);
 void or_vcycle(const or_amg *h, const double *b, double *x);
 void or_csr_free(or_csr *A);
 
+/* block ILU(0) of a point-ordered 2x2 BSR matrix (canonical (p,s) row-major blocks) on its own
+ * block pattern ("incomplete factorization with no fill ILU(0)"; reading R18); returns 0,
+ * or -1 - i if the pivot block of row i is singular (or no diagonal block) */
+int  or_ilu0(int32_t n, const int64_t *rp, const int32_t *ci, const double *v, double *lu, double *dinv);
+/* x = (L U)^-1 r on canonical interleaved vectors (forward then backward block substitution) */
+void or_ilu0_solve(int32_t n, const int64_t *rp, const int32_t *ci, const double *lu, const double *dinv,
+                   const double *r, double *x);
 int  or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
                  int32_t block_order, int32_t var_order, const or_options *o, or_bf **out);
 void or_bf_free(or_bf *b);
