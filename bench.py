@@ -339,22 +339,31 @@ def run_ours(args):
         e2e = {"value": ue / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(N * 8), "steps": k_e2e}
 
-    # context: time to solution with the Chebyshev(2) smoother option (one untimed-for-value step)
+    # context: time to solution of the other preconditioner options on the same J (one
+    # untimed-for-value step each): the Chebyshev(2) smoother, and the paper's two-stage
+    # CPR-AMG(1)/(2) preconditioners (Algorithms 1, 2) it compares BF against
     alt = None
     if not args.no_e2e:
-        o2 = bf.bf_default_options(smoother=1)
-        torch.cuda.synchronize()
-        a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        a0.record(stream)
-        h2 = bf.bf_setup(d_rp, d_ci, d_v, prob.dims, opt=o2)
-        a1.record(stream)
-        d_x.zero_()
-        r2 = bf.bf_solve(h2, d_b, d_x, args.tol, args.restart, args.maxit, True)
-        a2.record(stream)
-        torch.cuda.synchronize()
-        bf.bf_destroy(h2)
-        alt = {"smoother": "chebyshev(2) on [0.3,1] (option smoother=1)", "setup_ms": a0.elapsed_time(a1),
-               "solve_ms": a1.elapsed_time(a2), "iters": r2["iters"], "converged": r2["converged"]}
+        alt = []
+        for name, kw in (("BF, chebyshev(2) on [0.3,1] smoother (option smoother=1)", dict(smoother=1)),
+                         ("CPR-AMG(1) combinative, ILU(0) + A_pp V-cycle (option precond=1)", dict(precond=1)),
+                         ("CPR-AMG(2) additive, ILU(0) + A_pp, A_ss V-cycles (option precond=2)", dict(precond=2))):
+            o2 = bf.bf_default_options(timing=1, **kw)
+            torch.cuda.synchronize()
+            a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a0.record(stream)
+            h2 = bf.bf_setup(d_rp, d_ci, d_v, prob.dims, opt=o2)
+            a1.record(stream)
+            d_x.zero_()
+            r2 = bf.bf_solve(h2, d_b, d_x, args.tol, args.restart, args.maxit, True)
+            a2.record(stream)
+            torch.cuda.synchronize()
+            ams, alaunch, aby = bf.bf_kernel_time(h2, 2)
+            bf.bf_destroy(h2)
+            alt.append({"preconditioner": name, "setup_ms": a0.elapsed_time(a1), "solve_ms": a1.elapsed_time(a2),
+                        "iters": r2["iters"], "converged": r2["converged"], "relres": r2["relres"],
+                        "apply_us": 1e3 * ams / alaunch if alaunch else None,
+                        "apply_model_gbs": (aby / alaunch) / (ams / alaunch / 1e3) / 1e9 if alaunch and ams else None})
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

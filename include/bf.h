@@ -85,6 +85,14 @@ typedef struct {
   int32_t interp_norm;         /* 1: interpolation weights normalised so P 1 = 1 (default, R8); 0: Q26 denominators */
   int32_t timing;              /* 1: record CUDA events around the J SpMV and the GMRES
                                   orthogonalisation kernels (bf_kernel_time) */
+  int32_t precond;             /* preconditioner M of `precon-system`:
+                                  0 BF, Algorithm 3 (default; hierarchies 0 A_ss, 1 S~);
+                                  1 CPR-AMG(1) combinative, Algorithm 1;
+                                  2 CPR-AMG(2) additive, Algorithm 2.
+                                  CPR: first stage P_1 = block ILU(0) of J on its block
+                                  pattern in point order (R18), second stage
+                                  one V-cycle on A_pp (hierarchy 2) [and on A_ss, hierarchy 0].
+                                  A singular ILU pivot block is BF_ERR_ZERO_DIAG naming the cell. */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;
@@ -170,9 +178,11 @@ const char *bf_last_error(bf_handle h);
 /* ---- introspection (parity tests, statistics) ---------------------------------- */
 /* y = J x (P:L138-140 operator), vectors as in bf_solve. */
 bf_status bf_spmv(bf_handle h, const double *x, double *y, int32_t vec_mem, void *cuda_stream);
-/* z = M_bf^-1 r: one application of Algorithm 3. */
+/* z = M^-1 r: one application of the handle's preconditioner (Algorithm 3, or
+ * Algorithm 1/2, per opt.precond). */
 bf_status bf_apply_precond(bf_handle h, const double *r, double *z, int32_t vec_mem, void *cuda_stream);
-/* x = one V-cycle of hierarchy `which` (0 A_ss, 1 S~) applied to b (length n_cells). */
+/* x = one V-cycle of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp) applied to b (length n_cells).
+ * BF_ERR_ARG for a hierarchy the handle's preconditioner does not build. */
 bf_status bf_vcycle(bf_handle h, int32_t which, const double *b, double *x, int32_t vec_mem,
                     void *cuda_stream);
 bf_status bf_num_levels(bf_handle h, int32_t which, int32_t *nlev);
@@ -182,14 +192,23 @@ bf_status bf_num_levels(bf_handle h, int32_t which, int32_t *nlev);
 bf_status bf_get_level(bf_handle h, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
                        int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val,
                        int8_t *cf, int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1);
-/* which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~.  Sizes first; arrays optional (host). */
+/* which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~ (S~ only for precond 0).  Sizes first; arrays
+ * optional (host). */
 bf_status bf_get_block(bf_handle h, int32_t which, int64_t *nnz, int32_t *rowptr, int32_t *col,
                        double *val);
+/* CPR handles (precond 1, 2): the block ILU(0) factors of J copied to host buffers
+ * (either may be NULL): lu[4 nnzb] on J's block pattern, canonical row-major (p,s) blocks --
+ * strictly lower blocks hold L_ik (L unit block-lower), the others U_ij; dinv[4 n] the inverses
+ * of U's diagonal blocks.  *levels (may be NULL): number of dependency levels of the
+ * triangular sweeps.  BF_ERR_ARG on a BF handle. */
+bf_status bf_get_ilu(bf_handle h, double *lu, double *dinv, int32_t *levels);
+/* CPR handles: x = (L U)^-1 r, the ILU(0) forward and backward sweeps (vectors as bf_solve). */
+bf_status bf_ilu_solve(bf_handle h, const double *r, double *x, int32_t vec_mem, void *cuda_stream);
 /* Accumulated device time (ms, CUDA events on the solve stream), number of timed
  * regions and ALGORITHMIC bytes moved (each operand once per use)
  * of an instrumented kernel class since setup (requires opt.timing = 1):
  *   0 J SpMV (36 nnzb + 36 n bytes per launch), 1 GMRES orthogonalisation passes,
- *   2 whole BF apply, 3 whole bf_solve.  Any output pointer may be NULL. */
+ *   2 whole preconditioner apply, 3 whole bf_solve.  Any output pointer may be NULL. */
 bf_status bf_kernel_time(bf_handle h, int32_t kclass, double *ms, int64_t *launches, double *alg_bytes);
 /* Number of kernels this library launched since the handle was created. */
 bf_status bf_launch_count(bf_handle h, int64_t *launches);

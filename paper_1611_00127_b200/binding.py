@@ -25,7 +25,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE
 EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_update", "bf_destroy", "bf_last_error", "bf_spmv",
            "bf_assemble", "bf_assemble_nnzb", "bf_newton_update",
            "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_block",
-           "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
+           "bf_get_ilu", "bf_ilu_solve", "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
 
 
 class BFError(RuntimeError):
@@ -46,7 +46,7 @@ class bf_options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
                 ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
-                ("timing", C.c_int32)]
+                ("timing", C.c_int32), ("precond", C.c_int32)]
 
 
 class bf_twophase(C.Structure):
@@ -81,6 +81,8 @@ def _load():
     L.bf_num_levels.argtypes = [vp, i32, P(i32)]
     L.bf_get_level.argtypes = [vp, i32, i32, P(i32), P(i64), P(i64), vp, vp, vp, vp, vp, vp, vp, vp]
     L.bf_get_block.argtypes = [vp, i32, P(i64), vp, vp, vp]
+    L.bf_get_ilu.argtypes = [vp, vp, vp, P(i32)]
+    L.bf_ilu_solve.argtypes = [vp, vp, vp, i32, vp]
     L.bf_kernel_time.argtypes = [vp, i32, dp, P(i64), dp]
     L.bf_launch_count.argtypes = [vp, P(i64)]
     L.bf_device_bytes.argtypes = [vp, P(i64)]
@@ -224,7 +226,7 @@ def bf_num_levels(h, which) -> int:
 
 
 def bf_get_level(h, which, level):
-    """Copy level `level` of hierarchy `which` (0 A_ss, 1 S~) to host numpy arrays."""
+    """Copy level `level` of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp) to host numpy arrays."""
     n, nA, nP = C.c_int32(), C.c_int64(), C.c_int64()
     _check(lib.bf_get_level(h, which, level, C.byref(n), C.byref(nA), C.byref(nP), *([None] * 8)), h)
     n, nA, nP = n.value, nA.value, nP.value
@@ -261,10 +263,29 @@ def bf_get_block(h, which):
     return rp, ci[:nnz.value], v[:nnz.value]
 
 
-def bf_get_level_size(h, which=0, level=0) -> int:
+def bf_get_level_size(h, which=None, level=0) -> int:
+    """Rows of a level; which=None: the finest level of whichever hierarchy the handle built."""
     n = C.c_int32()
-    _check(lib.bf_get_level(h, which, level, C.byref(n), None, None, *([None] * 8)), h)
+    for w in ((0, 2) if which is None else (which,)):
+        if lib.bf_get_level(h, w, level, C.byref(n), None, None, *([None] * 8)) == BF_OK:
+            return n.value
+    _check(lib.bf_get_level(h, 0 if which is None else which, level, C.byref(n), None, None, *([None] * 8)), h)
     return n.value
+
+
+def bf_get_ilu(h, nnzb, n):
+    """CPR handles: (lu [nnzb,2,2], dinv [n,2,2], levels) host copies of the block ILU(0) of J."""
+    lu = np.empty(4 * nnzb)
+    dinv = np.empty(4 * n)
+    lev = C.c_int32()
+    _check(lib.bf_get_ilu(h, C.c_void_p(lu.ctypes.data), C.c_void_p(dinv.ctypes.data), C.byref(lev)), h)
+    return lu.reshape(-1, 2, 2), dinv.reshape(-1, 2, 2), lev.value
+
+
+def bf_ilu_solve(h, r, x, stream=None):
+    (rp, mr), (xp, mx) = _ptr(r), _ptr(x)
+    assert mr == mx
+    _check(lib.bf_ilu_solve(h, rp, xp, mr, _stream(stream)), h)
 
 
 def bf_kernel_time(h, kclass):
@@ -317,6 +338,12 @@ class BFSolver:
 
     def block(self, which):
         return bf_get_block(self.h, which)
+
+    def ilu(self, nnzb):
+        return bf_get_ilu(self.h, nnzb, self.n)
+
+    def ilu_solve(self, r, x, stream=None):
+        bf_ilu_solve(self.h, r, x, stream)
 
     def close(self):
         if getattr(self, "h", None):

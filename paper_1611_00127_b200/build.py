@@ -24,7 +24,7 @@ SO = os.path.join(PKG, "libbf.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
            "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")] + ARCH
-NOFMA = {"k_split.cu", "k_amg_setup.cu"}
+NOFMA = {"k_split.cu", "k_amg_setup.cu", "k_ilu.cu"}
 
 
 def nvcc():

@@ -245,6 +245,7 @@ bf_status bf_default_options(bf_options *o) {
   o->schur_as_printed = 0;
   o->interp_norm = 1;
   o->timing = 0;
+  o->precond = 0;
   return BF_OK;
 }
 
@@ -257,6 +258,7 @@ static const char *check_options(const bf_options *o) {
   if (o->smoother == 1 && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
   if (o->smoother == 1 && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
   if (o->orth != 0 && o->orth != 1) return "orth must be 0 or 1";
+  if (o->precond < 0 || o->precond > 2) return "precond must be 0 (BF), 1 (CPR-AMG(1)) or 2 (CPR-AMG(2))";
   return nullptr;
 }
 
@@ -296,16 +298,28 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     lap("ingest");
     build_split(c);
     lap("split");
-    build_schur(c);
-    lap("schur");
-    tile_csr(c, c->blk[1]);
-    setup_dia(c, c->blk[1]);
     if (getenv("BF_NO_TMA")) c->use_tma = false;
     if (getenv("BF_NO_PDL")) c->use_pdl = false;
-    build_hierarchy(c, 0, c->blk[3]);
-    lap("amg A_ss");
-    build_hierarchy(c, 1, c->blk[4]);
-    lap("amg S~");
+    const int pc = c->opt.precond;
+    if (pc == 0) {  // BF (Algorithm 3): S~, the A_ps coupling, hierarchies A_ss and S~
+      build_schur(c);
+      lap("schur");
+      tile_csr(c, c->blk[1]);
+      setup_dia(c, c->blk[1]);
+      build_hierarchy(c, 0, c->blk[3]);
+      lap("amg A_ss");
+      build_hierarchy(c, 1, c->blk[4]);
+      lap("amg S~");
+    } else {  // CPR-AMG(1)/(2) (Algorithms 1, 2): A_pp [and A_ss] hierarchies, ILU(0) of J
+      build_hierarchy(c, 2, c->blk[0]);
+      lap("amg A_pp");
+      if (pc == 2) {
+        build_hierarchy(c, 0, c->blk[3]);
+        lap("amg A_ss");
+      }
+      build_ilu(c);
+      lap("ilu0");
+    }
     alloc_solve_workspace(c, 30);
     BF_CUDA(cudaStreamSynchronize(c->stream));
     lap("workspace");
@@ -338,11 +352,17 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
   dfree(c, c->dss);
   c->dss = nullptr;
   build_split(c);
-  build_schur(c);
-  tile_csr(c, c->blk[1]);
-  setup_dia(c, c->blk[1]);
-  refresh_finest(c, 0, c->blk[3]);
-  refresh_finest(c, 1, c->blk[4]);
+  if (c->opt.precond == 0) {
+    build_schur(c);
+    tile_csr(c, c->blk[1]);
+    setup_dia(c, c->blk[1]);
+    refresh_finest(c, 0, c->blk[3]);
+    refresh_finest(c, 1, c->blk[4]);
+  } else {
+    refresh_finest(c, 2, c->blk[0]);
+    if (c->opt.precond == 2) refresh_finest(c, 0, c->blk[3]);
+    build_ilu(c);  // numeric refactorization on the kept schedule
+  }
   sync(c);
   return BF_OK;
   BF_GUARD_END(c)
@@ -471,7 +491,8 @@ bf_status bf_apply_precond(bf_handle c, const double *r, double *z, int32_t vec_
 }
 
 bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int32_t vec_mem, void *stream) {
-  if (!c || !b || !x || which < 0 || which > 1 || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  if (!c || !b || !x || which < 0 || which > 2 || c->h[which].nlev == 0 || (vec_mem != 0 && vec_mem != 1))
+    return BF_ERR_ARG;
   BF_GUARD_BEGIN
   c->stream = (cudaStream_t)stream;
   size_t bytes = sizeof(double) * (size_t)c->n;
@@ -490,7 +511,7 @@ bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int3
 }
 
 bf_status bf_num_levels(bf_handle c, int32_t which, int32_t *nlev) {
-  if (!c || !nlev || which < 0 || which > 1) return BF_ERR_ARG;
+  if (!c || !nlev || which < 0 || which > 2) return BF_ERR_ARG;
   *nlev = c->h[which].nlev;
   return BF_OK;
 }
@@ -504,7 +525,7 @@ static void copy_csr_out(bf_ctx *c, const DCsr &A, int32_t *rp, int32_t *ci, dou
 bf_status bf_get_level(bf_handle c, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
                        int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val, int8_t *cf,
                        int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1) {
-  if (!c || which < 0 || which > 1 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
+  if (!c || which < 0 || which > 2 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
   BF_GUARD_BEGIN
   const Level &L = c->h[which].lv[level];
   bool coarsest = level == c->h[which].nlev - 1;
@@ -527,6 +548,31 @@ bf_status bf_get_block(bf_handle c, int32_t which, int64_t *nnz, int32_t *rowptr
   BF_GUARD_BEGIN
   if (nnz) *nnz = c->blk[which].nnz;
   copy_csr_out(c, c->blk[which], rowptr, col, val);
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_get_ilu(bf_handle c, double *lu, double *dinv, int32_t *levels) {
+  if (!c || !c->ilu_lu) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  if (lu) BF_CUDA(cudaMemcpyAsync(lu, c->ilu_lu, sizeof(double) * 4 * (size_t)c->nnzb, cudaMemcpyDeviceToHost, c->stream));
+  if (dinv) BF_CUDA(cudaMemcpyAsync(dinv, c->ilu_dinv, sizeof(double) * 4 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  if (levels) *levels = c->ilu_levels;
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  return BF_OK;
+  BF_GUARD_END(c)
+}
+
+bf_status bf_ilu_solve(bf_handle c, const double *r, double *x, int32_t vec_mem, void *stream) {
+  if (!c || !r || !x || !c->ilu_lu || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  BF_GUARD_BEGIN
+  c->stream = (cudaStream_t)stream;
+  const double *rd = vec_in(c, r, vec_mem, c->bd);
+  double *xd = vec_mem ? x : c->xd;
+  ilu_solve_into(c, rd, xd);
+  if (!vec_mem)
+    BF_CUDA(cudaMemcpyAsync(x, xd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
   return BF_OK;
   BF_GUARD_END(c)

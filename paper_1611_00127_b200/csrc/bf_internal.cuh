@@ -91,7 +91,14 @@ struct bf_ctx {
   int32_t jdia_k = 0, jdia_off[8] = {0};
   bf::DCsr blk[5];       // A_pp, A_ps, A_sp, A_ss, S~
   double *dss = nullptr;
-  bf::Hier h[2];
+  bf::Hier h[3];         // AMG hierarchies: 0 A_ss, 1 S~ (BF), 2 A_pp (CPR)
+  // CPR-AMG(1)/(2) block ILU(0) of J (k_ilu.cu)
+  int32_t *ilu_perm = nullptr, *ilu_dpos = nullptr;  // level-sorted row schedule, diagonal block positions
+  int32_t ilu_levels = 0;
+  double *ilu_lu = nullptr, *ilu_dinv = nullptr;     // factors on J's block pattern, inverse pivot blocks
+  int *ilu_flag = nullptr;                           // per-row completion flags of the sync-free sweeps
+  unsigned *ilu_sync = nullptr;                      // tickets / epoch of the sweeps
+  double *ilu_y = nullptr, *ilu_u = nullptr;         // forward result, CPR first-stage solution (canonical)
   // solve workspace
   int32_t Vm = 0;
   double *Z = nullptr;  // preconditioned basis z_j = M^-1 v_j (restart x N)
@@ -114,8 +121,13 @@ struct bf_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaGraph_t apply_graph = nullptr;
   cudaGraphExec_t apply_exec = nullptr;
-  cudaGraphNode_t apply_split_node = nullptr, apply_merge_node = nullptr;
-  cudaKernelNodeParams split_params{}, merge_params{};
+  struct PatchNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams params;
+    int nargs = 0;
+    std::vector<std::pair<int, int>> roles;  // (argument index, 0 v | 1 nrm2 | 2 z)
+  };
+  std::vector<PatchNode> apply_patch;
   int64_t apply_graph_kernels = 0;
   int num_sms = 148;
   bool use_tma = true;
@@ -185,6 +197,11 @@ void alloc_solve_workspace(bf_ctx *c, int restart);                     // k_gmr
 void assemble(bf_ctx *c, const bf_twophase *P, const double *p, const double *sn, int32_t *rp, int32_t *ci,
               double *vals, double *R);                                   // k_assemble.cu
 void newton_update(bf_ctx *c, int n, double *p, double *sn, const double *delta, double chop);
+void build_ilu(bf_ctx *c);                                              // k_ilu.cu
+void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2);
+double cpr_model_bytes(bf_ctx *c);
+bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles);
+void ilu_solve_into(bf_ctx *c, const double *r, double *x);              // x = (LU)^-1 r, caller order
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
 

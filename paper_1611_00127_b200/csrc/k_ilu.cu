@@ -1,0 +1,542 @@
+// k_ilu.cu -- the two-stage CPR preconditioners of PAPER.md:
+//   Algorithm 1, CPR-AMG(1) (combinative), and Algorithm 2, CPR-AMG(2) (additive), P:L159-193:
+//     u = P_1^-1 r                       P_1 = block ILU(0) of J (reading R18)
+//     t = r - J u
+//     A_pp dp = R_p t                     one AMG V-cycle (hierarchy 2)
+//    [A_ss ds = R_s t                     one AMG V-cycle (hierarchy 0), Algorithm 2 only]
+//     z = u + R_p^T dp [+ R_s^T ds]
+//
+// ILU(0) on the GPU.  The factorization and both triangular solves follow the row
+// dependencies of J's block pattern in its natural (point) order -- the same ILU(0) as the
+// oracle, not a reordered one.  Rows are grouped by dependency level (level(i) = 1 + max
+// level of the rows it depends on; i+j+k on a 7-point grid, 3*128-2 levels at 128^3) and
+// processed by ONE persistent "sync-free" kernel per sweep: warps take 32 consecutive rows of
+// the level-sorted order from an atomic ticket, every lane polls the completion flags of its
+// row's dependencies (acquire loads), computes its row once they are all set, publishes the
+// row (release store of the flag).  A warp only waits on rows with smaller tickets, which were
+// taken by warps already resident, so the scheme cannot deadlock; lanes poll inside a
+// warp-uniform loop, so no lane ever blocks another.
+//
+// Determinism: every factor value is computed by one thread in the oracle's order with the
+// multiply and add rounded separately (this TU is built with --fmad=false), so the factors
+// are bit-identical to or_ilu0 (determinism contract); the solves use the same
+// ascending order per row.
+//
+// Roofline: the solves are HBM/latency bound (each moves J's blocks once: 36 B/block plus
+// vectors) but their critical path is the number of levels times one L2 round trip.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "bf_internal.cuh"
+
+namespace bf {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned *p) {
+  return *reinterpret_cast<const volatile unsigned *>(p);
+}
+
+// next 32 rows of the schedule for this warp (ticket shared by the whole grid)
+__device__ __forceinline__ unsigned warp_ticket(unsigned *ticket) {
+  unsigned base = 0;
+  if ((threadIdx.x & 31) == 0) base = atomicAdd(ticket, 32u);
+  return __shfl_sync(FULL, base, 0);
+}
+
+// ---- setup: dependency levels, schedule, diagonal positions ---------------------------
+// level[i] (init -1) doubles as the completion flag; rows in natural order
+__global__ void k_ilu_levels(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, int *level,
+                             unsigned *ticket) {
+  for (;;) {
+    unsigned base = warp_ticket(ticket);
+    if (base >= (unsigned)n) return;
+    int i = base + (threadIdx.x & 31);
+    bool done = i >= n;
+    int lo = done ? 0 : rp[i], hi = done ? 0 : rp[i + 1];
+    while (!__all_sync(FULL, done)) {
+      if (!done) {
+        int lev = 0;
+        bool ready = true;
+        for (int q = lo; q < hi; q++) {
+          int k = ci[q];
+          if (k >= i) break;
+          int lk = ld_acquire(level + k);
+          if (lk < 0) {
+            ready = false;
+            break;
+          }
+          lev = max(lev, lk + 1);
+        }
+        if (ready) {
+          st_release(level + i, lev);
+          done = true;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_ilu_keys(int n, const int *__restrict__ level, const int32_t *__restrict__ rp,
+                           const int32_t *__restrict__ ci, uint64_t *keys, int32_t *dpos) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = ((uint64_t)(uint32_t)level[i] << 32) | (uint32_t)i;
+  int d = -1;
+  for (int q = rp[i]; q < rp[i + 1]; q++)
+    if (ci[q] == i) d = q;
+  dpos[i] = d;
+}
+
+__global__ void k_ilu_perm(int n, const uint64_t *__restrict__ keys, int32_t *perm) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) perm[t] = (int32_t)(keys[t] & 0xffffffffu);
+}
+
+// ---- setup: numeric factorization (oracle or_ilu0) ------------------------------
+// 2x2 products entry (r,c) = A_r0 B_0c + A_r1 B_1c (no FMA: --fmad=false)
+struct B2 {
+  double a, b, c, d;  // row-major {b00, b01, b10, b11}
+};
+__device__ __forceinline__ B2 ldg_blk(const double *p) {  // another row's finished block (L2)
+  double2 x = __ldcg(reinterpret_cast<const double2 *>(p));
+  double2 y = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
+  return {x.x, x.y, y.x, y.y};
+}
+__device__ __forceinline__ B2 ld_blk(const double *p) {
+  double2 x = reinterpret_cast<const double2 *>(p)[0];
+  double2 y = reinterpret_cast<const double2 *>(p)[1];
+  return {x.x, x.y, y.x, y.y};
+}
+__device__ __forceinline__ void st_blk(double *p, B2 v) {
+  reinterpret_cast<double2 *>(p)[0] = make_double2(v.a, v.b);
+  reinterpret_cast<double2 *>(p)[1] = make_double2(v.c, v.d);
+}
+__device__ __forceinline__ B2 mul(B2 A, B2 B) {
+  return {A.a * B.a + A.b * B.c, A.a * B.b + A.b * B.d, A.c * B.a + A.d * B.c, A.c * B.b + A.d * B.d};
+}
+
+__global__ void k_ilu_factor(int n, const int32_t *__restrict__ perm, const int32_t *__restrict__ rp,
+                             const int32_t *__restrict__ ci, const int32_t *__restrict__ dpos, double *lu,
+                             double *dinv, int *flag, unsigned *ticket, int *bad) {
+  for (;;) {
+    unsigned base = warp_ticket(ticket);
+    if (base >= (unsigned)n) return;
+    unsigned t = base + (threadIdx.x & 31);
+    bool done = t >= (unsigned)n;
+    int i = done ? 0 : perm[t];
+    int lo = done ? 0 : rp[i], hi = done ? 0 : rp[i + 1], di = done ? 0 : dpos[i];
+    while (!__all_sync(FULL, done)) {
+      if (!done) {
+        bool ready = true;
+        for (int q = lo; q < di && ready; q++) ready = ld_acquire(flag + ci[q]) != 0;
+        if (ready) {
+          for (int q = lo; q < di; q++) {  // k < i ascending
+            int k = ci[q];
+            B2 L = mul(ld_blk(lu + 4 * (size_t)q), ldg_blk(dinv + 4 * (size_t)k));  // a_ik a_kk^-1
+            st_blk(lu + 4 * (size_t)q, L);
+            int u = dpos[k] + 1, ue = rp[k + 1];
+            for (int s = q + 1; s < hi; s++) {  // j > k in row i; (k, j) in row k's upper part
+              int j = ci[s];
+              while (u < ue && __ldcg(ci + u) < j) u++;
+              if (u == ue) break;
+              if (__ldcg(ci + u) != j) continue;
+              B2 P = mul(L, ldg_blk(lu + 4 * (size_t)u));
+              B2 A = ld_blk(lu + 4 * (size_t)s);
+              st_blk(lu + 4 * (size_t)s, {A.a - P.a, A.b - P.b, A.c - P.c, A.d - P.d});
+            }
+          }
+          B2 D = ld_blk(lu + 4 * (size_t)di);
+          double det = D.a * D.d - D.b * D.c;
+          if (det == 0.0 || !isfinite(det)) atomicMin(bad, i);
+          st_blk(dinv + 4 * (size_t)i, {D.d / det, -D.b / det, -D.c / det, D.a / det});
+          __threadfence();
+          st_release(flag + i, 1);
+          done = true;
+        }
+      }
+    }
+  }
+}
+
+// ---- solve: y = L^-1 r (forward), x = U^-1 y (backward) ---------------------------------
+// Sync state shared by the two sweeps: tickets are reset by the other sweep's last warp, the
+// flag targets are 2e+1 (forward) and 2e+2 (backward) of the epoch e, advanced by the last
+// warp of the backward sweep -- no memset between applies, graph-capturable.
+struct IluSync {
+  unsigned ticket[2];
+  unsigned done[2];
+  unsigned epoch;
+  unsigned pad[3];
+};
+
+__device__ __forceinline__ void sweep_exit(IluSync *sy, int which) {
+  if ((threadIdx.x & 31) != 0) return;
+  unsigned nw = gridDim.x * (blockDim.x >> 5);
+  __threadfence();
+  if (atomicAdd(&sy->done[which], 1u) == nw - 1) {
+    sy->done[which] = 0;
+    sy->ticket[1 - which] = 0;  // the other sweep is not running (stream order)
+    if (which == 1) sy->epoch = sy->epoch + 1;
+    __threadfence();
+  }
+}
+
+// Up to PF dependency entries of a row (column and 2x2 block) are loaded into registers BEFORE
+// polling: they do not depend on other rows, so only the dependencies' results remain on the
+// critical path (one L2 round trip per level).  Rows with more entries load the rest on the fly.
+constexpr int PF = 4;
+
+struct DepCache {
+  int col[PF];
+  double2 b01[PF], b23[PF];
+};
+__device__ __forceinline__ void dep_prefetch(DepCache &dc, int lo, int hi, const int32_t *__restrict__ ci,
+                                             const double *__restrict__ lu) {
+#pragma unroll
+  for (int e = 0; e < PF; e++) {
+    if (lo + e < hi) {
+      int q = lo + e;
+      dc.col[e] = __ldg(ci + q);
+      dc.b01[e] = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q);
+      dc.b23[e] = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q + 1);
+    }
+  }
+}
+__device__ __forceinline__ bool deps_ready(const DepCache &dc, int lo, int hi, const int32_t *__restrict__ ci,
+                                           const int *flag, int target) {
+  bool ready = true;
+#pragma unroll
+  for (int e = 0; e < PF; e++)
+    if (lo + e < hi) ready = ready && ld_acquire(flag + dc.col[e]) == target;
+  for (int q = lo + PF; q < hi && ready; q++) ready = ld_acquire(flag + __ldg(ci + q)) == target;
+  return ready;
+}
+// t -= sum_q B_q v[col_q], ascending q (the oracle's order)
+__device__ __forceinline__ void dep_subtract(const DepCache &dc, int lo, int hi, const int32_t *__restrict__ ci,
+                                             const double *__restrict__ lu, const double2 *v, double &t0,
+                                             double &t1) {
+#pragma unroll
+  for (int e = 0; e < PF; e++) {
+    if (lo + e < hi) {
+      double2 vk = __ldcg(v + dc.col[e]);
+      t0 = t0 - (dc.b01[e].x * vk.x + dc.b01[e].y * vk.y);
+      t1 = t1 - (dc.b23[e].x * vk.x + dc.b23[e].y * vk.y);
+    }
+  }
+  for (int q = lo + PF; q < hi; q++) {
+    double2 b01 = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q);
+    double2 b23 = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q + 1);
+    double2 vk = __ldcg(v + __ldg(ci + q));
+    t0 = t0 - (b01.x * vk.x + b01.y * vk.y);
+    t1 = t1 - (b23.x * vk.x + b23.y * vk.y);
+  }
+}
+
+// r: caller-ordered interleaved vector (v_j of GMRES); nrm2 != null: r is the unnormalised
+// basis slot with ||r||^2 = *nrm2 and is normalised here, in place (the BF split kernel's job
+// on the BF path).  y: canonical (p, s) pairs.  y_i = r_i - sum_{k<i} L_ik y_k.
+__global__ void __launch_bounds__(256) k_ilu_fwd(int n, const int32_t *__restrict__ perm,
+                                                 const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                 const int32_t *__restrict__ dpos, const double *__restrict__ lu,
+                                                 double2 *r, const double *nrm2, double2 *y, int *flag,
+                                                 IluSync *sy, int ip) {
+  const int target = 2 * (int)ld_volatile_u32(&sy->epoch) + 1;
+  const double sc = nrm2 ? 1.0 / sqrt(*nrm2) : 1.0;
+  for (;;) {
+    unsigned base = warp_ticket(&sy->ticket[0]);
+    if (base >= (unsigned)n) break;
+    unsigned t = base + (threadIdx.x & 31);
+    bool done = t >= (unsigned)n;
+    int i = done ? 0 : __ldg(perm + t);
+    int lo = done ? 0 : __ldg(rp + i), di = done ? 0 : __ldg(dpos + i);
+    DepCache dc;
+    dep_prefetch(dc, lo, di, ci, lu);
+    double y0 = 0.0, y1 = 0.0;
+    if (!done) {
+      double2 a = r[i];
+      if (nrm2) {
+        a.x = a.x * sc;
+        a.y = a.y * sc;
+        r[i] = a;
+      }
+      y0 = ip ? a.y : a.x;
+      y1 = ip ? a.x : a.y;
+    }
+    while (!__all_sync(FULL, done)) {
+      if (!done && deps_ready(dc, lo, di, ci, flag, target)) {
+        dep_subtract(dc, lo, di, ci, lu, y, y0, y1);
+        y[i] = make_double2(y0, y1);
+        __threadfence();
+        st_release(flag + i, target);
+        done = true;
+      }
+    }
+  }
+  sweep_exit(sy, 0);
+}
+
+// x (canonical) = U^-1 y:  x_i = D_i^-1 (y_i - sum_{j>i} U_ij x_j)
+__global__ void __launch_bounds__(256) k_ilu_bwd(int n, const int32_t *__restrict__ perm,
+                                                 const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                 const int32_t *__restrict__ dpos, const double *__restrict__ lu,
+                                                 const double *__restrict__ dinv, const double2 *y, double2 *x,
+                                                 int *flag, IluSync *sy) {
+  const int target = 2 * (int)ld_volatile_u32(&sy->epoch) + 2;
+  for (;;) {
+    unsigned base = warp_ticket(&sy->ticket[1]);
+    if (base >= (unsigned)n) break;
+    unsigned t = base + (threadIdx.x & 31);
+    bool done = t >= (unsigned)n;
+    int i = done ? 0 : __ldg(perm + (n - 1 - (int)t));
+    int lo = done ? 0 : __ldg(dpos + i) + 1, hi = done ? 0 : __ldg(rp + i + 1);
+    DepCache dc;
+    dep_prefetch(dc, lo, hi, ci, lu);
+    double t0 = 0.0, t1 = 0.0;
+    double2 d01 = make_double2(0.0, 0.0), d23 = d01;
+    if (!done) {
+      double2 yi = __ldcg(y + i);
+      t0 = yi.x;
+      t1 = yi.y;
+      d01 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i);
+      d23 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i + 1);
+    }
+    while (!__all_sync(FULL, done)) {
+      if (!done && deps_ready(dc, lo, hi, ci, flag, target)) {
+        dep_subtract(dc, lo, hi, ci, lu, x, t0, t1);
+        x[i] = make_double2(d01.x * t0 + d01.y * t1, d23.x * t0 + d23.y * t1);
+        __threadfence();
+        st_release(flag + i, target);
+        done = true;
+      }
+    }
+  }
+  sweep_exit(sy, 1);
+}
+
+// ---- CPR: t = r - J u, split into the right-hand sides of the inner V-cycles --------------
+// (Alg. 1/2 steps 3-4[-5]); writes the level invariant of vcycle_level: b and x0 = beta b ./ dl1.
+// J from its DIA copy when present (coalesced), else the CSR-BSR rows.
+struct JDia {
+  int k;
+  int off[8];
+};
+__global__ void __launch_bounds__(256) k_cpr_resid(int n, const int32_t *__restrict__ rp,
+                                                   const int32_t *__restrict__ ci, const double2 *__restrict__ bv,
+                                                   const double2 *__restrict__ jd, JDia o,
+                                                   const double2 *__restrict__ u, const double2 *__restrict__ r,
+                                                   double *__restrict__ bp, double *__restrict__ xp,
+                                                   const double *__restrict__ dp, double *__restrict__ bs,
+                                                   double *__restrict__ xs, const double *__restrict__ ds,
+                                                   double beta, int ip) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double w0 = 0.0, w1 = 0.0;
+  if (jd) {
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+      int col = i + o.off[d];
+      if (d < o.k && col >= 0 && col < n) {
+        size_t e = ((size_t)d * n + i) * 2;
+        double2 v01 = __ldcs(jd + e), v23 = __ldcs(jd + e + 1);
+        double2 uc = __ldg(u + col);
+        w0 += v01.x * uc.x + v01.y * uc.y;
+        w1 += v23.x * uc.x + v23.y * uc.y;
+      }
+    }
+  } else {
+    for (int q = __ldg(rp + i); q < __ldg(rp + i + 1); q++) {
+      double2 v01 = __ldcs(bv + 2 * (size_t)q), v23 = __ldcs(bv + 2 * (size_t)q + 1);
+      double2 uc = __ldg(u + __ldg(ci + q));
+      w0 += v01.x * uc.x + v01.y * uc.y;
+      w1 += v23.x * uc.x + v23.y * uc.y;
+    }
+  }
+  double2 ri = r[i];
+  double tp = (ip ? ri.y : ri.x) - w0, ts = (ip ? ri.x : ri.y) - w1;
+  bp[i] = tp;
+  xp[i] = beta * (tp * dp[i]);
+  if (bs) {
+    bs[i] = ts;
+    xs[i] = beta * (ts * ds[i]);
+  }
+}
+
+// z = u + R_p^T dp [+ R_s^T ds] in the caller's var_order (Alg. 1 step 5 / Alg. 2 step 6)
+__global__ void k_cpr_merge(int n, const double2 *__restrict__ u, const double *__restrict__ dp,
+                            const double *__restrict__ ds, double2 *__restrict__ z, int ip) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 a = u[i];
+  double p = a.x + dp[i], s = ds ? a.y + ds[i] : a.y;
+  z[i] = ip ? make_double2(s, p) : make_double2(p, s);
+}
+
+// ---- host side -------------------------------------------------------------------------
+static int ilu_grid(bf_ctx *c) { return c->num_sms * 4; }  // 4 CTAs of 256 threads per SM
+
+void build_ilu(bf_ctx *c) {
+  int n = c->n;
+  int64_t nnzb = c->nnzb;
+  if (!c->ilu_perm) {  // schedule (pattern only; kept across bf_update)
+    int *level = dalloc_t<int>(c, n);
+    unsigned *tk = dalloc_t<unsigned>(c, 4);
+    BF_CUDA(cudaMemsetAsync(level, 0xff, sizeof(int) * n, c->stream));
+    BF_CUDA(cudaMemsetAsync(tk, 0, sizeof(unsigned) * 4, c->stream));
+    k_ilu_levels<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->brp, c->bci, level, tk);
+    uint64_t *keys = dalloc_t<uint64_t>(c, n), *keys2 = dalloc_t<uint64_t>(c, n);
+    c->ilu_dpos = dalloc_t<int32_t>(c, n);
+    k_ilu_keys<<<div_up(n, 256), 256, 0, c->stream>>>(n, level, c->brp, c->bci, keys, c->ilu_dpos);
+    cub::DoubleBuffer<uint64_t> kb(keys, keys2);
+    size_t tmp = 0;
+    BF_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, n, 0, 64, c->stream));
+    void *tb = dalloc(c, tmp + 16);
+    BF_CUDA(cub::DeviceRadixSort::SortKeys(tb, tmp, kb, n, 0, 64, c->stream));
+    c->ilu_perm = dalloc_t<int32_t>(c, n);
+    k_ilu_perm<<<div_up(n, 256), 256, 0, c->stream>>>(n, kb.Current(), c->ilu_perm);
+    c->launches += 6;
+    BF_CUDA(cudaGetLastError());
+    int maxlev = 0;
+    BF_CUDA(cudaMemcpyAsync(&maxlev, reinterpret_cast<const char *>(kb.Current() + (n - 1)) + 4, sizeof(int),
+                            cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    c->ilu_levels = maxlev + 1;
+    dfree(c, tb);
+    dfree(c, keys);
+    dfree(c, keys2);
+    dfree(c, level);
+    dfree(c, tk);
+    c->ilu_flag = dalloc_t<int>(c, n);
+    c->ilu_sync = dalloc_t<unsigned>(c, sizeof(IluSync) / sizeof(unsigned));
+    c->ilu_lu = dalloc_t<double>(c, 4 * (size_t)nnzb);
+    c->ilu_dinv = dalloc_t<double>(c, 4 * (size_t)n);
+    c->ilu_y = dalloc_t<double>(c, 2 * (size_t)n);
+    c->ilu_u = dalloc_t<double>(c, 2 * (size_t)n);
+  }
+  // numeric factorization (oracle or_ilu0 order)
+  int *flag = dalloc_t<int>(c, n);
+  unsigned *tk = dalloc_t<unsigned>(c, 4);
+  int *bad = dalloc_t<int>(c, 1);
+  BF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int) * n, c->stream));
+  BF_CUDA(cudaMemsetAsync(tk, 0, sizeof(unsigned) * 4, c->stream));
+  BF_CUDA(cudaMemcpyAsync(bad, &n, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  BF_CUDA(cudaMemcpyAsync(c->ilu_lu, c->bv, sizeof(double) * 4 * (size_t)nnzb, cudaMemcpyDeviceToDevice,
+                          c->stream));
+  k_ilu_factor<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                   c->ilu_dinv, flag, tk, bad);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  int hb = n;
+  BF_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaMemsetAsync(c->ilu_flag, 0, sizeof(int) * n, c->stream));
+  BF_CUDA(cudaMemsetAsync(c->ilu_sync, 0, sizeof(IluSync), c->stream));
+  sync(c);
+  dfree(c, flag);
+  dfree(c, tk);
+  dfree(c, bad);
+  if (hb < n)
+    throw Error(BF_ERR_ZERO_DIAG, "ILU(0) pivot block singular at cell " + std::to_string(hb));
+}
+
+// u = (L U)^-1 r (canonical output in c->ilu_u); r in the caller's order, normalised in place
+// when nrm2 is given
+static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
+  int n = c->n;
+  IluSync *sy = reinterpret_cast<IluSync *>(c->ilu_sync);
+  k_ilu_fwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                reinterpret_cast<double2 *>(r), nrm2,
+                                                reinterpret_cast<double2 *>(c->ilu_y), c->ilu_flag, sy,
+                                                c->var_order);
+  k_ilu_bwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                c->ilu_dinv, reinterpret_cast<const double2 *>(c->ilu_y),
+                                                reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
+  c->launches += 2;
+  BF_CUDA(cudaGetLastError());
+}
+
+void vcycle_from_invariant(bf_ctx *c, int which);  // k_vcycle.cu
+double x0_beta_of(const bf_options &o);             // k_vcycle.cu
+
+void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
+  int n = c->n;
+  Hier &hp = c->h[2], &hs = c->h[0];
+  bool additive = c->opt.precond == 2;
+  ilu_solve(c, const_cast<double *>(v), nrm2);  // step 2
+  JDia o{};
+  o.k = c->jdia ? c->jdia_k : 0;
+  for (int d = 0; d < o.k; d++) o.off[d] = c->jdia_off[d];
+  k_cpr_resid<<<div_up(n, 256), 256, 0, c->stream>>>(
+      n, c->brp, c->bci, reinterpret_cast<const double2 *>(c->bv), reinterpret_cast<const double2 *>(c->jdia), o,
+      reinterpret_cast<const double2 *>(c->ilu_u), reinterpret_cast<const double2 *>(v), hp.lv[0].b, hp.lv[0].x,
+      hp.lv[0].d, additive ? hs.lv[0].b : nullptr, additive ? hs.lv[0].x : nullptr,
+      additive ? hs.lv[0].d : nullptr, x0_beta_of(c->opt), c->var_order);  // step 3
+  BF_LAUNCH(c);
+  vcycle_from_invariant(c, 2);  // step 4
+  if (additive) vcycle_from_invariant(c, 0);  // Alg. 2 step 5
+  k_cpr_merge<<<div_up(n, 256), 256, 0, c->stream>>>(n, reinterpret_cast<const double2 *>(c->ilu_u), hp.lv[0].x,
+                                                     additive ? hs.lv[0].x : nullptr,
+                                                     reinterpret_cast<double2 *>(z), c->var_order);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
+__global__ void k_to_caller(int n, const double2 *__restrict__ u, double2 *__restrict__ x, int ip) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = ip ? make_double2(u[i].y, u[i].x) : u[i];
+}
+
+// introspection (bf_ilu_solve): x = (L U)^-1 r, both in the caller's var_order
+void ilu_solve_into(bf_ctx *c, const double *r, double *x) {
+  if (!c->ilu_lu) throw Error(BF_ERR_ARG, "bf_ilu_solve: the handle has no ILU(0) (precond 0)");
+  ilu_solve(c, const_cast<double *>(r), nullptr);
+  k_to_caller<<<div_up(c->n, 256), 256, 0, c->stream>>>(c->n, reinterpret_cast<const double2 *>(c->ilu_u),
+                                                         reinterpret_cast<double2 *>(x), c->var_order);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
+// graph patching (k_vcycle.cu bf_apply_graph): which kernel arguments carry v, nrm2 and z
+bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
+  if (func == (const void *)k_ilu_fwd) {
+    nargs = 11;
+    roles = {{6, 0}, {7, 1}};
+  } else if (func == (const void *)k_cpr_resid) {
+    nargs = 16;
+    roles = {{7, 0}};
+  } else if (func == (const void *)k_cpr_merge) {
+    nargs = 6;
+    roles = {{4, 2}};
+  } else {
+    return false;
+  }
+  return true;
+}
+
+// algorithmic bytes of one CPR apply: ILU solves (J's blocks once: 36 B/block + row_ptr,
+// diagonal position, dinv 32 B, vectors r, y (w + r), x (w + r): 8+4+32+64 B/row), the
+// residual (a J SpMV, 36 nnzb + 36 n, + b/x0 outputs and 1/dl1 24 B per field), the V-cycles
+// (SURVEY 8(d) per-level model), the merge (u, dp[, ds], z)
+double cpr_model_bytes(bf_ctx *c) {
+  double n = c->n, nnzb = (double)c->nnzb;
+  bool additive = c->opt.precond == 2;
+  double bytes = 36.0 * nnzb + 108.0 * n;
+  bytes += 36.0 * nnzb + 36.0 * n + (additive ? 48.0 : 24.0) * n;
+  bytes += (additive ? 40.0 : 32.0) * n;
+  for (int w : {2, 0}) {
+    if (w == 0 && !additive) continue;
+    Hier &h = c->h[w];
+    for (int l = 0; l + 1 < h.nlev; l++)
+      bytes += 24.0 * h.lv[l].A.nnz + 24.0 * h.lv[l].P.nnz + 116.0 * h.lv[l].A.n + 12.0 * h.lv[l + 1].A.n;
+    bytes += 8.0 * h.nL * h.nL;
+  }
+  return bytes;
+}
+
+}  // namespace bf

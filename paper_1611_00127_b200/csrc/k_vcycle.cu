@@ -693,6 +693,11 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   }
 }
 
+double x0_beta_of(const bf_options &o) { return x0_beta(o); }
+
+// V-cycle of hierarchy `which` whose finest level already holds b and x0 (level invariant)
+void vcycle_from_invariant(bf_ctx *c, int which) { vcycle_level(c, c->h[which], 0); }
+
 void vcycle(bf_ctx *c, int which, const double *b, double *x) {
   Hier &h = c->h[which];
   Level &L0 = h.lv[0];
@@ -734,6 +739,10 @@ __global__ void k_merge_vec(int n, int ip, const double *__restrict__ p, const d
 }
 
 void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
+  if (c->opt.precond) {  // CPR-AMG(1)/(2), k_ilu.cu
+    cpr_apply(c, v, z, nrm2);
+    return;
+  }
   int n = c->n;
   int ip = c->var_order;
   Hier &hs = c->h[0], &hS = c->h[1];
@@ -774,20 +783,36 @@ void drop_apply_graph(bf_ctx *c) {
   if (c->apply_graph) cudaGraphDestroy(c->apply_graph);
   c->apply_exec = nullptr;
   c->apply_graph = nullptr;
-  c->apply_split_node = nullptr;
-  c->apply_merge_node = nullptr;
+  c->apply_patch.clear();
 }
 
-// The whole BF apply (~60 kernels, most of them small coarse-level kernels) replayed as one
-// CUDA graph: captured once per handle on a private stream, launched on the caller's stream.
-// Only the input vector changes between applies; it is patched into the split kernel node.
+// Kernel arguments of the captured apply that change per launch: role 0 = the input vector v,
+// 1 = the norm pointer for in-place normalisation, 2 = the output z.  The BF apply's only
+// reader of v is the split kernel and its only writer of z the merge kernel; the CPR apply's
+// are the ILU forward sweep, the residual kernel (v) and the merge kernel (z).
+static bool patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
+  if (func == (const void *)k_split_vec) {
+    nargs = 9;
+    roles = {{2, 0}, {8, 1}};
+  } else if (func == (const void *)k_merge_vec) {
+    nargs = 5;
+    roles = {{4, 2}};
+  } else {
+    return cpr_patch_roles(func, nargs, roles);
+  }
+  return true;
+}
+
+// The whole preconditioner apply (~40-60 kernels, most of them small coarse-level kernels)
+// replayed as one CUDA graph: captured once per handle on a private stream, launched on the
+// caller's stream.  Only v, the norm pointer and z change between applies; they are patched
+// into the kernel nodes that take them.
 void bf_apply_graph(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   if (!c->apply_exec) {
     if (!c->cap_stream) BF_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     cudaStream_t user = c->stream;
     c->stream = c->cap_stream;
     int64_t l0 = c->launches;
-    double b0 = c->alg_bytes;
     BF_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     try {
       bf_apply(c, v, z, nrm2);
@@ -802,51 +827,46 @@ void bf_apply_graph(bf_ctx *c, const double *v, double *z, const double *nrm2) {
     BF_CUDA(cudaStreamEndCapture(c->cap_stream, &g));
     c->stream = user;
     c->apply_graph_kernels = c->launches - l0;
-    c->apply_bytes = apply_model_bytes(c);
-    (void)b0;
+    c->apply_bytes = c->opt.precond ? cpr_model_bytes(c) : apply_model_bytes(c);
     c->launches = l0;
     BF_CUDA(cudaGraphInstantiate(&c->apply_exec, g, 0));
-    // locate the split node (the only reader of v) and the merge node (the only writer of z)
     size_t nn = 0;
     BF_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
     BF_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
-    c->apply_split_node = nullptr;
-    c->apply_merge_node = nullptr;
+    c->apply_patch.clear();
+    bool has_in = false, has_out = false;
     for (auto nd : nodes) {
       cudaGraphNodeType t;
       BF_CUDA(cudaGraphNodeGetType(nd, &t));
       if (t != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams p;
       BF_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
-      if (p.func == (void *)k_split_vec) {
-        c->apply_split_node = nd;
-        c->split_params = p;
-      } else if (p.func == (void *)k_merge_vec) {
-        c->apply_merge_node = nd;
-        c->merge_params = p;
+      bf_ctx::PatchNode pn;
+      if (!patch_roles(p.func, pn.nargs, pn.roles)) continue;
+      pn.node = nd;
+      pn.params = p;
+      for (auto &r : pn.roles) {
+        has_in |= r.second == 0;
+        has_out |= r.second == 2;
       }
+      c->apply_patch.push_back(pn);
     }
     c->apply_graph = g;
-    if (!c->apply_split_node || !c->apply_merge_node)
-      throw Error(BF_ERR_CUDA, "split/merge node not found in the BF apply graph");
+    if (!has_in || !has_out) throw Error(BF_ERR_CUDA, "input/output nodes not found in the apply graph");
   }
-  // patch the input pointer of the split kernel (argument 2: v; argument 8: the norm for in-place normalisation) and the output pointer of the
-  // merge kernel (argument 4: z); all other arguments are the handle's fixed buffers
   double *vin = const_cast<double *>(v);
   const double *nin = nrm2;
   double *zout = z;
-  void *sargs[9], *margs[5];
-  for (int k = 0; k < 9; k++) sargs[k] = c->split_params.kernelParams[k];
-  for (int k = 0; k < 5; k++) margs[k] = c->merge_params.kernelParams[k];
-  sargs[2] = (void *)&vin;
-  sargs[8] = (void *)&nin;
-  margs[4] = (void *)&zout;
-  cudaKernelNodeParams ps = c->split_params, pm = c->merge_params;
-  ps.kernelParams = sargs;
-  pm.kernelParams = margs;
-  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_split_node, &ps));
-  BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, c->apply_merge_node, &pm));
+  void *vals[3] = {(void *)&vin, (void *)&nin, (void *)&zout};
+  for (auto &pn : c->apply_patch) {
+    void *args[24];
+    for (int k = 0; k < pn.nargs; k++) args[k] = pn.params.kernelParams[k];
+    for (auto &r : pn.roles) args[r.first] = vals[r.second];
+    cudaKernelNodeParams p = pn.params;
+    p.kernelParams = args;
+    BF_CUDA(cudaGraphExecKernelNodeSetParams(c->apply_exec, pn.node, &p));
+  }
   cudaEvent_t t0;
   timer_begin(c, 2, &t0);
   BF_CUDA(cudaGraphLaunch(c->apply_exec, c->stream));

@@ -1,0 +1,7 @@
+# re-entry check: full GPU test suite, smoke, bench line
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench_now.json 2> gpurun_out/bench_now.err
+tail -c 600 gpurun_out/bench_now.json
