@@ -59,7 +59,8 @@ class BFs(C.Structure):
                 ("brp", C.POINTER(C.c_int64)), ("bci", C.POINTER(C.c_int32)), ("bv", C.POINTER(C.c_double)),
                 ("App", CSRs), ("Aps", CSRs), ("Asp", CSRs), ("Ass", CSRs), ("S", CSRs),
                 ("dss", C.POINTER(C.c_double)), ("hss", AMGs), ("hS", AMGs), ("opt", Options),
-                ("hpp", AMGs), ("ilu", C.POINTER(C.c_double)), ("ilu_dinv", C.POINTER(C.c_double))]
+                ("hpp", AMGs), ("ilu", C.POINTER(C.c_double)), ("ilu_dinv", C.POINTER(C.c_double)),
+                ("Jsc", CSRs), ("hJ", AMGs)]
 
 
 _lib = None
@@ -93,6 +94,7 @@ def lib():
         L.or_csr_free.argtypes = [P(CSRs)]
         L.or_ilu0.argtypes = [C.c_int32, lp, ip, dp, dp, dp]
         L.or_ilu0_solve.argtypes = [C.c_int32, lp, ip, dp, dp, dp, dp]
+        L.or_jscalar.argtypes = [C.c_int32, lp, ip, dp, P(CSRs)]
         L.or_bf_setup.argtypes = [C.c_int32, lp, ip, dp, C.c_int32, C.c_int32, P(Options), P(P(BFs))]
         L.or_bf_free.argtypes = [P(BFs)]
         L.or_bf_update.argtypes = [P(BFs), dp]
@@ -284,6 +286,16 @@ def l1diag(A: CSR):
     return d
 
 
+def jscalar(J) -> CSR:
+    """J as a scalar point-ordered CSR (coupled AMG, reading R20)."""
+    rp, ci, v = _bsr_arrays(J)
+    out = CSRs()
+    lib().or_jscalar(J.n, _p(rp, C.c_int64), _p(ci, C.c_int32), _p(v, C.c_double), C.byref(out))
+    r = _from_cstruct(out)
+    lib().or_csr_free(C.byref(out))
+    return r
+
+
 def ilu0(J):
     """Block ILU(0) of the 2x2 BSR J (canonical row-major blocks) on its own block pattern
     (reading R18).  Returns (lu [nnzb,2,2], dinv [n,2,2])."""
@@ -402,8 +414,8 @@ class BF:
         return np.ctypeslib.as_array(self.s.dss, (self.n,)).copy()
 
     def hierarchy(self, which):
-        """which: 0 -> A_ss, 1 -> S~, 2 -> A_pp (CPR)"""
-        return (self.s.hss, self.s.hS, self.s.hpp)[which]
+        """which: 0 -> A_ss, 1 -> S~, 2 -> A_pp (CPR), 3 -> J as a scalar matrix (coupled AMG)"""
+        return (self.s.hss, self.s.hS, self.s.hpp, self.s.hJ)[which]
 
     def ilu(self):
         """(lu [nnzb,2,2], dinv [n,2,2]) of the CPR preconditioner's block ILU(0)."""

@@ -736,11 +736,40 @@ void or_ilu0_solve(int32_t n, const int64_t *rp, const int32_t *ci, const double
   free(y);
 }
 
+/* Coupled "point" AMG: "in order to use BoomerAMG for the coupled system ...
+ * the Jacobian matrix needs to be ordered by grid points"; reading R20: the interleaved
+ * matrix is handed to the scalar AMG of c.2 step 3 as is. */
+void or_jscalar(int32_t n, const int64_t *rp, const int32_t *ci, const double *v, or_csr *out) {
+  int64_t cnt = 0;
+  for (int32_t c = 0; c < n; c++)
+    for (int r = 0; r < 2; r++)
+      for (int64_t q = rp[c]; q < rp[c + 1]; q++)
+        for (int s = 0; s < 2; s++)
+          if (v[4 * q + 2 * r + s] != 0.0 || (ci[q] == c && r == s)) cnt++;
+  csr_alloc(out, 2 * n, 2 * n, cnt);
+  int64_t k = 0;
+  for (int32_t c = 0; c < n; c++)
+    for (int r = 0; r < 2; r++) {
+      for (int64_t q = rp[c]; q < rp[c + 1]; q++)
+        for (int s = 0; s < 2; s++)
+          if (v[4 * q + 2 * r + s] != 0.0 || (ci[q] == c && r == s)) {
+            out->ci[k] = 2 * ci[q] + s;
+            out->v[k] = v[4 * q + 2 * r + s];
+            k++;
+          }
+      out->rp[2 * c + r + 1] = k;
+    }
+}
+
 /* hierarchies the chosen preconditioner uses: BF (Alg. 3) A_ss and S~; CPR-AMG(1) (Alg. 1)
  * A_pp; CPR-AMG(2) (Alg. 2) A_pp and A_ss */
 static int build_precond(or_bf *b) {
   const or_options *o = &b->opt;
   int st = 0;
+  if (o->precond == 3) {
+    or_jscalar(b->n, b->brp, b->bci, b->bv, &b->Jsc);
+    return or_amg_setup(&b->Jsc, o, &b->hJ);
+  }
   if (o->precond == 0 || o->precond == 2) {
     st = or_amg_setup(&b->Ass, o, &b->hss);
     if (st) return st;
@@ -754,7 +783,7 @@ static int build_precond(or_bf *b) {
 int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
                 int32_t block_order, int32_t var_order, const or_options *o, or_bf **out) {
   *out = NULL;
-  if (o->precond < 0 || o->precond > 2) { set_err("precond must be 0, 1 or 2"); return 1; }
+  if (o->precond < 0 || o->precond > 3) { set_err("precond must be 0, 1, 2 or 3"); return 1; }
   or_bf *b = (or_bf *)xcalloc(1, sizeof(or_bf));
   b->n = n;
   b->var_order = var_order;
@@ -771,7 +800,7 @@ int or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
     for (int r = 0; r < 2; r++)
       for (int c = 0; c < 2; c++) b->bv[4 * q + 2 * r + c] = vals[4 * q + blk_index(block_order, var_order, r, c)];
   b->dss = (double *)xmalloc((size_t)n * sizeof(double) + 8);
-  if (o->precond) {
+  if (o->precond == 1 || o->precond == 2) {
     b->ilu = (double *)xmalloc((size_t)nnzb * 4 * sizeof(double) + 8);
     b->ilu_dinv = (double *)xmalloc((size_t)n * 4 * sizeof(double) + 8);
   }
@@ -802,9 +831,13 @@ int or_bf_update(or_bf *b, const double *vals) {
                     b->dss);
   if (st) return st;
   or_schur(&b->App, &b->Aps, &b->Asp, b->dss, b->opt.schur_as_printed, &b->S);
-  or_amg *hs[3] = {&b->hss, &b->hS, &b->hpp};
-  const or_csr *A0[3] = {&b->Ass, &b->S, &b->App};
-  for (int k = 0; k < 3; k++) {
+  if (b->opt.precond == 3) {
+    or_csr_free(&b->Jsc);
+    or_jscalar(n, b->brp, b->bci, b->bv, &b->Jsc);
+  }
+  or_amg *hs[4] = {&b->hss, &b->hS, &b->hpp, &b->hJ};
+  const or_csr *A0[4] = {&b->Ass, &b->S, &b->App, &b->Jsc};
+  for (int k = 0; k < 4; k++) {
     or_amg *h = hs[k];
     if (h->nlev == 0) continue;                      /* not used by this preconditioner */
     if (h->nlev <= 1) {
@@ -817,7 +850,8 @@ int or_bf_update(or_bf *b, const double *vals) {
     csr_copy(A0[k], &h->A[0]);
     or_l1diag(&h->A[0], h->dl1[0]);
   }
-  if (b->opt.precond && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv)) return 4;
+  if ((b->opt.precond == 1 || b->opt.precond == 2) && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv))
+    return 4;
   return 0;
 }
 
@@ -826,7 +860,8 @@ void or_bf_free(or_bf *b) {
   free(b->brp); free(b->bci); free(b->bv); free(b->dss);
   or_csr_free(&b->App); or_csr_free(&b->Aps); or_csr_free(&b->Asp); or_csr_free(&b->Ass);
   or_csr_free(&b->S);
-  or_amg_free(&b->hss); or_amg_free(&b->hS); or_amg_free(&b->hpp);
+  or_amg_free(&b->hss); or_amg_free(&b->hS); or_amg_free(&b->hpp); or_amg_free(&b->hJ);
+  or_csr_free(&b->Jsc);
   free(b->ilu); free(b->ilu_dinv);
   free(b);
 }
@@ -878,7 +913,10 @@ void or_bf_apply(const or_bf *b, const double *v, double *z) {
     double *rc = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
     double *uc = (double *)xmalloc((size_t)2 * n * sizeof(double) + 8);
     for (int32_t c = 0; c < n; c++) { rc[2 * c] = v[2 * c + ip]; rc[2 * c + 1] = v[2 * c + is]; }
-    cpr_apply(b, rc, uc);
+    if (b->opt.precond == 3)
+      or_vcycle(&b->hJ, rc, uc);                    /* coupled point AMG: one V-cycle on J */
+    else
+      cpr_apply(b, rc, uc);
     for (int32_t c = 0; c < n; c++) { z[2 * c + ip] = uc[2 * c]; z[2 * c + is] = uc[2 * c + 1]; }
     free(rc); free(uc);
     return;

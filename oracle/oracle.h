@@ -36,7 +36,9 @@ typedef struct {
   int32_t  schur_as_printed; /* 0: A_sp (Q21); 1: literal P:L239 (A_pp) */
   int32_t  interp_norm;    /* 1: weights normalised to P 1 = 1 (R8, default); 0: Q26 denominators */
   int32_t  precond;        /* 0: BF (Algorithm 3, default); 1: CPR-AMG(1) combinative (Algorithm 1);
-                              2: CPR-AMG(2) additive (Algorithm 2) -- P:L159-193 */
+                              2: CPR-AMG(2) additive (Algorithm 2) -- P:L159-193, SURVEY 8(f) NEXT-3;
+                              3: coupled "point" AMG, one V-cycle on J itself as a scalar matrix in
+                                 point ordering (reading R20) */
 } or_options;
 
 #define OR_MAX_LEVELS 64
@@ -69,6 +71,9 @@ typedef struct {
   double *ilu;                    /* [4 nnzb] block ILU(0) factors on J's block pattern: strictly lower
                                      blocks hold L_ik (unit block-lower L), the rest hold U_ij */
   double *ilu_dinv;               /* [4 n] inverse of U's diagonal (pivot) blocks */
+  /* coupled point AMG (precond 3) */
+  or_csr Jsc;                     /* J as a scalar 2n x 2n CSR, point ordering (p,s per cell) */
+  or_amg hJ;                      /* its hierarchy */
 } or_bf;
 
 #ifdef __cplusplus
@@ -108,6 +113,9 @@ int  or_ilu0(int32_t n, const int64_t *rp, const int32_t *ci, const double *v, d
 /* x = (L U)^-1 r on canonical interleaved vectors (forward then backward block substitution) */
 void or_ilu0_solve(int32_t n, const int64_t *rp, const int32_t *ci, const double *lu, const double *dinv,
                    const double *r, double *x);
+/* J as a scalar CSR in point ordering (row 2c+r, column 2d+s = entry (r,s) of block (c,d));
+ * pattern = entries that are not +-0.0, plus the diagonal (the Q23 convention of the split) */
+void or_jscalar(int32_t n, const int64_t *rp, const int32_t *ci, const double *v, or_csr *out);
 int  or_bf_setup(int32_t n, const int64_t *rp, const int32_t *ci, const double *vals,
                  int32_t block_order, int32_t var_order, const or_options *o, or_bf **out);
 void or_bf_free(or_bf *b);

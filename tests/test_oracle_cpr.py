@@ -162,3 +162,32 @@ def test_cpr_var_order_and_update():
     assert np.array_equal(o.level(2, 0)["A"].to_dense(), oracle.split(J2)["App"].to_dense())
     if lev1 is not None:
         assert np.array_equal(o.level(2, 1)["A"].to_dense(), lev1)
+
+
+# ---------------------------------------------------------------------------- coupled point AMG
+def test_jscalar_is_point_ordered_J():
+    """The scalar matrix handed to the coupled AMG (reading R20) is J in point
+    ordering: dense-equal to the BSR J, pattern = nonzero entries plus the diagonal."""
+    prob, J, rhs = make_system(1, dims=(6, 5, 1))
+    A = oracle.jscalar(J)
+    D = J.to_dense()
+    assert np.array_equal(A.to_dense(), D)
+    nz = (D != 0) | np.eye(2 * J.n, dtype=bool)
+    assert A.nnz == int(nz.sum())
+    assert np.all(np.diff(A.ci[A.rp[0]:A.rp[1]]) > 0)
+
+
+def test_coupled_amg_exact_single_level_and_fails_on_transport():
+    """precond 3 with a single-level hierarchy is the exact solve (1 GMRES iteration); with the
+    default hierarchy it does not converge on the two-phase C1 Jacobian (the paper's finding,
+    P:L453 "Since AMG does not converge in this experiment")."""
+    prob, J, rhs = make_system(1, dims=(8, 6, 1))
+    r = oracle.BF(J, precond=3, max_coarse=BIG).gmres(rhs, tol=1e-10)
+    assert r["converged"] and r["iters"] == 1
+    prob, J, rhs = make_system(1)
+    o = oracle.BF(J, precond=3)
+    assert o.nlev(3) > 1
+    v = seeded_vector(2 * J.n, 1)
+    assert np.array_equal(o.apply(v), o.vcycle(3, v))
+    r = o.gmres(rhs, tol=1e-8, maxit=200)
+    assert not r["converged"]
