@@ -92,7 +92,10 @@ typedef struct {
                                   CPR: first stage P_1 = block ILU(0) of J on its block
                                   pattern in point order (R18), second stage
                                   one V-cycle on A_pp (hierarchy 2) [and on A_ss, hierarchy 0].
-                                  A singular ILU pivot block is BF_ERR_ZERO_DIAG naming the cell. */
+                                  A singular ILU pivot block is BF_ERR_ZERO_DIAG naming the cell.
+                                  3 coupled "point" AMG: one V-cycle of the same AMG on J itself as a
+                                  point-ordered scalar 2n x 2n matrix (R20;
+                                  hierarchy 3) -- the paper's AMG comparison. */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;
@@ -181,7 +184,8 @@ bf_status bf_spmv(bf_handle h, const double *x, double *y, int32_t vec_mem, void
 /* z = M^-1 r: one application of the handle's preconditioner (Algorithm 3, or
  * Algorithm 1/2, per opt.precond). */
 bf_status bf_apply_precond(bf_handle h, const double *r, double *z, int32_t vec_mem, void *cuda_stream);
-/* x = one V-cycle of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp) applied to b (length n_cells).
+/* x = one V-cycle of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp, 3 J scalar) applied to b (length
+ * n_cells; 2 n_cells for hierarchy 3, canonical (p,s) interleaving).
  * BF_ERR_ARG for a hierarchy the handle's preconditioner does not build. */
 bf_status bf_vcycle(bf_handle h, int32_t which, const double *b, double *x, int32_t vec_mem,
                     void *cuda_stream);

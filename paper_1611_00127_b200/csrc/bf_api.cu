@@ -258,7 +258,8 @@ static const char *check_options(const bf_options *o) {
   if (o->smoother == 1 && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
   if (o->smoother == 1 && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
   if (o->orth != 0 && o->orth != 1) return "orth must be 0 or 1";
-  if (o->precond < 0 || o->precond > 2) return "precond must be 0 (BF), 1 (CPR-AMG(1)) or 2 (CPR-AMG(2))";
+  if (o->precond < 0 || o->precond > 3)
+    return "precond must be 0 (BF), 1 (CPR-AMG(1)), 2 (CPR-AMG(2)) or 3 (coupled AMG)";
   return nullptr;
 }
 
@@ -310,6 +311,10 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
       lap("amg A_ss");
       build_hierarchy(c, 1, c->blk[4]);
       lap("amg S~");
+    } else if (pc == 3) {  // coupled point AMG on J
+      build_jscalar(c, c->jsc);
+      build_hierarchy(c, 3, c->jsc);
+      lap("amg J");
     } else {  // CPR-AMG(1)/(2) (Algorithms 1, 2): A_pp [and A_ss] hierarchies, ILU(0) of J
       build_hierarchy(c, 2, c->blk[0]);
       lap("amg A_pp");
@@ -358,6 +363,10 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
     setup_dia(c, c->blk[1]);
     refresh_finest(c, 0, c->blk[3]);
     refresh_finest(c, 1, c->blk[4]);
+  } else if (c->opt.precond == 3) {
+    free_csr(c, c->jsc);
+    build_jscalar(c, c->jsc);
+    refresh_finest(c, 3, c->jsc);
   } else {
     refresh_finest(c, 2, c->blk[0]);
     if (c->opt.precond == 2) refresh_finest(c, 0, c->blk[3]);
@@ -491,11 +500,11 @@ bf_status bf_apply_precond(bf_handle c, const double *r, double *z, int32_t vec_
 }
 
 bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int32_t vec_mem, void *stream) {
-  if (!c || !b || !x || which < 0 || which > 2 || c->h[which].nlev == 0 || (vec_mem != 0 && vec_mem != 1))
+  if (!c || !b || !x || which < 0 || which > 3 || c->h[which].nlev == 0 || (vec_mem != 0 && vec_mem != 1))
     return BF_ERR_ARG;
   BF_GUARD_BEGIN
   c->stream = (cudaStream_t)stream;
-  size_t bytes = sizeof(double) * (size_t)c->n;
+  size_t bytes = sizeof(double) * (size_t)c->h[which].lv[0].A.n;
   const double *bd = b;
   double *xd = x;
   if (!vec_mem) {
@@ -511,7 +520,7 @@ bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int3
 }
 
 bf_status bf_num_levels(bf_handle c, int32_t which, int32_t *nlev) {
-  if (!c || !nlev || which < 0 || which > 2) return BF_ERR_ARG;
+  if (!c || !nlev || which < 0 || which > 3) return BF_ERR_ARG;
   *nlev = c->h[which].nlev;
   return BF_OK;
 }
@@ -525,7 +534,7 @@ static void copy_csr_out(bf_ctx *c, const DCsr &A, int32_t *rp, int32_t *ci, dou
 bf_status bf_get_level(bf_handle c, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
                        int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val, int8_t *cf,
                        int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1) {
-  if (!c || which < 0 || which > 2 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
+  if (!c || which < 0 || which > 3 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
   BF_GUARD_BEGIN
   const Level &L = c->h[which].lv[level];
   bool coarsest = level == c->h[which].nlev - 1;

@@ -91,7 +91,8 @@ struct bf_ctx {
   int32_t jdia_k = 0, jdia_off[8] = {0};
   bf::DCsr blk[5];       // A_pp, A_ps, A_sp, A_ss, S~
   double *dss = nullptr;
-  bf::Hier h[3];         // AMG hierarchies: 0 A_ss, 1 S~ (BF), 2 A_pp (CPR)
+  bf::Hier h[4];         // AMG hierarchies: 0 A_ss, 1 S~ (BF), 2 A_pp (CPR), 3 J as a scalar matrix (coupled AMG)
+  bf::DCsr jsc;          // J as a point-ordered scalar CSR (precond 3)
   // CPR-AMG(1)/(2) block ILU(0) of J (k_ilu.cu)
   int32_t *ilu_perm = nullptr, *ilu_dpos = nullptr;  // level-sorted row schedule, diagonal block positions
   int32_t ilu_levels = 0;
@@ -198,6 +199,7 @@ void assemble(bf_ctx *c, const bf_twophase *P, const double *p, const double *sn
               double *vals, double *R);                                   // k_assemble.cu
 void newton_update(bf_ctx *c, int n, double *p, double *sn, const double *delta, double chop);
 void build_ilu(bf_ctx *c);                                              // k_ilu.cu
+void build_jscalar(bf_ctx *c, DCsr &A);                                 // k_ilu.cu
 void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2);
 double cpr_model_bytes(bf_ctx *c);
 bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles);

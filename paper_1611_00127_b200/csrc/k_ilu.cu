@@ -464,7 +464,13 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
 void vcycle_from_invariant(bf_ctx *c, int which);  // k_vcycle.cu
 double x0_beta_of(const bf_options &o);             // k_vcycle.cu
 
+void amg_apply(bf_ctx *c, const double *v, double *z, const double *nrm2);
+
 void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
+  if (c->opt.precond == 3) {
+    amg_apply(c, v, z, nrm2);
+    return;
+  }
   int n = c->n;
   Hier &hp = c->h[2], &hs = c->h[0];
   bool additive = c->opt.precond == 2;
@@ -503,7 +509,10 @@ void ilu_solve_into(bf_ctx *c, const double *r, double *x) {
 }
 
 // graph patching (k_vcycle.cu bf_apply_graph): which kernel arguments carry v, nrm2 and z
+bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles);
+
 bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
+  if (amg_patch_roles(func, nargs, roles)) return true;
   if (func == (const void *)k_ilu_fwd) {
     nargs = 11;
     roles = {{6, 0}, {7, 1}};
@@ -525,6 +534,13 @@ bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
 // (SURVEY 8(d) per-level model), the merge (u, dp[, ds], z)
 double cpr_model_bytes(bf_ctx *c) {
   double n = c->n, nnzb = (double)c->nnzb;
+  if (c->opt.precond == 3) {  // split 48 n (v in, b and x0 out, 1/dl1 in -- 2n each) + merge 32 n + V-cycle
+    Hier &h = c->h[3];
+    double bytes = 96.0 * n;
+    for (int l = 0; l + 1 < h.nlev; l++)
+      bytes += 24.0 * h.lv[l].A.nnz + 24.0 * h.lv[l].P.nnz + 116.0 * h.lv[l].A.n + 12.0 * h.lv[l + 1].A.n;
+    return bytes + 8.0 * h.nL * h.nL;
+  }
   bool additive = c->opt.precond == 2;
   double bytes = 36.0 * nnzb + 108.0 * n;
   bytes += 36.0 * nnzb + 36.0 * n + (additive ? 48.0 : 24.0) * n;
@@ -537,6 +553,104 @@ double cpr_model_bytes(bf_ctx *c) {
     bytes += 8.0 * h.nL * h.nL;
   }
   return bytes;
+}
+
+
+// ======================================================================================
+// Coupled "point" AMG (precond 3; the paper's AMG comparison, reading R20):
+// one V-cycle of the scalar AMG on J itself, interleaved (point-ordered) as a 2n x 2n CSR.
+// ======================================================================================
+// scalar row 2c+r of J: entries (r, s) of the row's blocks that are not +-0.0, plus the diagonal
+__global__ void k_jsc_count(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            const double *__restrict__ bv, int32_t *cnt) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= 2 * n) return;
+  int c = row >> 1, r = row & 1, k = 0;
+  for (int q = rp[c]; q < rp[c + 1]; q++)
+    for (int s = 0; s < 2; s++) k += (bv[4 * (size_t)q + 2 * r + s] != 0.0 || (ci[q] == c && r == s)) ? 1 : 0;
+  cnt[row] = k;
+}
+__global__ void k_jsc_fill(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                           const double *__restrict__ bv, const int32_t *__restrict__ orp, int32_t *oci,
+                           double *ov) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= 2 * n) return;
+  int c = row >> 1, r = row & 1, k = orp[row];
+  for (int q = rp[c]; q < rp[c + 1]; q++)
+    for (int s = 0; s < 2; s++) {
+      double a = bv[4 * (size_t)q + 2 * r + s];
+      if (a != 0.0 || (ci[q] == c && r == s)) {
+        oci[k] = 2 * ci[q] + s;
+        ov[k] = a;
+        k++;
+      }
+    }
+}
+
+void build_jscalar(bf_ctx *c, DCsr &A) {
+  int n2 = 2 * c->n;
+  int32_t *cnt = dalloc_t<int32_t>(c, n2);
+  k_jsc_count<<<div_up(n2, 256), 256, 0, c->stream>>>(c->n, c->brp, c->bci, c->bv, cnt);
+  BF_LAUNCH(c);
+  A.n = A.m = n2;
+  A.rp = dalloc_t<int32_t>(c, (size_t)n2 + 1);
+  A.nnz = exclusive_scan_i32(c, cnt, A.rp, n2);
+  A.ci = dalloc_t<int32_t>(c, A.nnz);
+  A.v = dalloc_t<double>(c, A.nnz);
+  k_jsc_fill<<<div_up(n2, 256), 256, 0, c->stream>>>(c->n, c->brp, c->bci, c->bv, A.rp, A.ci, A.v);
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+  dfree(c, cnt);
+}
+
+// v (caller order, normalised in place when nrm2) -> b = canonical v, x0 = beta b ./ dl1
+__global__ void k_jsc_split(int n, int ip, double2 *v, const double *nrm2, double2 *__restrict__ b,
+                            const double2 *__restrict__ dinv, double beta, double2 *__restrict__ x0) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 a = v[i];
+  if (nrm2) {
+    double sc = 1.0 / sqrt(*nrm2);
+    a.x = a.x * sc;
+    a.y = a.y * sc;
+    v[i] = a;
+  }
+  double2 cv = ip ? make_double2(a.y, a.x) : a;
+  b[i] = cv;
+  double2 d = dinv[i];
+  x0[i] = make_double2(beta * (cv.x * d.x), beta * (cv.y * d.y));
+}
+__global__ void k_jsc_merge(int n, int ip, const double2 *__restrict__ x, double2 *__restrict__ z) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[i] = ip ? make_double2(x[i].y, x[i].x) : x[i];
+}
+
+void amg_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
+  int n = c->n;
+  Level &L = c->h[3].lv[0];
+  k_jsc_split<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->var_order, reinterpret_cast<double2 *>(const_cast<double *>(v)),
+                                                      nrm2, reinterpret_cast<double2 *>(L.b),
+                                                      reinterpret_cast<const double2 *>(L.d), x0_beta_of(c->opt),
+                                                      reinterpret_cast<double2 *>(L.x));
+  BF_LAUNCH(c);
+  vcycle_from_invariant(c, 3);
+  k_jsc_merge<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->var_order, reinterpret_cast<const double2 *>(c->h[3].lv[0].x),
+                                                      reinterpret_cast<double2 *>(z));
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
+}
+
+bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
+  if (func == (const void *)k_jsc_split) {
+    nargs = 8;
+    roles = {{2, 0}, {3, 1}};
+  } else if (func == (const void *)k_jsc_merge) {
+    nargs = 4;
+    roles = {{3, 2}};
+  } else {
+    return false;
+  }
+  return true;
 }
 
 }  // namespace bf

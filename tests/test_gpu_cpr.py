@@ -151,3 +151,35 @@ def test_cpr_non_grid_pattern():
     r = g.solve(rhs, x, tol=1e-8)
     assert abs(r["iters"] - ro["iters"]) <= 1
     assert np.linalg.norm(x - ro["x"]) <= 1e-6 * np.linalg.norm(ro["x"])
+
+
+@pytest.mark.parametrize("config,dims", [(1, None), (2, (12, 11, 9)), (4, (20, 9, 8))])
+def test_coupled_amg(config, dims):
+    """precond 3 (coupled point AMG, R20): hierarchy of the scalar J bit-exact, one
+    apply <= 1e-10, 40 forced GMRES iterations <= 1e-6 per field, same convergence verdict."""
+    prob, J, rhs = make_system(config, dims=dims)
+    g = gpu_solver(J, prob.dims, precond=3)
+    o = oracle.BF(J, precond=3)
+    assert g.num_levels(3) == o.nlev(3) > 1
+    for l in range(o.nlev(3)):
+        G, O = g.level(3, l), o.level(3, l)
+        pat, val = csr_equal(G["A"], O["A"])
+        assert pat and val, l
+        if l < o.nlev(3) - 1:
+            assert np.array_equal(G["cf"], O["cf"]), l
+            pat, val = csr_equal(G["P"], O["P"])
+            assert pat and val, l
+    N = 2 * J.n
+    v = seeded_vector(N, 9)
+    zo = o.apply(v)
+    z = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(v), z)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+    ro = o.gmres(rhs, tol=0.0, restart=30, maxit=40)
+    x = torch.zeros(N, dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=0.0, restart=30, maxit=40)
+    assert r["iters"] == ro["iters"] == 40
+    x = x.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+    assert abs(r["relres"] - ro["relres"]) <= 1e-6 * ro["relres"]
