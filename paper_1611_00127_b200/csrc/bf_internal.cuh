@@ -100,6 +100,7 @@ struct bf_ctx {
   int *ilu_flag = nullptr;                           // per-row completion flags of the sync-free sweeps
   unsigned *ilu_sync = nullptr;                      // tickets / epoch of the sweeps
   double *ilu_y = nullptr, *ilu_u = nullptr;         // forward result, CPR first-stage solution (canonical)
+  bool ilu_vflag = true;                             // value-flag sweeps (default) or flag-array sweeps
   // solve workspace
   int32_t Vm = 0;
   double *Z = nullptr;  // preconditioned basis z_j = M^-1 v_j (restart x N)

@@ -321,6 +321,143 @@ __global__ void __launch_bounds__(256) k_ilu_bwd(int n, const int32_t *__restric
   sweep_exit(sy, 1);
 }
 
+// ---- value-flag variant of the sweeps (default) -------------------------------------------
+// The result itself is the completion flag: every entry of y and x holds a sentinel NaN bit
+// pattern (never produced by arithmetic) until its row publishes it, so a consumer's poll
+// returns the dependency's value -- no separate flag, no fence, one L2 round trip per level on
+// the critical path instead of three.  The consumers that read a row's result for the last
+// time restore the sentinel: the backward sweep for y (its own row), the CPR merge /
+// k_to_caller for x.  A computed value equal to the sentinel is replaced by the canonical NaN.
+constexpr unsigned long long SENT = 0x7FF4DEADBEEF0001ull;
+__device__ __forceinline__ double2 ld_poll(const double2 *p) {
+  double a, b;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p) : "memory");
+  return make_double2(a, b);
+}
+__device__ __forceinline__ void st_pub(double2 *p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ bool is_sent(double v) { return (unsigned long long)__double_as_longlong(v) == SENT; }
+__device__ __forceinline__ bool ready2(double2 v) { return !is_sent(v.x) && !is_sent(v.y); }
+__device__ __forceinline__ double unsent(double v) {
+  return is_sent(v) ? __longlong_as_double(0x7FFFFFFFFFFFFFFFll) : v;
+}
+__device__ __forceinline__ double2 sent2() {
+  return make_double2(__longlong_as_double((long long)SENT), __longlong_as_double((long long)SENT));
+}
+
+// poll every dependency once; on success vals[] holds the first PF dependencies' results
+__device__ __forceinline__ bool vdeps_ready(const DepCache &dc, int lo, int hi, const int32_t *__restrict__ ci,
+                                            const double2 *v, double2 *vals) {
+  bool ready = true;
+#pragma unroll
+  for (int e = 0; e < PF; e++)
+    if (lo + e < hi) {
+      vals[e] = ld_poll(v + dc.col[e]);
+      ready = ready && ready2(vals[e]);
+    }
+  for (int q = lo + PF; q < hi && ready; q++) ready = ready2(ld_poll(v + __ldg(ci + q)));
+  return ready;
+}
+__device__ __forceinline__ void vdep_subtract(const DepCache &dc, int lo, int hi, const int32_t *__restrict__ ci,
+                                              const double *__restrict__ lu, const double2 *v, const double2 *vals,
+                                              double &t0, double &t1) {
+#pragma unroll
+  for (int e = 0; e < PF; e++) {
+    if (lo + e < hi) {
+      double2 vk = vals[e];
+      t0 = t0 - (dc.b01[e].x * vk.x + dc.b01[e].y * vk.y);
+      t1 = t1 - (dc.b23[e].x * vk.x + dc.b23[e].y * vk.y);
+    }
+  }
+  for (int q = lo + PF; q < hi; q++) {
+    double2 b01 = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q);
+    double2 b23 = __ldg(reinterpret_cast<const double2 *>(lu) + 2 * (size_t)q + 1);
+    double2 vk = ld_poll(v + __ldg(ci + q));
+    t0 = t0 - (b01.x * vk.x + b01.y * vk.y);
+    t1 = t1 - (b23.x * vk.x + b23.y * vk.y);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ilu_fwd_v(int n, const int32_t *__restrict__ perm,
+                                                   const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                   const int32_t *__restrict__ dpos, const double *__restrict__ lu,
+                                                   double2 *r, const double *nrm2, double2 *y, int *unused,
+                                                   IluSync *sy, int ip) {
+  const double sc = nrm2 ? 1.0 / sqrt(*nrm2) : 1.0;
+  for (;;) {
+    unsigned base = warp_ticket(&sy->ticket[0]);
+    if (base >= (unsigned)n) break;
+    unsigned t = base + (threadIdx.x & 31);
+    bool done = t >= (unsigned)n;
+    int i = done ? 0 : __ldg(perm + t);
+    int lo = done ? 0 : __ldg(rp + i), di = done ? 0 : __ldg(dpos + i);
+    DepCache dc;
+    dep_prefetch(dc, lo, di, ci, lu);
+    double y0 = 0.0, y1 = 0.0;
+    if (!done) {
+      double2 a = r[i];
+      if (nrm2) {
+        a.x = a.x * sc;
+        a.y = a.y * sc;
+        r[i] = a;
+      }
+      y0 = ip ? a.y : a.x;
+      y1 = ip ? a.x : a.y;
+    }
+    while (!__all_sync(FULL, done)) {
+      double2 vals[PF];
+      if (!done && vdeps_ready(dc, lo, di, ci, y, vals)) {
+        vdep_subtract(dc, lo, di, ci, lu, y, vals, y0, y1);
+        st_pub(y + i, make_double2(unsent(y0), unsent(y1)));
+        done = true;
+      }
+    }
+  }
+  sweep_exit(sy, 0);
+}
+
+__global__ void __launch_bounds__(256) k_ilu_bwd_v(int n, const int32_t *__restrict__ perm,
+                                                   const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                   const int32_t *__restrict__ dpos, const double *__restrict__ lu,
+                                                   const double *__restrict__ dinv, double2 *y, double2 *x,
+                                                   int *unused, IluSync *sy) {
+  for (;;) {
+    unsigned base = warp_ticket(&sy->ticket[1]);
+    if (base >= (unsigned)n) break;
+    unsigned t = base + (threadIdx.x & 31);
+    bool done = t >= (unsigned)n;
+    int i = done ? 0 : __ldg(perm + (n - 1 - (int)t));
+    int lo = done ? 0 : __ldg(dpos + i) + 1, hi = done ? 0 : __ldg(rp + i + 1);
+    DepCache dc;
+    dep_prefetch(dc, lo, hi, ci, lu);
+    double t0 = 0.0, t1 = 0.0;
+    double2 d01 = make_double2(0.0, 0.0), d23 = d01;
+    if (!done) {
+      double2 yi = __ldcg(y + i);
+      y[i] = sent2();  // last read of y_i: restore the sentinel for the next forward sweep
+      t0 = yi.x;
+      t1 = yi.y;
+      d01 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i);
+      d23 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i + 1);
+    }
+    while (!__all_sync(FULL, done)) {
+      double2 vals[PF];
+      if (!done && vdeps_ready(dc, lo, hi, ci, x, vals)) {
+        vdep_subtract(dc, lo, hi, ci, lu, x, vals, t0, t1);
+        st_pub(x + i, make_double2(unsent(d01.x * t0 + d01.y * t1), unsent(d23.x * t0 + d23.y * t1)));
+        done = true;
+      }
+    }
+  }
+  sweep_exit(sy, 1);
+}
+
+__global__ void k_fill_sent(size_t n2, double2 *a) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i < n2) a[i] = sent2();
+}
+
 // ---- CPR: t = r - J u, split into the right-hand sides of the inner V-cycles --------------
 // (Alg. 1/2 steps 3-4[-5]); writes the level invariant of vcycle_level: b and x0 = beta b ./ dl1.
 // J from its DIA copy when present (coalesced), else the CSR-BSR rows.
@@ -370,11 +507,12 @@ __global__ void __launch_bounds__(256) k_cpr_resid(int n, const int32_t *__restr
 }
 
 // z = u + R_p^T dp [+ R_s^T ds] in the caller's var_order (Alg. 1 step 5 / Alg. 2 step 6)
-__global__ void k_cpr_merge(int n, const double2 *__restrict__ u, const double *__restrict__ dp,
+__global__ void k_cpr_merge(int n, double2 *__restrict__ u, const double *__restrict__ dp,
                             const double *__restrict__ ds, double2 *__restrict__ z, int ip) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 a = u[i];
+  u[i] = sent2();  // last read of u_i (value-flag sweeps)
   double p = a.x + dp[i], s = ds ? a.y + ds[i] : a.y;
   z[i] = ip ? make_double2(s, p) : make_double2(p, s);
 }
@@ -419,6 +557,10 @@ void build_ilu(bf_ctx *c) {
     c->ilu_dinv = dalloc_t<double>(c, 4 * (size_t)n);
     c->ilu_y = dalloc_t<double>(c, 2 * (size_t)n);
     c->ilu_u = dalloc_t<double>(c, 2 * (size_t)n);
+    c->ilu_vflag = getenv("BF_ILU_FLAGS") == nullptr;
+    k_fill_sent<<<div_up(n, 256), 256, 0, c->stream>>>((size_t)n, reinterpret_cast<double2 *>(c->ilu_y));
+    k_fill_sent<<<div_up(n, 256), 256, 0, c->stream>>>((size_t)n, reinterpret_cast<double2 *>(c->ilu_u));
+    c->launches += 2;
   }
   // numeric factorization (oracle or_ilu0 order)
   int *flag = dalloc_t<int>(c, n);
@@ -450,13 +592,18 @@ void build_ilu(bf_ctx *c) {
 static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
   int n = c->n;
   IluSync *sy = reinterpret_cast<IluSync *>(c->ilu_sync);
-  k_ilu_fwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
-                                                reinterpret_cast<double2 *>(r), nrm2,
-                                                reinterpret_cast<double2 *>(c->ilu_y), c->ilu_flag, sy,
-                                                c->var_order);
-  k_ilu_bwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
-                                                c->ilu_dinv, reinterpret_cast<const double2 *>(c->ilu_y),
-                                                reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
+  auto fwd = c->ilu_vflag ? k_ilu_fwd_v : k_ilu_fwd;
+  fwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                          reinterpret_cast<double2 *>(r), nrm2, reinterpret_cast<double2 *>(c->ilu_y),
+                                          c->ilu_flag, sy, c->var_order);
+  if (c->ilu_vflag)
+    k_ilu_bwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                    c->ilu_dinv, reinterpret_cast<double2 *>(c->ilu_y),
+                                                    reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
+  else
+    k_ilu_bwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                  c->ilu_dinv, reinterpret_cast<const double2 *>(c->ilu_y),
+                                                  reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
   c->launches += 2;
   BF_CUDA(cudaGetLastError());
 }
@@ -486,23 +633,26 @@ void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   BF_LAUNCH(c);
   vcycle_from_invariant(c, 2);  // step 4
   if (additive) vcycle_from_invariant(c, 0);  // Alg. 2 step 5
-  k_cpr_merge<<<div_up(n, 256), 256, 0, c->stream>>>(n, reinterpret_cast<const double2 *>(c->ilu_u), hp.lv[0].x,
+  k_cpr_merge<<<div_up(n, 256), 256, 0, c->stream>>>(n, reinterpret_cast<double2 *>(c->ilu_u), hp.lv[0].x,
                                                      additive ? hs.lv[0].x : nullptr,
                                                      reinterpret_cast<double2 *>(z), c->var_order);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
 }
 
-__global__ void k_to_caller(int n, const double2 *__restrict__ u, double2 *__restrict__ x, int ip) {
+__global__ void k_to_caller(int n, double2 *__restrict__ u, double2 *__restrict__ x, int ip) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = ip ? make_double2(u[i].y, u[i].x) : u[i];
+  if (i >= n) return;
+  double2 a = u[i];
+  u[i] = sent2();  // last read of u_i (value-flag sweeps)
+  x[i] = ip ? make_double2(a.y, a.x) : a;
 }
 
 // introspection (bf_ilu_solve): x = (L U)^-1 r, both in the caller's var_order
 void ilu_solve_into(bf_ctx *c, const double *r, double *x) {
   if (!c->ilu_lu) throw Error(BF_ERR_ARG, "bf_ilu_solve: the handle has no ILU(0) (precond 0)");
   ilu_solve(c, const_cast<double *>(r), nullptr);
-  k_to_caller<<<div_up(c->n, 256), 256, 0, c->stream>>>(c->n, reinterpret_cast<const double2 *>(c->ilu_u),
+  k_to_caller<<<div_up(c->n, 256), 256, 0, c->stream>>>(c->n, reinterpret_cast<double2 *>(c->ilu_u),
                                                          reinterpret_cast<double2 *>(x), c->var_order);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
@@ -513,7 +663,7 @@ bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
 
 bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
   if (amg_patch_roles(func, nargs, roles)) return true;
-  if (func == (const void *)k_ilu_fwd) {
+  if (func == (const void *)k_ilu_fwd || func == (const void *)k_ilu_fwd_v) {
     nargs = 11;
     roles = {{6, 0}, {7, 1}};
   } else if (func == (const void *)k_cpr_resid) {

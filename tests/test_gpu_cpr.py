@@ -183,3 +183,26 @@ def test_coupled_amg(config, dims):
     for f in (0, 1):
         assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
     assert abs(r["relres"] - ro["relres"]) <= 1e-6 * ro["relres"]
+
+
+def test_sweep_variants_bit_identical(monkeypatch):
+    """The flag-array sweeps (BF_ILU_FLAGS=1) and the default value-flag sweeps compute every
+    row in the same order: bit-identical ILU solves, repeated (sentinels restored each time)."""
+    prob, J, rhs = make_system(2, dims=(17, 13, 11))
+    g_v = gpu_solver(J, prob.dims, precond=2)
+    monkeypatch.setenv("BF_ILU_FLAGS", "1")
+    g_f = gpu_solver(J, prob.dims, precond=2)
+    N = 2 * J.n
+    for seed in (1, 2, 3):
+        r = torch_dev(seeded_vector(N, seed))
+        a = torch.empty(N, dtype=torch.float64, device="cuda")
+        b = torch.empty(N, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            g_v.ilu_solve(r, a)
+            g_f.ilu_solve(r, b)
+            assert torch.equal(a, b)
+        za = torch.empty(N, dtype=torch.float64, device="cuda")
+        zb = torch.empty(N, dtype=torch.float64, device="cuda")
+        g_v.apply_precond(r, za)
+        g_f.apply_precond(r, zb)
+        assert torch.equal(za, zb)
