@@ -208,6 +208,12 @@ void ilu_solve_into(bf_ctx *c, const double *r, double *x);              // x = 
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
 
+// number of parameters of a kernel (graph-node argument patching, k_vcycle.cu)
+template <typename... A>
+constexpr int nargs_of(void (*)(A...)) {
+  return (int)sizeof...(A);
+}
+
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // programmatic dependent launch (PDL): the kernel may begin while its stream predecessor is

@@ -664,13 +664,13 @@ bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
 bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
   if (amg_patch_roles(func, nargs, roles)) return true;
   if (func == (const void *)k_ilu_fwd || func == (const void *)k_ilu_fwd_v) {
-    nargs = 11;
+    nargs = nargs_of(k_ilu_fwd);
     roles = {{6, 0}, {7, 1}};
   } else if (func == (const void *)k_cpr_resid) {
-    nargs = 16;
+    nargs = nargs_of(k_cpr_resid);
     roles = {{7, 0}};
   } else if (func == (const void *)k_cpr_merge) {
-    nargs = 6;
+    nargs = nargs_of(k_cpr_merge);
     roles = {{4, 2}};
   } else {
     return false;
@@ -792,10 +792,10 @@ void amg_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
 
 bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
   if (func == (const void *)k_jsc_split) {
-    nargs = 8;
+    nargs = nargs_of(k_jsc_split);
     roles = {{2, 0}, {3, 1}};
   } else if (func == (const void *)k_jsc_merge) {
-    nargs = 4;
+    nargs = nargs_of(k_jsc_merge);
     roles = {{3, 2}};
   } else {
     return false;

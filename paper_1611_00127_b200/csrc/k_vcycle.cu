@@ -792,10 +792,10 @@ void drop_apply_graph(bf_ctx *c) {
 // are the ILU forward sweep, the residual kernel (v) and the merge kernel (z).
 static bool patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
   if (func == (const void *)k_split_vec) {
-    nargs = 9;
+    nargs = nargs_of(k_split_vec);
     roles = {{2, 0}, {8, 1}};
   } else if (func == (const void *)k_merge_vec) {
-    nargs = 5;
+    nargs = nargs_of(k_merge_vec);
     roles = {{4, 2}};
   } else {
     return cpr_patch_roles(func, nargs, roles);
