@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256) k_ilu_fwd_v(int n, const int32_t *__restr
                                                    const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                    const int32_t *__restrict__ dpos, const double *__restrict__ lu,
                                                    double2 *r, const double *nrm2, double2 *y, int *unused,
-                                                   IluSync *sy, int ip) {
+                                                   IluSync *sy, int ip, unsigned backoff) {
   const double sc = nrm2 ? 1.0 / sqrt(*nrm2) : 1.0;
   for (;;) {
     unsigned base = warp_ticket(&sy->ticket[0]);
@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(256) k_ilu_fwd_v(int n, const int32_t *__restr
     }
     while (!__all_sync(FULL, done)) {
       double2 vals[PF];
-      if (!done && vdeps_ready(dc, lo, di, ci, y, vals)) {
+      bool ok = !done && vdeps_ready(dc, lo, di, ci, y, vals);
+      if (!done && !ok && backoff) __nanosleep(backoff);
+      if (ok) {
         vdep_subtract(dc, lo, di, ci, lu, y, vals, y0, y1);
         st_pub(y + i, make_double2(unsent(y0), unsent(y1)));
         done = true;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(256) k_ilu_bwd_v(int n, const int32_t *__restr
                                                    const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                    const int32_t *__restrict__ dpos, const double *__restrict__ lu,
                                                    const double *__restrict__ dinv, double2 *y, double2 *x,
-                                                   int *unused, IluSync *sy) {
+                                                   int *unused, IluSync *sy, unsigned backoff) {
   for (;;) {
     unsigned base = warp_ticket(&sy->ticket[1]);
     if (base >= (unsigned)n) break;
@@ -443,7 +445,9 @@ __global__ void __launch_bounds__(256) k_ilu_bwd_v(int n, const int32_t *__restr
     }
     while (!__all_sync(FULL, done)) {
       double2 vals[PF];
-      if (!done && vdeps_ready(dc, lo, hi, ci, x, vals)) {
+      bool ok = !done && vdeps_ready(dc, lo, hi, ci, x, vals);
+      if (!done && !ok && backoff) __nanosleep(backoff);
+      if (ok) {
         vdep_subtract(dc, lo, hi, ci, lu, x, vals, t0, t1);
         st_pub(x + i, make_double2(unsent(d01.x * t0 + d01.y * t1), unsent(d23.x * t0 + d23.y * t1)));
         done = true;
@@ -518,7 +522,11 @@ __global__ void k_cpr_merge(int n, double2 *__restrict__ u, const double *__rest
 }
 
 // ---- host side -------------------------------------------------------------------------
-static int ilu_grid(bf_ctx *c) { return c->num_sms * 4; }  // 4 CTAs of 256 threads per SM
+// CTAs of 256 threads per SM for the persistent sweeps (BF_ILU_CTAS overrides, experiments)
+static int ilu_grid(bf_ctx *c) {
+  static const int per_sm = getenv("BF_ILU_CTAS") ? atoi(getenv("BF_ILU_CTAS")) : 4;
+  return c->num_sms * (per_sm > 0 ? per_sm : 4);
+}
 
 void build_ilu(bf_ctx *c) {
   int n = c->n;
@@ -592,18 +600,24 @@ void build_ilu(bf_ctx *c) {
 static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
   int n = c->n;
   IluSync *sy = reinterpret_cast<IluSync *>(c->ilu_sync);
-  auto fwd = c->ilu_vflag ? k_ilu_fwd_v : k_ilu_fwd;
-  fwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
-                                          reinterpret_cast<double2 *>(r), nrm2, reinterpret_cast<double2 *>(c->ilu_y),
-                                          c->ilu_flag, sy, c->var_order);
-  if (c->ilu_vflag)
+  static const unsigned backoff = getenv("BF_ILU_SLEEP") ? (unsigned)atoi(getenv("BF_ILU_SLEEP")) : 0u;
+  if (c->ilu_vflag) {
+    k_ilu_fwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                    reinterpret_cast<double2 *>(r), nrm2,
+                                                    reinterpret_cast<double2 *>(c->ilu_y), c->ilu_flag, sy,
+                                                    c->var_order, backoff);
     k_ilu_bwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
                                                     c->ilu_dinv, reinterpret_cast<double2 *>(c->ilu_y),
-                                                    reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
-  else
+                                                    reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy, backoff);
+  } else {
+    k_ilu_fwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
+                                                  reinterpret_cast<double2 *>(r), nrm2,
+                                                  reinterpret_cast<double2 *>(c->ilu_y), c->ilu_flag, sy,
+                                                  c->var_order);
     k_ilu_bwd<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
                                                   c->ilu_dinv, reinterpret_cast<const double2 *>(c->ilu_y),
                                                   reinterpret_cast<double2 *>(c->ilu_u), c->ilu_flag, sy);
+  }
   c->launches += 2;
   BF_CUDA(cudaGetLastError());
 }
@@ -663,8 +677,11 @@ bool amg_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
 
 bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, int>> &roles) {
   if (amg_patch_roles(func, nargs, roles)) return true;
-  if (func == (const void *)k_ilu_fwd || func == (const void *)k_ilu_fwd_v) {
+  if (func == (const void *)k_ilu_fwd) {
     nargs = nargs_of(k_ilu_fwd);
+    roles = {{6, 0}, {7, 1}};
+  } else if (func == (const void *)k_ilu_fwd_v) {
+    nargs = nargs_of(k_ilu_fwd_v);
     roles = {{6, 0}, {7, 1}};
   } else if (func == (const void *)k_cpr_resid) {
     nargs = nargs_of(k_cpr_resid);

@@ -120,7 +120,7 @@ def test_cpr_var_order_host_pointers_update_and_errors():
     with pytest.raises(BFError, match="BF_ERR_ZERO_DIAG.*ILU.*cell 5"):
         gpu_solver(Jb, prob.dims, precond=1)
     with pytest.raises(BFError, match="BF_ERR_ARG.*precond"):
-        gpu_solver(J, prob.dims, precond=3)
+        gpu_solver(J, prob.dims, precond=4)
     # a BF handle has no ILU
     gb = gpu_solver(J, prob.dims)
     with pytest.raises(BFError):
