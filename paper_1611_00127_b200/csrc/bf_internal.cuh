@@ -101,6 +101,10 @@ struct bf_ctx {
   unsigned *ilu_sync = nullptr;                      // tickets / epoch of the sweeps
   double *ilu_y = nullptr, *ilu_u = nullptr;         // forward result, CPR first-stage solution (canonical)
   bool ilu_vflag = true;                             // value-flag sweeps (default) or flag-array sweeps
+  bool ilu_pencil = false, ilu_pencil_checked = false;  // pencil-wavefront sweeps (grid-structured J)
+  double *ilu_ld = nullptr, *ilu_ud = nullptr;       // DIA copies of L (k-1, j-1, i-1) and U (i+1, j+1, k+1)
+  int2 *ilu_order = nullptr;                         // tile order (anti-diagonals)
+  int ilu_geom[7] = {0};                             // nx, ny, nz, TJ, TK, NJ, NK
   // solve workspace
   int32_t Vm = 0;
   double *Z = nullptr;  // preconditioned basis z_j = M^-1 v_j (restart x N)

@@ -24,6 +24,8 @@
 //
 // Roofline: the solves are HBM/latency bound (each moves J's blocks once: 36 B/block plus
 // vectors) but their critical path is the number of levels times one L2 round trip.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "bf_internal.cuh"
@@ -462,6 +464,211 @@ __global__ void k_fill_sent(size_t n2, double2 *a) {
   if (i < n2) a[i] = sent2();
 }
 
+// ---- pencil-wavefront sweeps for grid-structured J (default when the pattern is exactly the
+// 5/7-point stencil of the nx x ny x nz grid in natural order) ----------------------------
+// Row c = i + nx (j + ny k) depends on (i-1), (j-1), (k-1) in the forward sweep.  A CTA owns a
+// tile of TJ x TK x-lines (j, k) and walks them as a local wavefront: at CTA step s, thread
+// (jj, kk) computes cell i = s - jj - kk of its line, so its (j-1) and (k-1) dependencies are the
+// neighbouring threads' results of step s-1 (shared memory) and its (i-1) dependency is its own
+// previous result (register): one __syncthreads per step instead of one L2 round trip per
+// dependency level.  Dependencies across tile faces are read from global memory with the
+// value-flag protocol above (sentinel until published), prefetched one step ahead; tiles are
+// taken from an atomic ticket in anti-diagonal order, so a CTA waits only on tiles already
+// taken by resident CTAs (deadlock-free).  The backward sweep is the same walk mirrored
+// (i, j, k -> n-1-i, ...) with the U blocks and the pivot inverse.  Factor blocks are read from a
+// DIA copy (ld[d][c], ud[d][c]) so a thread's consecutive cells are consecutive in memory.
+// Arithmetic order per row = ascending columns, as the oracle: forward (k-1), (j-1), (i-1);
+// backward (i+1), (j+1), (k+1); results are bit-identical to the generic sweeps.
+struct PencilGeom {
+  int nx, ny, nz, TJ, TK, NJ, NK;
+};
+
+__global__ void k_grid_check(int n, int nx, int ny, int nz, const int32_t *__restrict__ rp,
+                             const int32_t *__restrict__ ci, int *bad) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+  int want[7], m = 0;
+  long sxy = (long)nx * ny;
+  if (k > 0) want[m++] = c - (int)sxy;
+  if (j > 0) want[m++] = c - nx;
+  if (i > 0) want[m++] = c - 1;
+  want[m++] = c;
+  if (i < nx - 1) want[m++] = c + 1;
+  if (j < ny - 1) want[m++] = c + nx;
+  if (k < nz - 1) want[m++] = c + (int)sxy;
+  int q0 = rp[c];
+  bool ok = rp[c + 1] - q0 == m;
+  for (int e = 0; ok && e < m; e++) ok = ci[q0 + e] == want[e];
+  if (!ok) atomicExch(bad, 1);
+}
+
+// lu (CSR blocks) -> ld[3][n] (k-1, j-1, i-1) and ud[3][n] (i+1, j+1, k+1), zero where absent
+__global__ void k_ilu_to_dia(int n, int nx, int ny, int nz, const int32_t *__restrict__ rp,
+                             const double2 *__restrict__ lu, double2 *ld, double2 *ud) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+  bool has[7] = {k > 0, j > 0, i > 0, true, i < nx - 1, j < ny - 1, k < nz - 1};
+  int q = rp[c];
+  for (int e = 0; e < 7; e++) {
+    double2 a = make_double2(0.0, 0.0), b = a;
+    if (has[e]) {
+      a = lu[2 * (size_t)q];
+      b = lu[2 * (size_t)q + 1];
+      q++;
+    }
+    if (e == 3) continue;
+    double2 *dst = e < 3 ? ld + 2 * ((size_t)e * n + c) : ud + 2 * ((size_t)(e - 4) * n + c);
+    dst[0] = a;
+    dst[1] = b;
+  }
+}
+
+// per-thread staging of one cell's inputs (cp.async, PD steps ahead): the input pair, three
+// factor blocks, the pivot inverse (backward only)
+constexpr int PD = 4;
+struct Stage {
+  double2 in;
+  double2 f[6];
+  double2 d[2];
+};
+__device__ __forceinline__ void cp16(void *smem, const void *gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 *__restrict__ fac,
+                                                    const double2 *__restrict__ dinv, double2 *in,
+                                                    const double *nrm2, double2 *out, double2 *yreset,
+                                                    const int2 *__restrict__ order, unsigned *ticket,
+                                                    unsigned *done, unsigned *other_ticket, int ip) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2 *sbuf = reinterpret_cast<double2 *>(smem_raw);                        // [2][TK][TJ]
+  Stage *ring = reinterpret_cast<Stage *>(smem_raw + 2 * 128 * sizeof(double2));  // [PD][128]
+  __shared__ unsigned s_tile;
+  const int n = g.nx * g.ny * g.nz;
+  const long sxy = (long)g.nx * g.ny;
+  const int jj = threadIdx.x % g.TJ, kk = threadIdx.x / g.TJ;
+  const bool thr = kk < g.TK;
+  const double sc = (!BWD && nrm2) ? 1.0 / sqrt(*nrm2) : 1.0;
+  const int ntiles = g.NJ * g.NK;
+  const int nsteps = g.nx + g.TJ + g.TK - 2;
+  const int dj = BWD ? g.nx : -g.nx;  // the (j-1) / (j+1) neighbour
+  const long dk = BWD ? sxy : -sxy;   // the (k-1) / (k+1) neighbour
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    unsigned t = s_tile;
+    if (t >= (unsigned)ntiles) break;
+    int2 JK = order[t];
+    // walk-frame coordinates (the backward sweep walks the mirrored grid)
+    const int jw = JK.x * g.TJ + jj, kw = JK.y * g.TK + kk;
+    const bool line = thr && jw < g.ny && kw < g.nz;
+    const int j = BWD ? g.ny - 1 - jw : jw, k = BWD ? g.nz - 1 - kw : kw;
+    const int base = g.nx * (j + g.ny * k);
+    auto cell_of = [&](int s) -> int {
+      int iw = s - jj - kk;
+      if (!line || iw < 0 || iw >= g.nx) return -1;
+      return base + (BWD ? g.nx - 1 - iw : iw);
+    };
+    auto issue = [&](int s) {  // stage step s's inputs into ring slot s % PD
+      int c = cell_of(s);
+      if (c >= 0) {
+        Stage &st = ring[(s % PD) * 128 + threadIdx.x];
+        cp16(&st.in, in + c);
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+          cp16(&st.f[2 * d], fac + 2 * ((size_t)d * n + c));
+          cp16(&st.f[2 * d + 1], fac + 2 * ((size_t)d * n + c) + 1);
+        }
+        if (BWD) {
+          cp16(&st.d[0], dinv + 2 * (size_t)c);
+          cp16(&st.d[1], dinv + 2 * (size_t)c + 1);
+        }
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < PD - 1; s++) issue(s);
+    double2 prev = make_double2(0.0, 0.0);
+    for (int s = 0; s < nsteps; s++) {
+      issue(s + PD - 1);
+      cp_wait<PD - 1>();
+      int c = cell_of(s);
+      double2 res = make_double2(0.0, 0.0);
+      if (c >= 0) {
+        const Stage &st = ring[(s % PD) * 128 + threadIdx.x];
+        const int iw = s - jj - kk;
+        double t0, t1;
+        double2 a = st.in;
+        if (!BWD) {
+          if (nrm2) {
+            a.x = a.x * sc;
+            a.y = a.y * sc;
+            in[c] = a;
+          }
+          t0 = ip ? a.y : a.x;
+          t1 = ip ? a.x : a.y;
+        } else {
+          yreset[c] = sent2();  // last read of y_c
+          t0 = a.x;
+          t1 = a.y;
+        }
+        double2 vk = make_double2(0.0, 0.0), vj = vk;
+        const bool hk = kw > 0, hj = jw > 0, hi = iw > 0;
+        if (hk) {
+          if (kk > 0) vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
+          else
+            do vk = ld_poll(out + (c + dk)); while (!ready2(vk));
+        }
+        if (hj) {
+          if (jj > 0) vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
+          else
+            do vj = ld_poll(out + (c + dj)); while (!ready2(vj));
+        }
+        auto sub = [&](int slot, double2 v) {
+          double2 b01 = st.f[2 * slot], b23 = st.f[2 * slot + 1];
+          t0 = t0 - (b01.x * v.x + b01.y * v.y);
+          t1 = t1 - (b23.x * v.x + b23.y * v.y);
+        };
+        if (!BWD) {  // ascending columns: (k-1), (j-1), (i-1)
+          if (hk) sub(0, vk);
+          if (hj) sub(1, vj);
+          if (hi) sub(2, prev);
+          res = make_double2(unsent(t0), unsent(t1));
+        } else {  // ascending columns: (i+1), (j+1), (k+1)
+          if (hi) sub(0, prev);
+          if (hj) sub(1, vj);
+          if (hk) sub(2, vk);
+          res = make_double2(unsent(st.d[0].x * t0 + st.d[0].y * t1), unsent(st.d[1].x * t0 + st.d[1].y * t1));
+        }
+        st_pub(out + c, res);
+        prev = res;
+      }
+      if (thr) sbuf[(s & 1) * 128 + kk * g.TJ + jj] = res;
+      __syncthreads();
+    }
+    cp_wait<0>();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0;
+      *other_ticket = 0;
+      __threadfence();
+    }
+  }
+}
+constexpr size_t kPencilSmem = 2 * 128 * sizeof(double2) + (size_t)PD * 128 * sizeof(Stage);
+
 // ---- CPR: t = r - J u, split into the right-hand sides of the inner V-cycles --------------
 // (Alg. 1/2 steps 3-4[-5]); writes the level invariant of vcycle_level: b and x0 = beta b ./ dl1.
 // J from its DIA copy when present (coalesced), else the CSR-BSR rows.
@@ -526,6 +733,57 @@ __global__ void k_cpr_merge(int n, double2 *__restrict__ u, const double *__rest
 static int ilu_grid(bf_ctx *c) {
   static const int per_sm = getenv("BF_ILU_CTAS") ? atoi(getenv("BF_ILU_CTAS")) : 4;
   return c->num_sms * (per_sm > 0 ? per_sm : 4);
+}
+
+// grid-structured J (exactly the 5/7-point stencil in natural order): DIA copies of the factors
+// and the tile geometry of the pencil-wavefront sweeps (BF_ILU_PENCIL=0 keeps the generic ones)
+static void setup_pencil(bf_ctx *c) {
+  int n = c->n;
+  if (!c->ilu_pencil_checked) {
+    c->ilu_pencil_checked = true;
+    const char *e = getenv("BF_ILU_PENCIL");
+    if ((e && atoi(e) == 0) || getenv("BF_ILU_FLAGS") || (int64_t)c->nx * c->ny * c->nz != n) return;
+    int *bad = dalloc_t<int>(c, 1);
+    BF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    k_grid_check<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->nx, c->ny, c->nz, c->brp, c->bci, bad);
+    BF_LAUNCH(c);
+    int hb = 0;
+    BF_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    dfree(c, bad);
+    if (hb) return;
+    PencilGeom g;
+    g.nx = c->nx;
+    g.ny = c->ny;
+    g.nz = c->nz;
+    g.TK = std::min(c->nz, 8);
+    g.TJ = std::min(c->ny, 128 / g.TK);
+    g.NJ = div_up(c->ny, g.TJ);
+    g.NK = div_up(c->nz, g.TK);
+    std::vector<int2> ord;
+    for (int d = 0; d <= g.NJ + g.NK - 2; d++)  // anti-diagonals: every tile after its (J-1) and (K-1) neighbours
+      for (int J = 0; J < g.NJ; J++) {
+        int K = d - J;
+        if (K >= 0 && K < g.NK) ord.push_back(make_int2(J, K));
+      }
+    c->ilu_order = dalloc_t<int2>(c, ord.size());
+    BF_CUDA(cudaMemcpyAsync(c->ilu_order, ord.data(), sizeof(int2) * ord.size(), cudaMemcpyHostToDevice, c->stream));
+    c->ilu_geom[0] = g.nx; c->ilu_geom[1] = g.ny; c->ilu_geom[2] = g.nz;
+    c->ilu_geom[3] = g.TJ; c->ilu_geom[4] = g.TK; c->ilu_geom[5] = g.NJ; c->ilu_geom[6] = g.NK;
+    c->ilu_ld = dalloc_t<double>(c, 12 * (size_t)n);
+    c->ilu_ud = dalloc_t<double>(c, 12 * (size_t)n);
+    BF_CUDA(cudaFuncSetAttribute(k_ilu_pencil<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPencilSmem));
+    BF_CUDA(cudaFuncSetAttribute(k_ilu_pencil<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPencilSmem));
+    c->ilu_pencil = true;
+    sync(c);
+  }
+  if (!c->ilu_pencil) return;
+  k_ilu_to_dia<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->nx, c->ny, c->nz, c->brp,
+                                                       reinterpret_cast<const double2 *>(c->ilu_lu),
+                                                       reinterpret_cast<double2 *>(c->ilu_ld),
+                                                       reinterpret_cast<double2 *>(c->ilu_ud));
+  BF_LAUNCH(c);
+  BF_CUDA(cudaGetLastError());
 }
 
 void build_ilu(bf_ctx *c) {
@@ -593,6 +851,7 @@ void build_ilu(bf_ctx *c) {
   dfree(c, bad);
   if (hb < n)
     throw Error(BF_ERR_ZERO_DIAG, "ILU(0) pivot block singular at cell " + std::to_string(hb));
+  setup_pencil(c);
 }
 
 // u = (L U)^-1 r (canonical output in c->ilu_u); r in the caller's order, normalised in place
@@ -601,7 +860,19 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
   int n = c->n;
   IluSync *sy = reinterpret_cast<IluSync *>(c->ilu_sync);
   static const unsigned backoff = getenv("BF_ILU_SLEEP") ? (unsigned)atoi(getenv("BF_ILU_SLEEP")) : 0u;
-  if (c->ilu_vflag) {
+  if (c->ilu_pencil) {
+    PencilGeom g{c->ilu_geom[0], c->ilu_geom[1], c->ilu_geom[2], c->ilu_geom[3], c->ilu_geom[4], c->ilu_geom[5],
+                 c->ilu_geom[6]};
+    int grid = std::min(g.NJ * g.NK, c->num_sms * 2);
+    k_ilu_pencil<false><<<grid, 128, kPencilSmem, c->stream>>>(
+        g, reinterpret_cast<const double2 *>(c->ilu_ld), nullptr, reinterpret_cast<double2 *>(r), nrm2,
+        reinterpret_cast<double2 *>(c->ilu_y), nullptr, c->ilu_order, &sy->ticket[0], &sy->done[0], &sy->ticket[1],
+        c->var_order);
+    k_ilu_pencil<true><<<grid, 128, kPencilSmem, c->stream>>>(
+        g, reinterpret_cast<const double2 *>(c->ilu_ud), reinterpret_cast<const double2 *>(c->ilu_dinv),
+        reinterpret_cast<double2 *>(c->ilu_y), nullptr, reinterpret_cast<double2 *>(c->ilu_u),
+        reinterpret_cast<double2 *>(c->ilu_y), c->ilu_order, &sy->ticket[1], &sy->done[1], &sy->ticket[0], 0);
+  } else if (c->ilu_vflag) {
     k_ilu_fwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
                                                     reinterpret_cast<double2 *>(r), nrm2,
                                                     reinterpret_cast<double2 *>(c->ilu_y), c->ilu_flag, sy,
@@ -683,6 +954,9 @@ bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
   } else if (func == (const void *)k_ilu_fwd_v) {
     nargs = nargs_of(k_ilu_fwd_v);
     roles = {{6, 0}, {7, 1}};
+  } else if (func == (const void *)k_ilu_pencil<false>) {
+    nargs = nargs_of(k_ilu_pencil<false>);
+    roles = {{3, 0}, {4, 1}};
   } else if (func == (const void *)k_cpr_resid) {
     nargs = nargs_of(k_cpr_resid);
     roles = {{7, 0}};

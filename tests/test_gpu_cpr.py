@@ -186,23 +186,47 @@ def test_coupled_amg(config, dims):
 
 
 def test_sweep_variants_bit_identical(monkeypatch):
-    """The flag-array sweeps (BF_ILU_FLAGS=1) and the default value-flag sweeps compute every
-    row in the same order: bit-identical ILU solves, repeated (sentinels restored each time)."""
-    prob, J, rhs = make_system(2, dims=(17, 13, 11))
-    g_v = gpu_solver(J, prob.dims, precond=2)
-    monkeypatch.setenv("BF_ILU_FLAGS", "1")
-    g_f = gpu_solver(J, prob.dims, precond=2)
-    N = 2 * J.n
-    for seed in (1, 2, 3):
-        r = torch_dev(seeded_vector(N, seed))
-        a = torch.empty(N, dtype=torch.float64, device="cuda")
-        b = torch.empty(N, dtype=torch.float64, device="cuda")
-        for _ in range(2):
-            g_v.ilu_solve(r, a)
-            g_f.ilu_solve(r, b)
-            assert torch.equal(a, b)
-        za = torch.empty(N, dtype=torch.float64, device="cuda")
-        zb = torch.empty(N, dtype=torch.float64, device="cuda")
-        g_v.apply_precond(r, za)
-        g_f.apply_precond(r, zb)
-        assert torch.equal(za, zb)
+    """The three ILU sweep implementations compute every row in the oracle's order: the
+    pencil-wavefront sweeps (default on grid-structured J), the generic value-flag sweeps
+    (BF_ILU_PENCIL=0) and the flag-array sweeps (BF_ILU_FLAGS=1) give bit-identical solves and
+    applies, repeatedly (sentinels and tickets restored each time), on 3D and 2D grids."""
+    for config, dims in ((2, (17, 13, 11)), (3, (40, 33, 21)), (1, (37, 23, 1))):
+        prob, J, rhs = make_system(config, dims=dims)
+        monkeypatch.delenv("BF_ILU_FLAGS", raising=False)
+        monkeypatch.delenv("BF_ILU_PENCIL", raising=False)
+        g_p = gpu_solver(J, prob.dims, precond=2)
+        monkeypatch.setenv("BF_ILU_PENCIL", "0")
+        g_v = gpu_solver(J, prob.dims, precond=2)
+        monkeypatch.delenv("BF_ILU_PENCIL")
+        monkeypatch.setenv("BF_ILU_FLAGS", "1")
+        g_f = gpu_solver(J, prob.dims, precond=2)
+        monkeypatch.delenv("BF_ILU_FLAGS")
+        o = oracle.BF(J, precond=2)
+        olu, odinv = o.ilu()
+        N = 2 * J.n
+        for seed in (1, 2):
+            rn = seeded_vector(N, seed)
+            r = torch_dev(rn)
+            outs = []
+            for g in (g_p, g_v, g_f):
+                a = torch.empty(N, dtype=torch.float64, device="cuda")
+                for _ in range(2):
+                    g.ilu_solve(r, a)
+                outs.append(a)
+            assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2]), dims
+            xo = oracle.ilu0_solve(J, olu, odinv, rn)
+            assert np.linalg.norm(outs[0].cpu().numpy() - xo) <= 1e-12 * np.linalg.norm(xo)
+            zs = []
+            for g in (g_p, g_v, g_f):
+                z = torch.empty(N, dtype=torch.float64, device="cuda")
+                g.apply_precond(r, z)
+                zs.append(z)
+            assert torch.equal(zs[0], zs[1]) and torch.equal(zs[1], zs[2]), dims
+        # GMRES through the graph-captured apply with the pencil sweeps
+        x = torch.zeros(N, dtype=torch.float64, device="cuda")
+        rg = g_p.solve(torch_dev(rhs), x, tol=1e-8, maxit=300)
+        ro = o.gmres(rhs, tol=1e-8, maxit=300)
+        assert abs(rg["iters"] - ro["iters"]) <= 1
+        x = x.cpu().numpy()
+        for f in (0, 1):
+            assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
