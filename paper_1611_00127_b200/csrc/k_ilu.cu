@@ -599,6 +599,28 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
 #pragma unroll
     for (int s = 0; s < PD - 1; s++) issue(s);
     double2 prev = make_double2(0.0, 0.0);
+    // cross-tile dependencies (threads on the tile's jj = 0 / kk = 0 faces) are loaded XD steps
+    // before use: the neighbouring tile runs ahead, so the value is usually already published
+    // and the L2 round trip leaves the critical path; a sentinel falls back to polling
+    // (two steps ahead: slots 0/1 by step parity, named registers so nothing spills to the stack)
+    double2 pk0 = sent2(), pk1 = sent2(), pj0 = sent2(), pj1 = sent2();
+    auto xfetch = [&](int s) {
+      int c = cell_of(s);
+      double2 vk = sent2(), vj = sent2();
+      if (c >= 0) {
+        if (kw > 0 && kk == 0) vk = ld_poll(out + (c + dk));
+        if (jw > 0 && jj == 0) vj = ld_poll(out + (c + dj));
+      }
+      if (s & 1) {
+        pk1 = vk;
+        pj1 = vj;
+      } else {
+        pk0 = vk;
+        pj0 = vj;
+      }
+    };
+    xfetch(0);
+    xfetch(1);
     for (int s = 0; s < nsteps; s++) {
       issue(s + PD - 1);
       cp_wait<PD - 1>();
@@ -625,14 +647,20 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
         double2 vk = make_double2(0.0, 0.0), vj = vk;
         const bool hk = kw > 0, hj = jw > 0, hi = iw > 0;
         if (hk) {
-          if (kk > 0) vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
-          else
-            do vk = ld_poll(out + (c + dk)); while (!ready2(vk));
+          if (kk > 0) {
+            vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
+          } else {
+            vk = (s & 1) ? pk1 : pk0;
+            while (!ready2(vk)) vk = ld_poll(out + (c + dk));
+          }
         }
         if (hj) {
-          if (jj > 0) vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
-          else
-            do vj = ld_poll(out + (c + dj)); while (!ready2(vj));
+          if (jj > 0) {
+            vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
+          } else {
+            vj = (s & 1) ? pj1 : pj0;
+            while (!ready2(vj)) vj = ld_poll(out + (c + dj));
+          }
         }
         auto sub = [&](int slot, double2 v) {
           double2 b01 = st.f[2 * slot], b23 = st.f[2 * slot + 1];
@@ -654,6 +682,7 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
         prev = res;
       }
       if (thr) sbuf[(s & 1) * 128 + kk * g.TJ + jj] = res;
+      xfetch(s + 2);
       __syncthreads();
     }
     cp_wait<0>();
