@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
                                                     const double2 *__restrict__ dinv, double2 *in,
                                                     const double *nrm2, double2 *out, double2 *yreset,
                                                     const int2 *__restrict__ order, unsigned *ticket,
-                                                    unsigned *done, unsigned *other_ticket, int ip) {
+                                                    unsigned *done, unsigned *other_ticket, int ip, int lag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2 *sbuf = reinterpret_cast<double2 *>(smem_raw);                        // [2][TK][TJ]
   Stage *ring = reinterpret_cast<Stage *>(smem_raw + 2 * 128 * sizeof(double2));  // [PD][128]
@@ -599,29 +599,37 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
 #pragma unroll
     for (int s = 0; s < PD - 1; s++) issue(s);
     double2 prev = make_double2(0.0, 0.0);
-    // cross-tile dependencies (threads on the tile's jj = 0 / kk = 0 faces) are loaded XD steps
+    // cross-tile dependencies (threads on the tile's jj = 0 / kk = 0 faces) are loaded two steps
     // before use: the neighbouring tile runs ahead, so the value is usually already published
-    // and the L2 round trip leaves the critical path; a sentinel falls back to polling
-    // (two steps ahead: slots 0/1 by step parity, named registers so nothing spills to the stack)
-    double2 pk0 = sent2(), pk1 = sent2(), pj0 = sent2(), pj1 = sent2();
-    auto xfetch = [&](int s) {
+    // and the L2 round trip leaves the critical path; a sentinel falls back to polling.  The
+    // step loop is unrolled by two so each prefetch slot is a fixed register pair (a select on
+    // the step parity would make the thread wait for the load immediately).
+    auto xfetch = [&](int s, double2 &pk, double2 &pj) {
       int c = cell_of(s);
-      double2 vk = sent2(), vj = sent2();
+      pk = sent2();
+      pj = sent2();
       if (c >= 0) {
-        if (kw > 0 && kk == 0) vk = ld_poll(out + (c + dk));
-        if (jw > 0 && jj == 0) vj = ld_poll(out + (c + dj));
-      }
-      if (s & 1) {
-        pk1 = vk;
-        pj1 = vj;
-      } else {
-        pk0 = vk;
-        pj0 = vj;
+        if (kw > 0 && kk == 0) pk = ld_poll(out + (c + dk));
+        if (jw > 0 && jj == 0) pj = ld_poll(out + (c + dj));
       }
     };
-    xfetch(0);
-    xfetch(1);
-    for (int s = 0; s < nsteps; s++) {
+    double2 pk0, pk1, pj0, pj1;
+    // optional start lag: face threads first wait until the neighbouring tile has published the
+    // cell `lag` positions ahead of their first dependency, so the two-step prefetch finds
+    // published values (the tiles then run with that slack)
+    if (lag > 0 && line) {
+      int iw = min(lag, g.nx - 1);
+      int c = base + (BWD ? g.nx - 1 - iw : iw);
+      if (kw > 0 && kk == 0)
+        while (!ready2(ld_poll(out + (c + dk)))) {
+        }
+      if (jw > 0 && jj == 0)
+        while (!ready2(ld_poll(out + (c + dj)))) {
+        }
+    }
+    xfetch(0, pk0, pj0);
+    xfetch(1, pk1, pj1);
+    auto step = [&](int s, double2 &pk, double2 &pj) {
       issue(s + PD - 1);
       cp_wait<PD - 1>();
       int c = cell_of(s);
@@ -650,7 +658,7 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
           if (kk > 0) {
             vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
           } else {
-            vk = (s & 1) ? pk1 : pk0;
+            vk = pk;
             while (!ready2(vk)) vk = ld_poll(out + (c + dk));
           }
         }
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
           if (jj > 0) {
             vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
           } else {
-            vj = (s & 1) ? pj1 : pj0;
+            vj = pj;
             while (!ready2(vj)) vj = ld_poll(out + (c + dj));
           }
         }
@@ -682,8 +690,12 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
         prev = res;
       }
       if (thr) sbuf[(s & 1) * 128 + kk * g.TJ + jj] = res;
-      xfetch(s + 2);
+      xfetch(s + 2, pk, pj);  // this slot's next use is step s + 2
       __syncthreads();
+    };
+    for (int s = 0; s < nsteps; s += 2) {
+      step(s, pk0, pj0);
+      if (s + 1 < nsteps) step(s + 1, pk1, pj1);
     }
     cp_wait<0>();
   }
@@ -785,8 +797,9 @@ static void setup_pencil(bf_ctx *c) {
     g.nx = c->nx;
     g.ny = c->ny;
     g.nz = c->nz;
-    g.TK = std::min(c->nz, 8);
-    g.TJ = std::min(c->ny, 128 / g.TK);
+    g.TK = std::min(c->nz, getenv("BF_PENCIL_TK") ? atoi(getenv("BF_PENCIL_TK")) : 8);
+    g.TJ = std::min(c->ny, getenv("BF_PENCIL_TJ") ? atoi(getenv("BF_PENCIL_TJ")) : 128 / g.TK);
+    if (g.TK < 1 || g.TJ < 1 || g.TJ * g.TK > 128) throw Error(BF_ERR_ARG, "pencil tile TJ*TK must be in [1, 128]");
     g.NJ = div_up(c->ny, g.TJ);
     g.NK = div_up(c->nz, g.TK);
     std::vector<int2> ord;
@@ -893,14 +906,15 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
     PencilGeom g{c->ilu_geom[0], c->ilu_geom[1], c->ilu_geom[2], c->ilu_geom[3], c->ilu_geom[4], c->ilu_geom[5],
                  c->ilu_geom[6]};
     int grid = std::min(g.NJ * g.NK, c->num_sms * 2);
+    static const int lag = getenv("BF_PENCIL_LAG") ? atoi(getenv("BF_PENCIL_LAG")) : 0;
     k_ilu_pencil<false><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ld), nullptr, reinterpret_cast<double2 *>(r), nrm2,
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, c->ilu_order, &sy->ticket[0], &sy->done[0], &sy->ticket[1],
-        c->var_order);
+        c->var_order, lag);
     k_ilu_pencil<true><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ud), reinterpret_cast<const double2 *>(c->ilu_dinv),
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, reinterpret_cast<double2 *>(c->ilu_u),
-        reinterpret_cast<double2 *>(c->ilu_y), c->ilu_order, &sy->ticket[1], &sy->done[1], &sy->ticket[0], 0);
+        reinterpret_cast<double2 *>(c->ilu_y), c->ilu_order, &sy->ticket[1], &sy->done[1], &sy->ticket[0], 0, lag);
   } else if (c->ilu_vflag) {
     k_ilu_fwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
                                                     reinterpret_cast<double2 *>(r), nrm2,

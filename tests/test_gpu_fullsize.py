@@ -68,9 +68,15 @@ def test_c3_gmres_forced_iterations(c3):
 def test_c5_full_size_sampled():
     """C5 (256x256x128, 16.8M DOF), the largest configuration: hierarchies bit-exact on every
     level, BF apply <= 1e-10 and 5 forced GMRES iterations <= 1e-6 against the oracle."""
+    import time
+    t0 = time.time()
+    lap = lambda what: print(f"[c5] {what} {time.time() - t0:.1f} s", flush=True)
     prob, J, rhs = make_system(5)
+    lap("make_system")
     g = gpu_solver(J, prob.dims)
+    lap("gpu setup")
     o = oracle.BF(J)
+    lap("oracle setup")
     for which in (0, 1):
         assert g.num_levels(which) == o.nlev(which)
         for l in range(o.nlev(which)):
@@ -79,14 +85,19 @@ def test_c5_full_size_sampled():
             assert pat and val, (which, l)
             if l < o.nlev(which) - 1:
                 assert np.array_equal(G["cf"], O["cf"]), (which, l)
+            del G, O
+    lap("hierarchies compared")
     x = seeded_vector(2 * J.n, 55)
     z = torch.empty(2 * J.n, dtype=torch.float64, device="cuda")
     g.apply_precond(torch_dev(x), z)
     zo = o.apply(x)
     assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+    lap("apply compared")
     ro = o.gmres(rhs, tol=0.0, restart=30, maxit=5)
+    lap("oracle gmres")
     xg = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
     r = g.solve(torch_dev(rhs), xg, tol=0.0, restart=30, maxit=5)
     xg = xg.cpu().numpy()
+    lap("gpu gmres")
     for f in (0, 1):
         assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
