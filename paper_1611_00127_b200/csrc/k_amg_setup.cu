@@ -543,10 +543,13 @@ __device__ __forceinline__ int row_table_mask(const DCsr &A, const DCsr &B, int 
 __device__ __forceinline__ int hash_slot(int key, int mask) { return (int)(((unsigned)key * 2654435761u) >> 16) & mask; }
 
 // returns the slot of key, inserting it if absent (inserted == true for the inserting lane)
+// returns the key's slot, or -1 when the table is full (every slot probed: the caller falls back
+// to the expand-sort-compress product -- a row of the coarse Galerkin operators can exceed the
+// table between two of the count kernel's fill checks, e.g. on C5's stalled coarse levels)
 __device__ __forceinline__ int hash_insert(int *keys, int key, int mask, bool &inserted) {
   int s = hash_slot(key, mask);
   inserted = false;
-  while (true) {
+  for (int probe = 0; probe <= mask; probe++) {
     int prev = atomicCAS(&keys[s], -1, key);
     if (prev == -1) {
       inserted = true;
@@ -555,6 +558,7 @@ __device__ __forceinline__ int hash_insert(int *keys, int key, int mask, bool &i
     if (prev == key) return s;
     s = (s + 1) & mask;
   }
+  return -1;
 }
 
 // the row's A entries (column k, value a) and B row bounds are loaded lane-parallel, 32 at
@@ -600,15 +604,20 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, D
     int nq = min(32, r1 - q0);
     for (int u = 0; u < nq && !full; u++) {
       int bs = __shfl_sync(0xffffffffu, ch.bs, u), be = __shfl_sync(0xffffffffu, ch.be, u);
+      bool spill = false;
       for (int t = bs + lane; t < be; t += 32) {
         bool ins;
-        hash_insert(keys, B.ci[t], mask, ins);
+        if (hash_insert(keys, B.ci[t], mask, ins) < 0) {
+          spill = true;
+          break;
+        }
         count += ins;
       }
       // stop early once the row cannot fit (the product then falls back to the ESC path)
       int tot = count;
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      full = tot > HASH_MAX;
+      full = tot > HASH_MAX || __any_sync(0xffffffffu, spill);
+      if (full && lane == 0) count = HASH_MAX + 1;  // forces the overflow flag below
     }
   }
   for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);

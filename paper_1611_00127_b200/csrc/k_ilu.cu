@@ -548,7 +548,8 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
                                                     const double2 *__restrict__ dinv, double2 *in,
                                                     const double *nrm2, double2 *out, double2 *yreset,
                                                     const int2 *__restrict__ order, unsigned *ticket,
-                                                    unsigned *done, unsigned *other_ticket, int ip, int lag) {
+                                                    unsigned *done, unsigned *other_ticket, int ip, int lag,
+                                                    unsigned backoff) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2 *sbuf = reinterpret_cast<double2 *>(smem_raw);                        // [2][TK][TJ]
   Stage *ring = reinterpret_cast<Stage *>(smem_raw + 2 * 128 * sizeof(double2));  // [PD][128]
@@ -621,11 +622,9 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
       int iw = min(lag, g.nx - 1);
       int c = base + (BWD ? g.nx - 1 - iw : iw);
       if (kw > 0 && kk == 0)
-        while (!ready2(ld_poll(out + (c + dk)))) {
-        }
+        while (!ready2(ld_poll(out + (c + dk)))) __nanosleep(backoff);
       if (jw > 0 && jj == 0)
-        while (!ready2(ld_poll(out + (c + dj)))) {
-        }
+        while (!ready2(ld_poll(out + (c + dj)))) __nanosleep(backoff);
     }
     xfetch(0, pk0, pj0);
     xfetch(1, pk1, pj1);
@@ -659,7 +658,10 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
             vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
           } else {
             vk = pk;
-            while (!ready2(vk)) vk = ld_poll(out + (c + dk));
+            while (!ready2(vk)) {  // not yet published: back off so waiting tiles do not flood L2
+              __nanosleep(backoff);
+              vk = ld_poll(out + (c + dk));
+            }
           }
         }
         if (hj) {
@@ -667,7 +669,10 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
             vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
           } else {
             vj = pj;
-            while (!ready2(vj)) vj = ld_poll(out + (c + dj));
+            while (!ready2(vj)) {
+              __nanosleep(backoff);
+              vj = ld_poll(out + (c + dj));
+            }
           }
         }
         auto sub = [&](int slot, double2 v) {
@@ -907,14 +912,15 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
                  c->ilu_geom[6]};
     int grid = std::min(g.NJ * g.NK, c->num_sms * 2);
     static const int lag = getenv("BF_PENCIL_LAG") ? atoi(getenv("BF_PENCIL_LAG")) : 0;
+    static const unsigned pbackoff = getenv("BF_PENCIL_SLEEP") ? (unsigned)atoi(getenv("BF_PENCIL_SLEEP")) : 200u;
     k_ilu_pencil<false><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ld), nullptr, reinterpret_cast<double2 *>(r), nrm2,
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, c->ilu_order, &sy->ticket[0], &sy->done[0], &sy->ticket[1],
-        c->var_order, lag);
+        c->var_order, lag, pbackoff);
     k_ilu_pencil<true><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ud), reinterpret_cast<const double2 *>(c->ilu_dinv),
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, reinterpret_cast<double2 *>(c->ilu_u),
-        reinterpret_cast<double2 *>(c->ilu_y), c->ilu_order, &sy->ticket[1], &sy->done[1], &sy->ticket[0], 0, lag);
+        reinterpret_cast<double2 *>(c->ilu_y), c->ilu_order, &sy->ticket[1], &sy->done[1], &sy->ticket[0], 0, lag, pbackoff);
   } else if (c->ilu_vflag) {
     k_ilu_fwd_v<<<ilu_grid(c), 256, 0, c->stream>>>(n, c->ilu_perm, c->brp, c->bci, c->ilu_dpos, c->ilu_lu,
                                                     reinterpret_cast<double2 *>(r), nrm2,
