@@ -912,7 +912,7 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
                  c->ilu_geom[6]};
     int grid = std::min(g.NJ * g.NK, c->num_sms * 2);
     static const int lag = getenv("BF_PENCIL_LAG") ? atoi(getenv("BF_PENCIL_LAG")) : 0;
-    static const unsigned pbackoff = getenv("BF_PENCIL_SLEEP") ? (unsigned)atoi(getenv("BF_PENCIL_SLEEP")) : 200u;
+    static const unsigned pbackoff = getenv("BF_PENCIL_SLEEP") ? (unsigned)atoi(getenv("BF_PENCIL_SLEEP")) : 0u;
     k_ilu_pencil<false><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ld), nullptr, reinterpret_cast<double2 *>(r), nrm2,
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, c->ilu_order, &sy->ticket[0], &sy->done[0], &sy->ticket[1],
