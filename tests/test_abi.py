@@ -53,3 +53,36 @@ def test_default_options_without_gpu():
     from paper_1611_00127_b200 import bf_default_options
     o = bf_default_options()
     assert o.theta == 0.25 and o.max_coarse == 64 and o.nu_pre == 1 and o.interp_norm == 1
+    assert o.precond == 0  # BF (Algorithm 3); 1, 2 CPR-AMG(1)/(2), 3 coupled AMG
+    # the binding's struct mirrors include/bf.h field by field (a missing field would shift the rest)
+    import ctypes
+    from paper_1611_00127_b200 import binding
+    src = open(os.path.join(ROOT, "include", "bf.h")).read()
+    body = src[src.index("typedef struct {\n  double theta;"):src.index("} bf_options;")]
+    decls = re.findall(r"^\s*(?:double|int32_t|uint64_t)\s+([\w\s,]+);", body, re.M)
+    fields = [f.strip() for d in decls for f in d.split(",")]
+    assert [f for f, _ in binding.bf_options._fields_] == fields
+
+
+def test_oracle_struct_mirrors():
+    """oracle/__init__.py's ctypes mirrors of or_options and or_bf follow oracle.h field by field."""
+    import oracle
+    src = open(os.path.join(ROOT, "oracle", "oracle.h")).read()
+
+    def fields(tag):
+        body = src[src.rindex("typedef struct {", 0, src.index("} " + tag + ";")):src.index("} " + tag + ";")]
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        out = []
+        types = r"(?:double|int32_t|uint64_t|int64_t|int8_t|uint8_t|or_csr|or_amg|or_options)"
+        for stmt in body.split(";"):
+            m = re.match(r"\s*" + types + r"\s+(.+)$", stmt.replace("typedef struct {", ""), re.S)
+            if not m:
+                continue
+            for f in m.group(1).split(","):
+                out.append(re.sub(r"[\*\s]|\[.*\]", "", f))
+        return out
+
+    assert [f for f, _ in oracle.Options._fields_] == fields("or_options")
+    names = [f for f, _ in oracle.BFs._fields_]
+    want = fields("or_bf")
+    assert names == want, (names, want)
