@@ -28,6 +28,7 @@ struct DCsr {
   int32_t g = 1;             // lanes per row in the TMA kernel
   int32_t stages = 2;        // TMA pipeline depth
   int32_t nt = 256;          // TMA kernel CTA size (128 for long Galerkin rows: smaller tiles, more CTAs)
+  bool short_rows = false;   // thread-per-row kernel (k_csr_short): large P / R with mean row length <= 4
   int16_t *lidx = nullptr;   // local-index variant (k_csr_lx.cuh): per-nonzero index into its tile's U_t
   int32_t *ucol = nullptr, *uoff = nullptr;  // concatenated U_t, tile offsets
   int32_t ucap = 0;

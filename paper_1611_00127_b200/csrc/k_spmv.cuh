@@ -94,6 +94,61 @@ __global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, const int32_t *__
   }
 }
 
+// Short-row CSR kernel (interpolation P and restriction R of the large levels: 1-8 entries per
+// row): one thread per row, no staging.  The row's (col, val) entries -- setup data -- are
+// loaded into registers BEFORE griddepcontrol.wait (programmatic dependent launch), so only
+// the gathers of x and the epilogue wait for the kernel that produced x; consecutive threads'
+// entries are contiguous, so the streaming loads of a warp coalesce.
+constexpr int SHORT_K = 8;
+template <int MODE>
+__global__ void __launch_bounds__(256) k_csr_short(int n, const int32_t *__restrict__ rp,
+                                                   const int32_t *__restrict__ ci,
+                                                   const double *__restrict__ v, const double *__restrict__ x,
+                                                   const double *__restrict__ b, const double *__restrict__ dinv,
+                                                   double *__restrict__ y, double *__restrict__ aux, double alpha,
+                                                   double beta, const double *__restrict__ dir) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int lo = 0, hi = 0;
+  int col[SHORT_K];
+  double val[SHORT_K];
+  if (r < n) {
+    lo = __ldg(rp + r);
+    hi = __ldg(rp + r + 1);
+#pragma unroll
+    for (int e = 0; e < SHORT_K; e++)
+      if (lo + e < hi) {
+        col[e] = __ldcs(ci + lo + e);
+        val[e] = __ldcs(v + lo + e);
+      }
+  }
+  pdl_wait();
+  if (r >= n) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < SHORT_K; e++)
+    if (lo + e < hi) acc += val[e] * __ldg(x + col[e]);
+  for (int q = lo + SHORT_K; q < hi; q++) acc += __ldcs(v + q) * __ldg(x + __ldcs(ci + q));
+  if (MODE == OP_SPMV) {
+    y[r] = acc;
+  } else if (MODE == OP_SPMV_X0) {
+    y[r] = acc;
+    aux[r] = beta * (acc * dinv[r]);
+  } else if (MODE == OP_RESID) {
+    y[r] = b[r] - acc;
+  } else if (MODE == OP_SUB_X0) {
+    double t = b[r] - acc;
+    y[r] = t;
+    aux[r] = beta * (t * dinv[r]);
+  } else if (MODE == OP_SMOOTH) {
+    double dn = beta * ((b[r] - acc) * dinv[r]);
+    if (dir) dn += alpha * dir[r];
+    y[r] = x[r] + dn;
+    if (aux) aux[r] = dn;
+  } else if (MODE == OP_ADD) {
+    y[r] += acc;
+  }
+}
+
 // lanes per row: keep R * (mean row length) near one chunk, and keep >= ~4 warps per SM
 inline int lanes_for(const bf_ctx *c, const DCsr &A) {
   double avg = A.n ? (double)A.nnz / A.n : 1.0;
@@ -132,6 +187,13 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
   if (A.n == 0) return;
   c->alg_bytes += csr_op_bytes<MODE>(A, dir != nullptr, aux != nullptr);
   if (csr_op_dia<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
+  if (A.short_rows) {
+    launch_pdl(c, k_csr_short<MODE>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.rp, A.ci, A.v, x, b, dinv, y, aux,
+               alpha, beta, dir);
+    BF_LAUNCH(c);
+    BF_CUDA(cudaGetLastError());
+    return;
+  }
   if (c->use_tma && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   int G = lanes_for(c, A);
   int rows_per_block = (32 / G) * CSR_WARPS;

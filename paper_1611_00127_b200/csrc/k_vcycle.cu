@@ -441,8 +441,16 @@ __global__ void k_zero(int n, double *x) {
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   A.rpt = 0;
   A.cap = 0;
+  A.short_rows = false;
   if (A.n == 0 || A.nnz == 0) return;
   double mean = (double)A.nnz / A.n;
+  {  // large matrices with short rows (the fine levels' P and R): thread-per-row kernel
+    static const char *es = getenv("BF_SHORT");
+    static const double lim = es ? atof(es) : 8.0;  // BF_SHORT=0 disables
+    static const char *en = getenv("BF_SHORT_N");
+    static const int64_t nmin = en ? atoll(en) : 65536;
+    if (!stencil && mean <= lim && A.n >= nmin) A.short_rows = true;
+  }
   int g = 1;
   if (force_g > 0) {
     g = force_g;
