@@ -329,3 +329,47 @@ def test_solve_path_variants(variant, config, dims, monkeypatch):
     for f in (0, 1):
         assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2]), variant
     g.close()
+
+
+def test_long_rows_hash_overflow_regression():
+    """A hub cell coupled to 700 others makes rows longer than the 512-slot shared-memory hash
+    table of the SpGEMM (the C5 setup hang of round 1): setup must fall back to the
+    expand-sort-compress product and stay bit-exact with the oracle."""
+    n = 1200
+    rng = np.random.default_rng(11)
+    hub = set(rng.choice(np.arange(1, n), 700, replace=False).tolist())
+    rows, cols = [], []
+    for i in range(n):
+        nb = {i}
+        if i > 0:
+            nb.add(i - 1)
+        if i < n - 1:
+            nb.add(i + 1)
+        if i == 0:
+            nb |= hub
+        elif i in hub:
+            nb.add(0)
+        for j in sorted(nb):
+            rows.append(i)
+            cols.append(j)
+    rows, cols = np.array(rows), np.array(cols)
+    rp = np.zeros(n + 1, np.int32)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    vals = np.zeros((len(cols), 2, 2))
+    off = rows != cols
+    vals[off] = -rng.uniform(0.5, 1.5, (off.sum(), 1, 1)) * np.array([[1.0, 0.1], [0.05, 1.0]])
+    deg = np.bincount(rows, weights=off.astype(float), minlength=n)
+    vals[~off] = np.array([[1.0, 0.0], [0.0, 1.0]]) * (2.0 * deg[rows[~off]] + 1.0)[:, None, None]
+    J = BSR2(n, rp, cols.astype(np.int32), vals)
+    g = gpu_solver(J, (n, 1, 1), max_coarse=32)
+    o = oracle.BF(J, max_coarse=32)
+    for which in (0, 1):
+        assert g.num_levels(which) == o.nlev(which)
+        for l in range(o.nlev(which)):
+            pat, val = csr_equal(g.level(which, l)["A"], o.level(which, l)["A"])
+            assert pat and val, (which, l)
+    v = seeded_vector(2 * n, 4)
+    z = np.zeros(2 * n)
+    g.apply_precond(v, z)
+    zo = o.apply(v)
+    assert np.linalg.norm(z - zo) <= 1e-10 * np.linalg.norm(zo)
