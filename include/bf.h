@@ -83,8 +83,10 @@ typedef struct {
   int32_t orth;                /* 0 CGS2 (default), 1 CGS1 */
   int32_t schur_as_printed;    /* 0: A_sp (default, R1); 1: literal P:L239 (A_pp), diagnostics only */
   int32_t interp_norm;         /* 1: interpolation weights normalised so P 1 = 1 (default, R8); 0: Q26 denominators */
-  int32_t timing;              /* 1: record CUDA events around the J SpMV and the GMRES
-                                  orthogonalisation kernels (bf_kernel_time) */
+  int32_t timing;              /* 1: record CUDA events around the J SpMV, the GMRES
+                                  orthogonalisation kernels and the preconditioner apply of every
+                                  Arnoldi step (bf_kernel_time); k > 1: of every k-th step only
+                                  (sampled, less perturbation of the timed solve); 0: off */
   int32_t precond;             /* preconditioner M of `precon-system`:
                                   0 BF, Algorithm 3 (default; hierarchies 0 A_ss, 1 S~);
                                   1 CPR-AMG(1) combinative, Algorithm 1;

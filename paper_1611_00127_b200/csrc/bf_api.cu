@@ -155,7 +155,7 @@ static cudaEvent_t event_get(bf_ctx *c) {
 
 void timer_begin(bf_ctx *c, int k, cudaEvent_t *start) {
   *start = nullptr;
-  if (!c->opt.timing) return;
+  if (!c->opt.timing || (k != 3 && c->timing_skip)) return;
   *start = event_get(c);
   BF_CUDA(cudaEventRecord(*start, c->stream));
 }

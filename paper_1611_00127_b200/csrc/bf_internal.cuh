@@ -145,6 +145,7 @@ struct bf_ctx {
   double apply_bytes = 0.0;     // algorithmic bytes of one BF apply (set at graph capture)
   int64_t syncs = 0;
   double sync_ms = 0.0;
+  bool timing_skip = false;     // opt.timing = k > 1: only every k-th Arnoldi step is timed
 };
 
 namespace bf {

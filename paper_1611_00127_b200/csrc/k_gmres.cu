@@ -325,6 +325,9 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
   // step j+1 already runs; a step enqueued past the stopping point is simply discarded.
   const int SLOT = 2 * MAXNV + 8;
   auto enqueue = [&](int j) {
+    // sampled instrumentation (opt.timing = k > 1): events around every k-th step only, so the
+    // timed region is barely perturbed; per-launch averages stay representative
+    c->timing_skip = c->opt.timing > 1 && ((*iters + j) % c->opt.timing) != 0;
     const double *vj = V + (size_t)j * N;
     double *vn = V + (size_t)(j + 1) * N;
     double *zj = c->Z + (size_t)j * N;
@@ -356,6 +359,7 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     BF_CUDA(cudaMemcpyAsync(c->hpin + (j & 1) * SLOT, c->hdev, sizeof(double) * (2 * MAXNV + 1),
                             cudaMemcpyDeviceToHost, c->stream));
     BF_CUDA(cudaEventRecord(c->step_ev[j & 1], c->stream));
+    c->timing_skip = false;
   };
   for (;;) {
     std::fill(g.begin(), g.end(), 0.0);
