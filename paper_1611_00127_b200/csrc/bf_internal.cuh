@@ -146,6 +146,7 @@ struct bf_ctx {
   int64_t syncs = 0;
   double sync_ms = 0.0;
   bool timing_skip = false;     // opt.timing = k > 1: only every k-th Arnoldi step is timed
+  int64_t timing_step = 0;      // Arnoldi steps enqueued since setup (sampling counter)
 };
 
 namespace bf {

@@ -327,7 +327,7 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
   auto enqueue = [&](int j) {
     // sampled instrumentation (opt.timing = k > 1): events around every k-th step only, so the
     // timed region is barely perturbed; per-launch averages stay representative
-    c->timing_skip = c->opt.timing > 1 && ((*iters + j) % c->opt.timing) != 0;
+    c->timing_skip = c->opt.timing > 1 && (c->timing_step++ % c->opt.timing) != 0;
     const double *vj = V + (size_t)j * N;
     double *vn = V + (size_t)(j + 1) * N;
     double *zj = c->Z + (size_t)j * N;
