@@ -9,6 +9,11 @@
  * Schur complement  S~ = A_pp - A_ps diag(A_ss)^-1 A_sp  (`SIMPLE-Schur`,
  * P:L236-241, read with A_sp in the last slot -- DESIGN.md R1).
  *
+ * The paper's comparison preconditioners are options of the same handle
+ * (bf_options.precond): CPR-AMG(1) / CPR-AMG(2), the two-stage combinative / additive
+ * preconditioners of Algorithms 1, 2 with a block ILU(0) of J as the first stage,
+ * and the coupled "point" AMG on J itself.
+ *
  * Everything on the path runs in hand-written CUDA kernels for sm_100a on one
  * GPU in fp64.  No torch types cross this boundary: plain pointers and sizes.
  *
