@@ -663,6 +663,8 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DC
       }
       if (cc >= 0) {
         bool ins;
+        // cannot return -1 here: the count kernel admitted this row (<= HASH_MAX distinct columns
+        // in a table of the same size), otherwise the whole product went to the ESC path
         int s = hash_insert(keys, cc, mask, ins);
         double acc = ins ? 0.0 : vals[s];
         vals[s] = __dadd_rn(acc, __dmul_rn(a, cv));
