@@ -162,8 +162,21 @@ def oracle_sample(J_full, prob, gpu_iters, restart, tol):
     sample = (f"oracle (plain C, -O2, 1 thread) on the first {nzs} of {nz} z-planes of the same C{prob_cfg(prob)} "
               f"Jacobian ({ns} cells, {2 * ns} DOF): full setup {t1 - t0:.2f} s + {r['iters']} GMRES "
               f"iterations at {per_iter:.3f} s each, extrapolated to {iters} iterations")
-    return dict(value=value, unit=UNIT, cores=1, kind="oracle", sample=sample,
+    return dict(value=value, unit=UNIT, cores=1, kind="oracle", sample=sample, host=host_cpu(),
                 setup_s=t1 - t0, per_iter_s=per_iter, wall_s=t2 - t0)
+
+
+def host_cpu():
+    """The box's host CPU (report nproc and the model next to the oracle timing)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}, nproc {os.cpu_count()}"
 
 
 def prob_cfg(prob):
@@ -205,7 +218,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, SPE10 stand-in)",
             "config": {"workload": workload_name(args.config, prob), "restart": args.restart, "tol": args.tol},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"],
+                             "host": res["host"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -377,7 +391,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(J, prob, int(statistics.median(rec["iters"])), args.restart, args.tol)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host")}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
