@@ -65,6 +65,35 @@ def test_c3_gmres_forced_iterations(c3):
     assert np.allclose(r["hist"], ro["hist"], rtol=1e-6, atol=0)
 
 
+def test_c3_cpr2_full_size(c3):
+    """NEXT-3 at full size (C3, 128^3, the bench configuration): CPR-AMG(2) block-ILU(0) factors
+    and A_pp / A_ss hierarchies bit-exact, ILU solve <= 1e-12 and one CPR apply <= 1e-10 against
+    the oracle, the pencil-wavefront sweeps on the 382-level dependency chain."""
+    prob, J, rhs, g0, o0 = c3
+    g = gpu_solver(J, prob.dims, precond=2)
+    o = oracle.BF(J, precond=2)
+    lu, dinv, levels = g.ilu(J.nnzb)
+    olu, odinv = o.ilu()
+    assert levels == 382
+    assert np.array_equal(lu.view(np.uint64), olu.view(np.uint64))
+    assert np.array_equal(dinv.view(np.uint64), odinv.view(np.uint64))
+    for which in (2, 0):
+        assert g.num_levels(which) == o.nlev(which)
+        for l in range(o.nlev(which)):
+            pat, val = csr_equal(g.level(which, l)["A"], o.level(which, l)["A"])
+            assert pat and val, (which, l)
+    N = 2 * J.n
+    r = seeded_vector(N, 31)
+    x = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.ilu_solve(torch_dev(r), x)
+    xo = oracle.ilu0_solve(J, olu, odinv, r)
+    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-12 * np.linalg.norm(xo)
+    z = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(r), z)
+    zo = o.apply(r)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+
+
 def test_c5_full_size_sampled():
     """C5 (256x256x128, 16.8M DOF), the largest configuration: hierarchies bit-exact on every
     level, BF apply <= 1e-10 and 5 forced GMRES iterations <= 1e-6 against the oracle."""
