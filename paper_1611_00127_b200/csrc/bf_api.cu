@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <string>
+#include <thread>
 
 #include "bf_internal.cuh"
 
@@ -227,6 +229,70 @@ static void destroy_ctx(bf_ctx *c) {
     return BF_ERR_CUDA;                                             \
   }
 
+
+// The two AMG hierarchies of a preconditioner are independent: they are built concurrently,
+// each on its own host thread and CUDA stream with a child context (its own allocation list,
+// counters and DIA offset storage), then merged into the handle.  The setup is partly
+// host-latency bound (~160 size read-backs per hierarchy at C3), so one hierarchy's host gaps
+// overlap the other's kernels.  Every value is computed by the same kernels in the same order,
+// so the hierarchies stay bit-identical to the oracle.  BF_SERIAL_SETUP=1 builds them in turn.
+static void build_two_hierarchies(bf_ctx *c, int w0, const DCsr &A0, int w1, const DCsr &A1) {
+  static const bool serial = getenv("BF_SERIAL_SETUP") != nullptr;
+  if (serial) {
+    build_hierarchy(c, w0, A0);
+    build_hierarchy(c, w1, A1);
+    return;
+  }
+  BF_CUDA(cudaStreamSynchronize(c->stream));  // A0, A1 were produced on the handle's stream
+  int dev = 0;
+  BF_CUDA(cudaGetDevice(&dev));
+  const int w[2] = {w0, w1};
+  const DCsr *A[2] = {&A0, &A1};
+  bf_ctx kid[2];
+  std::exception_ptr err[2];
+  for (int k = 0; k < 2; k++) {
+    kid[k].opt = c->opt;
+    kid[k].n = c->n;
+    kid[k].nx = c->nx;
+    kid[k].ny = c->ny;
+    kid[k].nz = c->nz;
+    kid[k].nnzb = c->nnzb;
+    kid[k].var_order = c->var_order;
+    kid[k].block_order = c->block_order;
+    kid[k].num_sms = c->num_sms;
+    kid[k].use_tma = c->use_tma;
+    kid[k].use_pdl = c->use_pdl;
+    BF_CUDA(cudaStreamCreateWithFlags(&kid[k].stream, cudaStreamNonBlocking));
+  }
+  std::thread th[2];
+  for (int k = 0; k < 2; k++)
+    th[k] = std::thread([&, k]() {
+      try {
+        BF_CUDA(cudaSetDevice(dev));
+        build_hierarchy(&kid[k], w[k], *A[k]);
+        sync(&kid[k]);
+      } catch (...) {
+        err[k] = std::current_exception();
+      }
+    });
+  for (auto &t : th) t.join();
+  for (int k = 0; k < 2; k++) {
+    cudaStreamSynchronize(kid[k].stream);
+    c->h[w[k]] = kid[k].h[w[k]];
+    for (auto &a : kid[k].allocs) c->allocs.push_back(a);
+    for (auto &a : kid[k].pending_free) c->pending_free.push_back(a);
+    for (auto &v : kid[k].dia_offsets) c->dia_offsets.emplace_back(std::move(v));  // buffers keep their address
+    c->dev_bytes += kid[k].dev_bytes;
+    c->launches += kid[k].launches;
+    c->alloc_ms += kid[k].alloc_ms;
+    c->syncs += kid[k].syncs;
+    c->sync_ms += kid[k].sync_ms;
+    cudaStreamDestroy(kid[k].stream);
+  }
+  for (int k = 0; k < 2; k++)
+    if (err[k]) std::rethrow_exception(err[k]);
+}
+
 extern "C" {
 
 bf_status bf_default_options(bf_options *o) {
@@ -307,21 +373,19 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
       lap("schur");
       tile_csr(c, c->blk[1]);
       setup_dia(c, c->blk[1]);
-      build_hierarchy(c, 0, c->blk[3]);
-      lap("amg A_ss");
-      build_hierarchy(c, 1, c->blk[4]);
-      lap("amg S~");
+      build_two_hierarchies(c, 0, c->blk[3], 1, c->blk[4]);
+      lap("amg A_ss + S~");
     } else if (pc == 3) {  // coupled point AMG on J
       build_jscalar(c, c->jsc);
       build_hierarchy(c, 3, c->jsc);
       lap("amg J");
     } else {  // CPR-AMG(1)/(2) (Algorithms 1, 2): A_pp [and A_ss] hierarchies, ILU(0) of J
-      build_hierarchy(c, 2, c->blk[0]);
-      lap("amg A_pp");
       if (pc == 2) {
-        build_hierarchy(c, 0, c->blk[3]);
-        lap("amg A_ss");
+        build_two_hierarchies(c, 2, c->blk[0], 0, c->blk[3]);
+      } else {
+        build_hierarchy(c, 2, c->blk[0]);
       }
+      lap("amg A_pp [+ A_ss]");
       build_ilu(c);
       lap("ilu0");
     }
