@@ -145,6 +145,7 @@ struct bf_ctx {
   double apply_bytes = 0.0;     // algorithmic bytes of one BF apply (set at graph capture)
   int64_t syncs = 0;
   double sync_ms = 0.0;
+  bool fuse_post0 = false;      // BF apply: S~ finest post-sweep fused with the merge (k_vcycle.cu)
   bool timing_skip = false;     // opt.timing = k > 1: only every k-th Arnoldi step is timed
   int64_t timing_step = 0;      // Arnoldi steps enqueued since setup (sampling counter)
 };

@@ -694,7 +694,9 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   }
   vcycle_level(c, h, l + 1);
   csr_op<OP_ADD>(c, L.P, Lc.x, nullptr, nullptr, x, nullptr, 0.0, 0.0, nullptr);  // x += P e
-  for (int s = 0; s < o.nu_post; s++) smooth_pass(c, L, x, false, false);
+  const bool skip_post = c->fuse_post0 && l == 0 && &h == &c->h[1];  // done by k_dia_smooth_merge
+  if (!skip_post)
+    for (int s = 0; s < o.nu_post; s++) smooth_pass(c, L, x, false, false);
   if (x != L.x) {  // keep the result in L.x (swap the buffers, no copy)
     L.t = L.x;
     L.x = x;
@@ -739,6 +741,30 @@ __global__ void k_split_vec(int n, int ip, double *__restrict__ v, double *__res
   x0[i] = beta * (s * dinv[i]);
 }
 
+// the last step of the BF apply on a DIA finest S~ level: one l1-Jacobi post-sweep
+// p = x + (b - S~ x) ./ dl1 (the OP_SMOOTH arithmetic, beta = 1) written straight into the
+// interleaved output with s: z = R_p^T p + R_s^T s (no p round trip, one launch less)
+__global__ void __launch_bounds__(256) k_dia_smooth_merge(int n, DiaOffsets o, const double *__restrict__ dv,
+                                                          const double *__restrict__ x,
+                                                          const double *__restrict__ b,
+                                                          const double *__restrict__ dinv,
+                                                          const double *__restrict__ s, double2 *__restrict__ z,
+                                                          int ip) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double eb = __ldg(b + r), ed = __ldg(dinv + r), ex = __ldg(x + r), es = __ldg(s + r);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int d = 0; d < o.k; d++) {
+    int col = r + o.off[d];
+    double a = __ldcs(dv + (size_t)d * n + r);
+    if (col >= 0 && col < n) acc += a * __ldg(x + col);
+  }
+  double dn = 1.0 * ((eb - acc) * ed);
+  double p = ex + dn;
+  z[r] = ip ? make_double2(es, p) : make_double2(p, es);
+}
+
 __global__ void k_merge_vec(int n, int ip, const double *__restrict__ p, const double *__restrict__ s,
                             double *__restrict__ z) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -763,9 +789,23 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   // step 3: r = R_p r_k - A_ps s
   csr_op<OP_SUB_X0>(c, c->blk[1], hs.lv[0].x, c->vp, hS.lv[0].d, hS.lv[0].b, hS.lv[0].x, 0.0, x0_beta(c->opt),
                     nullptr);
-  // step 4: S~ p = r by one V-cycle
+  // step 4: S~ p = r by one V-cycle.  With one l1-Jacobi post-sweep on a DIA finest level,
+  // that sweep and the merge z = R_p^T p + R_s^T s are one kernel (k_dia_smooth_merge)
+  static const bool no_fuse = getenv("BF_NO_MERGE_FUSE") != nullptr;
+  Level &S0 = hS.lv[0];
+  c->fuse_post0 = !no_fuse && c->opt.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
+                  hS.nlev > 1 && hS.dtail != 0 && hS.tail != 0;
   vcycle_level(c, hS, 0);
-  k_merge_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, hS.lv[0].x, hs.lv[0].x, z);
+  if (c->fuse_post0) {
+    c->fuse_post0 = false;
+    DiaOffsets o;
+    o.k = S0.A.dia_k;
+    for (int d = 0; d < o.k; d++) o.off[d] = S0.A.dia_off[d];
+    k_dia_smooth_merge<<<div_up(n, 256), 256, 0, c->stream>>>(n, o, S0.A.dia_v, S0.x, S0.b, S0.d, hs.lv[0].x,
+                                                              reinterpret_cast<double2 *>(z), ip);
+  } else {
+    k_merge_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, hS.lv[0].x, hs.lv[0].x, z);
+  }
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
 }
@@ -805,6 +845,9 @@ static bool patch_roles(const void *func, int &nargs, std::vector<std::pair<int,
   } else if (func == (const void *)k_merge_vec) {
     nargs = nargs_of(k_merge_vec);
     roles = {{4, 2}};
+  } else if (func == (const void *)k_dia_smooth_merge) {
+    nargs = nargs_of(k_dia_smooth_merge);
+    roles = {{7, 2}};
   } else {
     return cpr_patch_roles(func, nargs, roles);
   }
