@@ -564,8 +564,11 @@ bf_status bf_apply_precond(bf_handle c, const double *r, double *z, int32_t vec_
 }
 
 bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int32_t vec_mem, void *stream) {
-  if (!c || !b || !x || which < 0 || which > 3 || c->h[which].nlev == 0 || (vec_mem != 0 && vec_mem != 1))
+  if (!c) return BF_ERR_ARG;
+  if (!b || !x || which < 0 || which > 3 || c->h[which].nlev == 0 || (vec_mem != 0 && vec_mem != 1)) {
+    c->err = "bf_vcycle: bad argument or hierarchy not built by this handle's preconditioner";
     return BF_ERR_ARG;
+  }
   BF_GUARD_BEGIN
   c->stream = (cudaStream_t)stream;
   size_t bytes = sizeof(double) * (size_t)c->h[which].lv[0].A.n;
@@ -627,7 +630,11 @@ bf_status bf_get_block(bf_handle c, int32_t which, int64_t *nnz, int32_t *rowptr
 }
 
 bf_status bf_get_ilu(bf_handle c, double *lu, double *dinv, int32_t *levels) {
-  if (!c || !c->ilu_lu) return BF_ERR_ARG;
+  if (!c) return BF_ERR_ARG;
+  if (!c->ilu_lu) {
+    c->err = "bf_get_ilu: the handle has no ILU(0) (only CPR handles, precond 1 or 2)";
+    return BF_ERR_ARG;
+  }
   BF_GUARD_BEGIN
   if (lu) BF_CUDA(cudaMemcpyAsync(lu, c->ilu_lu, sizeof(double) * 4 * (size_t)c->nnzb, cudaMemcpyDeviceToHost, c->stream));
   if (dinv) BF_CUDA(cudaMemcpyAsync(dinv, c->ilu_dinv, sizeof(double) * 4 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
@@ -638,7 +645,11 @@ bf_status bf_get_ilu(bf_handle c, double *lu, double *dinv, int32_t *levels) {
 }
 
 bf_status bf_ilu_solve(bf_handle c, const double *r, double *x, int32_t vec_mem, void *stream) {
-  if (!c || !r || !x || !c->ilu_lu || (vec_mem != 0 && vec_mem != 1)) return BF_ERR_ARG;
+  if (!c) return BF_ERR_ARG;
+  if (!r || !x || !c->ilu_lu || (vec_mem != 0 && vec_mem != 1)) {
+    c->err = "bf_ilu_solve: needs a CPR handle (precond 1 or 2), non-NULL r and x, vec_mem 0|1";
+    return BF_ERR_ARG;
+  }
   BF_GUARD_BEGIN
   c->stream = (cudaStream_t)stream;
   const double *rd = vec_in(c, r, vec_mem, c->bd);

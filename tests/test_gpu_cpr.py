@@ -123,8 +123,10 @@ def test_cpr_var_order_host_pointers_update_and_errors():
         gpu_solver(J, prob.dims, precond=4)
     # a BF handle has no ILU
     gb = gpu_solver(J, prob.dims)
-    with pytest.raises(BFError):
+    with pytest.raises(BFError, match="BF_ERR_ARG.*CPR"):
         gb.ilu(J.nnzb)
+    with pytest.raises(BFError, match="BF_ERR_ARG.*hierarchy not built"):
+        gb.vcycle(2, np.zeros(J.n), np.zeros(J.n))
 
 
 def test_cpr_non_grid_pattern():
