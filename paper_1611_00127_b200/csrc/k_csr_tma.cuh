@@ -158,8 +158,22 @@ __global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int 
         if (MODE == OP_ADD) ex = y[r];
       }
       double acc = 0.0;
+      if (G >= 4) {  // Galerkin rows: all of a lane's gathers (<= 8) issued before the first FMA
+        double xv[8], av[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          int q = lo + sub + e * G;
+          xv[e] = q < hi ? __ldg(x + sc[q]) : 0.0;
+          av[e] = q < hi ? sv[q] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+          if (lo + sub + e * G < hi) acc += av[e] * xv[e];
+        for (int q = lo + sub + 8 * G; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+      } else {
 #pragma unroll 4
-      for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+        for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+      }
       if (G > 1) {
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);

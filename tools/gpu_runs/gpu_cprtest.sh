@@ -1,0 +1,2 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_cpr.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2
