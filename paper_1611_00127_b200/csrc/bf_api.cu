@@ -73,7 +73,7 @@ void *dalloc(bf_ctx *c, size_t bytes) {
   {
     std::lock_guard<std::mutex> lk(g_dev_mu);
     auto it = g_dev_free.lower_bound(sc);
-    if (it != g_dev_free.end() && it->first <= 2 * sc) {  // accept up to 2x: the concurrent setup threads interleave their requests
+    if (it != g_dev_free.end() && it->first <= sc + sc / 4) {  // accept <= 25 % slack
       sc = it->first;
       p = it->second;
       g_dev_free.erase(it);
