@@ -129,16 +129,12 @@ def traffic_from_profiles(kernel_class):
 
 
 # ------------------------------------------------------------------------------------------
-def oracle_sample(J_full, prob, gpu_iters, restart, tol):
-    """Bounded sample of the same workload for the CPU oracle (1 core): the first nz/4
-    z-planes of the SAME Jacobian (couplings to the dropped planes removed), full setup +
-    4 GMRES iterations; the per-iteration time is extrapolated to the GPU's iteration
-    count so the number is in the metric's unit (DOF-iters/s over setup+solve)."""
+def sub_jacobian(J_full, prob, frac=4):
+    """The first nz/frac z-planes of the SAME Jacobian (couplings to the dropped planes removed)."""
     import numpy as np
-    import oracle
     from workload import BSR2
     nx, ny, nz = prob.dims
-    nzs = max(1, nz // 4)
+    nzs = max(1, nz // frac)
     ns = nx * ny * nzs
     rp, ci, v = J_full.row_ptr, J_full.col_idx, J_full.vals
     keep = np.arange(rp[ns])
@@ -147,23 +143,51 @@ def oracle_sample(J_full, prob, gpu_iters, restart, tol):
     rows = rows[ci[:rp[ns]] < ns]
     rps = np.zeros(ns + 1, np.int32)
     np.cumsum(np.bincount(rows, minlength=ns), out=rps[1:])
-    Js = BSR2(ns, rps, np.ascontiguousarray(ci[keep]), np.ascontiguousarray(v[keep]), (nx, ny, nzs))
+    return BSR2(ns, rps, np.ascontiguousarray(ci[keep]), np.ascontiguousarray(v[keep]), (nx, ny, nzs)), nzs
+
+
+def oracle_sample(J_full, prob, iters, restart, tol, frac=4):
+    """Bounded sample of the same workload for the CPU oracle (1 core), in the metric's unit.
+
+    The sample is the first nz/frac z-planes of the SAME Jacobian.  Its cost is measured, not
+    modelled per iteration: the oracle setup, then ONE complete GMRES(restart) cycle (initial
+    residual, `restart` Arnoldi steps with CGS2 over the growing basis, the cycle-end update and
+    true residual) and one partial cycle of (iters mod restart) steps with its own cycle end.  A
+    solve of `iters` Arnoldi steps is floor(iters/restart) complete cycles plus that partial
+    one, so  t(iters) = setup + floor(iters/restart) t_cycle + t_partial  is the oracle's time
+    for `iters` iterations on the sample (each cycle of restarted GMRES does the same work,
+    independent of the residual).  `iters` is a measured iteration count of the full problem
+    (GPU and oracle agree within +-1, tests/test_gpu_*).  Calibrated against a full-size
+    oracle run (profiles/r02_oracle_c3_full.json)."""
+    import numpy as np
+    import oracle
+    Js, nzs = sub_jacobian(J_full, prob, frac)
+    ns = Js.n
+    nz = prob.dims[2]
     rhs = np.ones(2 * ns)
     t0 = time.perf_counter()
     bf = oracle.BF(Js)
     t1 = time.perf_counter()
-    k = 4
-    r = bf.gmres(rhs, tol=0.0, restart=restart, maxit=k)
+    r = bf.gmres(rhs, tol=0.0, restart=restart, maxit=restart)        # one complete cycle
     t2 = time.perf_counter()
-    per_iter = (t2 - t1) / max(r["iters"], 1)
-    iters = max(gpu_iters, 1)
-    t_est = (t1 - t0) + iters * per_iter
+    iters = max(int(iters), 1)
+    full_cycles, rem = divmod(iters, restart)
+    t_part = 0.0
+    if rem:
+        r2 = bf.gmres(rhs, tol=0.0, restart=restart, maxit=rem)        # the partial last cycle
+        t_part = time.perf_counter() - t2
+        assert r2["iters"] == rem
+    assert r["iters"] == restart
+    t_cycle = t2 - t1
+    t_est = (t1 - t0) + full_cycles * t_cycle + t_part
     value = 2 * ns * iters / t_est
     sample = (f"oracle (plain C, -O2, 1 thread) on the first {nzs} of {nz} z-planes of the same C{prob_cfg(prob)} "
-              f"Jacobian ({ns} cells, {2 * ns} DOF): full setup {t1 - t0:.2f} s + {r['iters']} GMRES "
-              f"iterations at {per_iter:.3f} s each, extrapolated to {iters} iterations")
+              f"Jacobian ({ns} cells, {2 * ns} DOF): setup {t1 - t0:.2f} s measured, one full GMRES({restart}) "
+              f"cycle {t_cycle:.2f} s measured, partial cycle of {rem} steps {t_part:.2f} s measured; "
+              f"{iters} iterations = {full_cycles} cycles + {rem} steps")
     return dict(value=value, unit=UNIT, cores=1, kind="oracle", sample=sample, host=host_cpu(),
-                setup_s=t1 - t0, per_iter_s=per_iter, wall_s=t2 - t0)
+                setup_s=t1 - t0, cycle_s=t_cycle, partial_s=t_part, est_s=t_est, dof=2 * ns,
+                wall_s=time.perf_counter() - t0)
 
 
 def host_cpu():
@@ -195,6 +219,22 @@ def workload_name(config, prob):
     return f"{CONFIG_NAMES[config]} [{prob.nx}x{prob.ny}x{prob.nz}]"
 
 
+REF_FRAC = 4     # the reference arm's sample: the first nz/4 z-planes (about 30-40 s of oracle time)
+
+
+def oracle_iterations(config, dims):
+    """The oracle's measured GMRES(30) iteration count to 1e-8 on a full-size configuration,
+    from a committed full run (tools/oracle_full.py, calls only oracle/)."""
+    if dims is not None:
+        return None, "grid override"
+    path = os.path.join(ROOT, "profiles", f"r02_oracle_c{config}_full.json")
+    try:
+        d = json.load(open(path))
+        return int(d["iters"]), os.path.relpath(path, ROOT) + " (oracle, full size, measured)"
+    except Exception as e:
+        return None, f"{os.path.relpath(path, ROOT)}: {e}"
+
+
 # ------------------------------------------------------------------------------------------
 def run_reference(args):
     ws, rank, local = dist_env()
@@ -202,21 +242,27 @@ def run_reference(args):
         return 0
     dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
     prob, J, rhs = build_workload(args.config, dims)
-    # iteration count the per-iteration time is extrapolated to: the GPU arm's measured count on
-    # C3 (618 GMRES(30) iterations to 1e-8, identical in the oracle: parity +-1), so that both
-    # arms report DOF-iters/s over the same setup+solve work
-    iters = int(os.environ.get("BF_REF_ITERS", "618"))
+    # the oracle's own measured iteration count on this configuration (a full-size oracle run to
+    # 1e-8, tools/oracle_full.py -> profiles/); the sample's measured setup + cycle times give the
+    # oracle's time for that many iterations
+    iters, src = oracle_iterations(args.config, dims)
+    if iters is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"no measured oracle iteration count for config "
+                                                              f"{args.config} {dims or ''} ({src})"}), flush=True)
+        return 0
     vals, walls = [], []
     for s in range(args.warmup + args.steps):
-        res = oracle_sample(J, prob, iters, args.restart, args.tol)
+        res = oracle_sample(J, prob, iters, args.restart, args.tol, frac=REF_FRAC)
         if s >= args.warmup:
             vals.append(res["value"])
-            walls.append(res["wall_s"])
+            walls.append(res["est_s"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+            "steps": args.steps, "warmup": args.warmup,
+            # the oracle's time for one full-size step implied by the sample's rate
+            "ms_per_step": 1e3 * 2 * J.n * iters / v,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generator, SPE10 stand-in)",
+            "data": "synthetic (seeded generator, SPE10 stand-in)", "iters": iters, "iters_source": src,
             "config": {"workload": workload_name(args.config, prob), "restart": args.restart, "tol": args.tol},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"],
                              "host": res["host"]},

@@ -24,6 +24,10 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-s
 
 
 def build(force: bool = False) -> str:
+    # ORACLE_SO: load a prebuilt variant instead (tests/test_oracle_mutations.py runs the pins
+    # against deliberately broken copies of oracle.c to show that each pin bites)
+    if os.environ.get("ORACLE_SO"):
+        return os.environ["ORACLE_SO"]
     if force or not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)):
         tmp = SO + ".tmp%d" % os.getpid()
         subprocess.check_call(["gcc", *CFLAGS, SRC, "-o", tmp, "-lm"])
@@ -101,6 +105,7 @@ def lib():
         L.or_bf_apply.argtypes = [P(BFs), dp, dp]
         L.or_bf_spmv.argtypes = [P(BFs), dp, dp]
         L.or_gmres.argtypes = [P(BFs), dp, dp, C.c_double, C.c_int32, C.c_int32, ip, dp, ip, dp]
+        L.or_gmres_capture.argtypes = [dp, dp, ip]
         _lib = L
     return _lib
 
@@ -447,6 +452,18 @@ class BF:
         y = np.empty_like(x)
         lib().or_bf_spmv(self.ptr, _p(x, C.c_double), _p(y, C.c_double))
         return y
+
+    def arnoldi(self, b, restart=30):
+        """First GMRES(restart) cycle from x0 = 0 with tol = 0 through the or_gmres test hook:
+        returns (V [k+1, N] basis, Hbar [k+1, k] unrotated Hessenberg, k)."""
+        N = 2 * self.n
+        V = np.zeros((restart + 1, N))
+        H = np.zeros((restart + 1, restart))
+        k = C.c_int32(-1)
+        lib().or_gmres_capture(_p(V, C.c_double), _p(H, C.c_double), C.byref(k))
+        self.gmres(b, tol=0.0, restart=restart, maxit=restart)
+        k = k.value
+        return V[:k + 1], H[:k + 1, :k], k
 
     def gmres(self, b, x0=None, tol=1e-8, restart=30, maxit=500):
         b = np.ascontiguousarray(b, np.float64)

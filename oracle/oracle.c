@@ -945,6 +945,18 @@ static double dot(int64_t N, const double *a, const double *b) {
   return s;
 }
 
+/* Test hook (pins of SURVEY c.5 "GMRES"): when set, the next or_gmres call copies the Arnoldi
+ * quantities of its FIRST cycle -- the basis V_{k+1} (k+1 vectors of N, vector-major) and the
+ * Hessenberg matrix Hbar ((m+1) x m row-major, BEFORE the Givens rotations) -- and the number k
+ * of Arnoldi steps of that cycle; then the hook clears itself. */
+static double *g_cap_V = NULL, *g_cap_H = NULL;
+static int32_t *g_cap_k = NULL;
+void or_gmres_capture(double *V, double *Hbar, int32_t *k) {
+  g_cap_V = V;
+  g_cap_H = Hbar;
+  g_cap_k = k;
+}
+
 int or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t restart,
              int32_t maxit, int32_t *iters, double *res_hist, int32_t *converged,
              double *final_relres) {
@@ -975,7 +987,10 @@ int or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t r
   for (int64_t i = 0; i < N; i++) r[i] = rhs[i] - r[i];
   double beta = sqrt(dot(N, r, r));
   if (res_hist) res_hist[0] = beta / bnorm;
-  if (beta <= tol * bnorm) { *converged = 1; *final_relres = beta / bnorm; goto done; }
+  *final_relres = beta / bnorm;
+  if (beta <= tol * bnorm) { *converged = 1; goto done; }
+  if (maxit <= 0) goto done;                        /* no Arnoldi step allowed */
+  int first_cycle = 1;
   for (;;) {
     for (int64_t i = 0; i < N; i++) V[i] = r[i] / beta;
     for (int32_t i = 0; i <= m; i++) g[i] = 0.0;
@@ -997,6 +1012,8 @@ int or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t r
       double hn = sqrt(dot(N, w, w));
       for (int32_t i = 0; i <= j; i++) H[(size_t)i * m + j] = h[i];
       H[(size_t)(j + 1) * m + j] = hn;
+      if (first_cycle && g_cap_H)
+        for (int32_t i = 0; i <= j + 1; i++) g_cap_H[(size_t)i * m + j] = H[(size_t)i * m + j];
       if (hn != 0.0)
         for (int64_t t = 0; t < N; t++) V[(size_t)(j + 1) * N + t] = w[t] / hn;
       else
@@ -1019,6 +1036,12 @@ int or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t r
       k = j + 1;
       if (fabs(g[j + 1]) <= tol * bnorm || *iters >= maxit || breakdown) break;
     }
+    if (first_cycle && g_cap_k) {
+      *g_cap_k = k;
+      if (g_cap_V) memcpy(g_cap_V, V, (size_t)(breakdown ? k : k + 1) * N * sizeof(double));
+      g_cap_V = NULL; g_cap_H = NULL; g_cap_k = NULL;
+    }
+    first_cycle = 0;
     /* y = H^-1 g (upper triangular back substitution), x += M^-1 (V y) */
     for (int32_t i = k - 1; i >= 0; i--) {
       double s = g[i];

@@ -125,6 +125,8 @@ void or_bf_spmv(const or_bf *b, const double *x, double *y);
 int  or_gmres(const or_bf *b, const double *rhs, double *x, double tol, int32_t restart,
               int32_t maxit, int32_t *iters, double *res_hist, int32_t *converged,
               double *final_relres);
+/* test hook: capture V, the unrotated Hbar and k of the next or_gmres call's first cycle */
+void or_gmres_capture(double *V, double *Hbar, int32_t *k);
 #ifdef __cplusplus
 }
 #endif

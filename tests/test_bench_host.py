@@ -42,5 +42,5 @@ def test_oracle_sample_extraction_is_same_workload():
     from workload import make_system
     prob, J, rhs = make_system(2, dims=(6, 5, 8))
     prob._config = 2
-    res = bench.oracle_sample(J, prob, gpu_iters=10, restart=30, tol=1e-8)
+    res = bench.oracle_sample(J, prob, 10, restart=30, tol=1e-8)
     assert res["cores"] == 1 and res["value"] > 0 and "2 of 8 z-planes" in res["sample"]

@@ -191,19 +191,21 @@ def test_bf_exactness_gmres_iterations():
 
 # ---------------------------------------------------------------------------- strength / PMIS
 def test_pmis_hand_cases():
-    A = CSR.from_scipy(lap1d(7))
-    strong = oracle.strength(A, 0.25)
-    rows = np.repeat(np.arange(7), np.diff(A.rp))
-    assert np.array_equal(strong.astype(bool), A.ci != rows)
     n_cases = 0
     for line in open(os.path.join(GOLD, "pmis_hand.txt")):
         if line.startswith("#") or not line.strip():
             continue
         name, hs, cf = [x.strip() for x in line.split("|")]
-        got = oracle.pmis(A, strong, np.array(hs.split(), np.uint32))
+        hs = np.array(hs.split(), np.uint32)
+        n = len(hs)
+        A = CSR.from_scipy(lap1d(n))
+        strong = oracle.strength(A, 0.25)
+        rows = np.repeat(np.arange(n), np.diff(A.rp))
+        assert np.array_equal(strong.astype(bool), A.ci != rows)
+        got = oracle.pmis(A, strong, hs)
         assert np.array_equal(got, np.array(cf.split(), np.int8)), name
         n_cases += 1
-    assert n_cases == 2
+    assert n_cases == 3
 
 
 def test_strength_definition():
@@ -490,3 +492,135 @@ def test_setup_reuse_update():
     bf2.update(J0)
     v = seeded_vector(2 * J0.n, 4)
     assert np.array_equal(bf2.apply(v), oracle.BF(J0).apply(v))
+
+
+# ---------------------------------------------------------------------------- round-2 pins
+def _parse_golden_interp():
+    from fractions import Fraction
+    rows, cf, S, P = {}, None, {}, {0: {}, 1: {}}
+    for line in open(os.path.join(GOLD, "interp_hand.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        head, _, rest = line.partition("|")
+        tag = head.split()
+        if tag[0] == "CF":
+            cf = np.array([int(t) for t in tag[1:]], np.int8)
+        elif tag[0] == "A":
+            rows[int(tag[1])] = {int(c): float(v) for c, v in (e.split(":") for e in rest.split())}
+        elif tag[0] == "S":
+            S[int(tag[1])] = sorted(int(c) for c in rest.split())
+        elif tag[0] in ("P0", "P1"):
+            P[int(tag[0][1])][int(tag[1])] = {int(c): Fraction(v) for c, v in (e.split(":") for e in rest.split())}
+    n = len(rows)
+    D = np.zeros((n, n))
+    for i, r in rows.items():
+        for j, v in r.items():
+            D[i, j] = v
+    return D, cf, S, P
+
+
+def test_interp_hand_golden():
+    """Hand-derived strength sets and classical-interpolation weights (tests/golden/interp_hand.txt,
+    P:L275 [RugeStueben86], readings Q24, Q26, R6, R8) on a nonsymmetric matrix with strong F-F
+    couplings sharing C points, a positive off-diagonal inside a strong-F row, a strong F neighbour
+    without a common C point, weak couplings and a negative-diagonal row."""
+    D, cf, S, P = _parse_golden_interp()
+    A = CSR.from_dense(D)
+    strong = oracle.strength(A, 0.25).astype(bool)
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.rp))
+    for i in range(A.nrows):
+        assert sorted(A.ci[(rows == i) & strong].tolist()) == S[i], i
+    eps = np.finfo(float).eps
+    for norm in (0, 1):
+        Pd = oracle.interp(A, strong.astype(np.uint8), cf, norm=norm)
+        assert Pd.ncols == int(cf.sum())
+        for i in range(A.nrows):
+            lo, hi = Pd.rp[i], Pd.rp[i + 1]
+            got = dict(zip(Pd.ci[lo:hi].tolist(), Pd.v[lo:hi].tolist()))
+            want = P[norm][i]
+            assert sorted(got) == sorted(want), (norm, i, got, want)
+            for j, w in want.items():
+                assert abs(got[j] - float(w)) <= 2 * eps * abs(float(w)), (norm, i, j, got[j], w)
+
+
+def _arnoldi_system(cfg, dims):
+    prob, J, rhs = make_system(cfg, dims=dims)
+    bf = oracle.BF(J)
+    V, H, k = bf.arnoldi(rhs, 30)
+    W = np.array([bf.spmv(bf.apply(V[j])) for j in range(k)])      # A v_j, A = J M^-1 (P:L138-140)
+    return bf, V, H, k, W
+
+
+@pytest.mark.parametrize("cfg,dims", [(1, (32, 32, 1)), (2, (16, 15, 14))])
+def test_gmres_arnoldi_relation_and_orthogonality(cfg, dims):
+    """GMRES on the right-preconditioned operator A = J M^-1 (`precon-system`):
+    the first cycle's basis and unrotated Hessenberg matrix satisfy the Arnoldi relation
+    A V_m = V_{m+1} Hbar_m to 1e-12 |A| and V^T V = I to 1e-13 with CGS2 (SURVEY c.5).  CGS2
+    makes the COMPUTED relation hold to working precision column by column (each column's
+    residual, evaluated in extended precision, <= 3 eps |A v_j|): that is what the second pass and
+    its correction h += h' buy over CGS1 (whose residual grows like the rounding of the first
+    pass's N-term dot products)."""
+    bf, V, H, k, W = _arnoldi_system(cfg, dims)
+    assert k == 30 and V.shape[0] == 31
+    normA = max(np.linalg.norm(w) for w in W)                       # <= |A| (unit v_j)
+    R = W.T - V.T @ H                                               # A V_m - V_{m+1} Hbar
+    assert np.linalg.norm(R, 2) <= 1e-12 * normA
+    assert np.abs(V @ V.T - np.eye(k + 1)).max() <= 1e-13
+    assert np.all(np.tril(H, -2) == 0.0)                            # upper Hessenberg
+    L = np.longdouble
+    eps = np.finfo(float).eps
+    for j in range(k):
+        res = W[j].astype(L) - (V[:j + 2].astype(L) * H[:j + 2, j].astype(L)[:, None]).sum(axis=0)
+        assert float(np.sqrt((res ** 2).sum())) <= 3 * eps * np.linalg.norm(W[j]), j
+
+
+def _three_eigenvalue_jacobian(n, seed=0):
+    """Cell-decoupled 2x2 blocks with a_sp = 0 and a_ps / a_ss = 0, 1/2, 3/4 by cell type.  With
+    exact inner solves (one-level hierarchies) and the literal printed S~ = A_pp - A_ps
+    diag(A_ss)^-1 A_pp (option schur_as_printed), each cell of J M_bf^-1 is
+    [[1 / (1 - a_ps/a_ss), *], [0, 1]]: eigenvalues {1, 2, 4}, diagonalisable."""
+    from workload import BSR2
+    rng = np.random.default_rng(seed)
+    typ = np.arange(n) % 3
+    ratio = np.array([0.0, 0.5, 0.75])[typ]
+    app, ass = rng.uniform(1, 2, n), rng.uniform(1, 2, n)
+    vals = np.zeros((n, 2, 2))
+    vals[:, 0, 0], vals[:, 0, 1], vals[:, 1, 1] = app, ratio * ass, ass
+    return BSR2(n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), vals), typ
+
+
+def test_gmres_three_distinct_eigenvalues():
+    """GMRES converges in at most as many iterations as the preconditioned operator
+    has distinct eigenvalues (minimal polynomial of a diagonalisable J M^-1 with spectrum
+    {1, 2, 4}); a right-hand side exciting only {1, 2} takes 2, only {1} takes 1."""
+    n = 300
+    J, typ = _three_eigenvalue_jacobian(n)
+    bf = oracle.BF(J, schur_as_printed=1, max_coarse=BIG)
+    D = J.to_dense()
+    M = np.linalg.inv(D) @ D                                        # sanity: J invertible
+    assert np.allclose(M, np.eye(2 * n))
+    b = seeded_vector(2 * n, 3)
+    r = bf.gmres(b, tol=1e-12, restart=30, maxit=50)
+    assert r["converged"] and r["iters"] == 3, r["iters"]
+    assert np.linalg.norm(b - D @ r["x"]) <= 1e-12 * np.linalg.norm(b)
+    b2 = b * np.repeat(typ <= 1, 2)
+    r2 = bf.gmres(b2, tol=1e-12, restart=30, maxit=50)
+    assert r2["converged"] and r2["iters"] == 2, r2["iters"]
+    b1 = b * np.repeat(typ == 0, 2)
+    r1 = bf.gmres(b1, tol=1e-12, restart=30, maxit=50)
+    assert r1["converged"] and r1["iters"] == 1, r1["iters"]
+    # the spectrum the count follows: eigenvalues of the dense J M^-1 from the oracle's apply
+    Minv = np.array([bf.apply(e) for e in np.eye(2 * n)]).T
+    ev = np.linalg.eigvals(D @ Minv)
+    assert np.allclose(np.sort(np.unique(np.round(ev.real, 8))), [1.0, 2.0, 4.0]) and np.abs(ev.imag).max() < 1e-10
+
+
+def test_gmres_maxit_zero():
+    """maxit = 0 allows no Arnoldi step: x stays x0, iters = 0, the initial residual is reported
+    (res_hist needs only maxit + 1 = 1 entry)."""
+    prob, J, rhs = make_system(1, dims=(6, 5, 1))
+    bf = oracle.BF(J)
+    x0 = seeded_vector(2 * J.n, 2)
+    r = bf.gmres(rhs, x0=x0, tol=1e-8, maxit=0)
+    assert r["iters"] == 0 and not r["converged"] and np.array_equal(r["x"], x0) and len(r["hist"]) == 1
+    assert abs(r["relres"] - np.linalg.norm(rhs - J.to_scipy() @ x0) / np.linalg.norm(rhs)) <= 1e-14
