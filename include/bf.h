@@ -121,11 +121,18 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *cuda_stream, b
  *   x: in = x0, out = the last iterate.
  *   tol: relative to ||rhs||_2 (P:L275 form); the Givens estimate drives the loop and
  *        the true residual is recomputed at the end of every cycle (R11).
- *   maxit: cap on Arnoldi steps summed over restarts.
+ *   restart: 1 <= restart <= 256 (BF_ERR_ARG otherwise).  The basis V and the preconditioned
+ *        basis Z take (2 restart + 1) * 2 n_cells doubles of device memory (BF_ERR_OOM if they
+ *        do not fit); bases longer than 32 vectors are orthogonalised in blocks of 32.
+ *   maxit: cap on Arnoldi steps summed over restarts, >= 0.  maxit = 0 takes no step: x stays
+ *        x0 and only the initial residual is reported.
  *   *iters: Arnoldi steps taken.  res_hist (host, may be NULL, length >= maxit+1):
  *        res_hist[0] = ||r0||/||rhs||, res_hist[k] = Givens estimate after step k.
  *   *converged: 1 if the true relative residual <= tol.  *final_true_relres: that residual.
- *   ||rhs|| == 0 gives x = 0, iters = 0, converged = 1. */
+ *   ||rhs|| == 0 gives x = 0, iters = 0, converged = 1.
+ *   BF_ERR_NONFINITE: a NaN/Inf in rhs or x0 (the message names the first entry and its cell),
+ *        or a non-finite Arnoldi coefficient / true residual during the iteration (checked every
+ *        Arnoldi step and every cycle end); x then holds the iterate of the last completed cycle. */
 bf_status bf_solve(bf_handle h, const double *rhs, double *x, double tol, int32_t restart,
                    int32_t maxit, int32_t vec_mem, int32_t *iters, double *res_hist,
                    int32_t *converged, double *final_true_relres, void *cuda_stream);

@@ -3,13 +3,14 @@
 #include <chrono>
 #include <functional>
 #include <map>
+#include <set>
+#include <algorithm>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
-#include <thread>
 
 #include "bf_internal.cuh"
 
@@ -29,23 +30,30 @@ void cuda_check(cudaError_t e, const char *what) {
 // process-wide pool of small pinned host buffers (cudaMallocHost costs milliseconds; a
 // setup+solve step must not pay it every time).  Thread-safe; one buffer per live handle.
 static std::mutex g_pin_mu;
-static std::vector<double *> g_pin_free;
+static std::multimap<size_t, double *> g_pin_free;  // size -> block
 
-double *pinned_acquire() {
-  std::lock_guard<std::mutex> lk(g_pin_mu);
-  if (!g_pin_free.empty()) {
-    double *p = g_pin_free.back();
-    g_pin_free.pop_back();
-    return p;
+double *pinned_acquire(size_t bytes, size_t *got) {
+  size_t sz = 4096;
+  while (sz < bytes) sz <<= 1;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(sz);
+    if (it != g_pin_free.end()) {
+      double *p = it->second;
+      *got = it->first;
+      g_pin_free.erase(it);
+      return p;
+    }
   }
   void *p = nullptr;
-  cuda_check(cudaMallocHost(&p, kPinnedBytes), "cudaMallocHost");
+  cuda_check(cudaMallocHost(&p, sz), "cudaMallocHost");
+  *got = sz;
   return static_cast<double *>(p);
 }
 
-void pinned_release(double *p) {
+void pinned_release(double *p, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_pin_mu);
-  g_pin_free.push_back(p);
+  g_pin_free.emplace(bytes, p);
 }
 
 // Process-wide caching device allocator.  cudaMallocAsync/cudaFreeAsync were measured to
@@ -137,10 +145,7 @@ void free_csr(bf_ctx *c, DCsr &A) {
   dfree(c, A.rp);
   dfree(c, A.ci);
   dfree(c, A.v);
-  dfree(c, A.lidx);
   dfree(c, A.dia_v);
-  dfree(c, A.ucol);
-  dfree(c, A.uoff);
   A = DCsr();
 }
 
@@ -194,6 +199,64 @@ void timer_flush(bf_ctx *c) {
   }
 }
 
+static bool env_flag(const char *name) { return getenv(name) != nullptr; }
+static double env_num(const char *name, double dflt) {
+  const char *e = getenv(name);
+  return e ? atof(e) : dflt;
+}
+
+Tuning tuning_from_env() {
+  Tuning t;
+  t.verbose = env_flag("BF_VERBOSE");
+  t.tma = !env_flag("BF_NO_TMA");
+  t.pdl = !env_flag("BF_NO_PDL");
+  t.dia = !env_flag("BF_NO_DIA");
+  t.tail = !env_flag("BF_NO_TAIL");
+  t.tail_nnz = (int64_t)env_num("BF_TAIL_NNZ", (double)t.tail_nnz);
+  t.tail_bps = std::max(1, (int)env_num("BF_TAIL_BPS", t.tail_bps));
+  t.dtail = !env_flag("BF_NO_DTAIL");
+  t.dtail_n = (int)env_num("BF_DTAIL_N", t.dtail_n);
+  t.rfuse = !env_flag("BF_NO_RFUSE");
+  t.rfuse_l0 = env_flag("BF_RFUSE_L0");
+  t.merge_fuse = !env_flag("BF_NO_MERGE_FUSE");
+  t.short_lim = env_num("BF_SHORT", t.short_lim);
+  t.short_nmin = (int64_t)env_num("BF_SHORT_N", (double)t.short_nmin);
+  t.stencil_g2 = env_num("BF_STENCIL_G2", t.stencil_g2);
+  t.tma_g_div = env_num("BF_TMA_G", t.tma_g_div);
+  t.tma_tile = env_num("BF_TMA_TILE", t.tma_tile);
+  t.tma_ctas = std::max(1, (int)env_num("BF_TMA_CTAS", t.tma_ctas));
+  t.tma_g_p = (int)env_num("BF_TMA_G_P", 0);
+  t.tma_g_r = (int)env_num("BF_TMA_G_R", 0);
+  t.spgemm = env_flag("BF_SPGEMM_ESC") ? 2 : (env_flag("BF_SPGEMM_HASH") ? 1 : 0);
+  t.ilu_ctas = std::max(1, (int)env_num("BF_ILU_CTAS", t.ilu_ctas));
+  t.ilu_pencil = env_num("BF_ILU_PENCIL", 1.0) != 0.0;
+  t.ilu_flags = env_flag("BF_ILU_FLAGS");
+  t.pencil_tk = std::max(1, (int)env_num("BF_PENCIL_TK", t.pencil_tk));
+  t.pencil_tj = (int)env_num("BF_PENCIL_TJ", 0);
+  return t;
+}
+
+int occupancy(bf_ctx *c, const void *kernel, int threads, size_t smem) {
+  auto it = c->occ_cache.find(kernel);
+  if (it != c->occ_cache.end()) return it->second;
+  int per_sm = 0;
+  BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  c->occ_cache[kernel] = per_sm;
+  return per_sm;
+}
+
+static std::mutex g_attr_mu;
+static std::set<std::pair<int, const void *>> g_attr_done;
+
+void ensure_smem_attr(const void *kernel, int bytes) {
+  int dev = 0;
+  BF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.count({dev, kernel})) return;
+  BF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_attr_done.insert({dev, kernel});
+}
+
 }  // namespace bf
 
 using namespace bf;
@@ -207,7 +270,7 @@ static void destroy_ctx(bf_ctx *c) {
   for (auto &a : c->allocs) c->pending_free.push_back(a);
   c->allocs.clear();
   bf::release_pending(c);
-  if (c->hpin) bf::pinned_release(c->hpin);
+  if (c->hpin) bf::pinned_release(c->hpin, c->hpin_bytes);
   for (auto e : c->step_ev)
     if (e) cudaEventDestroy(e);
   if (c->apply_exec) cudaGraphExecDestroy(c->apply_exec);
@@ -230,70 +293,12 @@ static void destroy_ctx(bf_ctx *c) {
   }
 
 
-// The two AMG hierarchies of a preconditioner are independent: they are built concurrently,
-// each on its own host thread and CUDA stream with a child context (its own allocation list,
-// counters and DIA offset storage), then merged into the handle.  The setup is partly
-// host-latency bound (~160 size read-backs per hierarchy at C3), so one hierarchy's host gaps
-// overlap the other's kernels.  Every value is computed by the same kernels in the same order,
-// so the hierarchies stay bit-identical to the oracle.  Opt-in (BF_CONCURRENT_SETUP=1): it
-// saves ~5 ms of the 52 ms C3 setup, but the two threads interleave their requests to the
-// caching allocator differently from step to step and occasionally force fresh cudaMallocs
-// (measured setup outliers of 60-120 ms), so the serial order is the default.
+// the two AMG hierarchies of a preconditioner, built one after the other on the handle's stream
+// (building them concurrently on two host threads was measured: ~5 ms faster on C3 but with
+// 60-120 ms setup outliers from interleaved allocator requests -- not kept)
 static void build_two_hierarchies(bf_ctx *c, int w0, const DCsr &A0, int w1, const DCsr &A1) {
-  static const bool serial = getenv("BF_CONCURRENT_SETUP") == nullptr;
-  if (serial) {
-    build_hierarchy(c, w0, A0);
-    build_hierarchy(c, w1, A1);
-    return;
-  }
-  BF_CUDA(cudaStreamSynchronize(c->stream));  // A0, A1 were produced on the handle's stream
-  int dev = 0;
-  BF_CUDA(cudaGetDevice(&dev));
-  const int w[2] = {w0, w1};
-  const DCsr *A[2] = {&A0, &A1};
-  bf_ctx kid[2];
-  std::exception_ptr err[2];
-  for (int k = 0; k < 2; k++) {
-    kid[k].opt = c->opt;
-    kid[k].n = c->n;
-    kid[k].nx = c->nx;
-    kid[k].ny = c->ny;
-    kid[k].nz = c->nz;
-    kid[k].nnzb = c->nnzb;
-    kid[k].var_order = c->var_order;
-    kid[k].block_order = c->block_order;
-    kid[k].num_sms = c->num_sms;
-    kid[k].use_tma = c->use_tma;
-    kid[k].use_pdl = c->use_pdl;
-    BF_CUDA(cudaStreamCreateWithFlags(&kid[k].stream, cudaStreamNonBlocking));
-  }
-  std::thread th[2];
-  for (int k = 0; k < 2; k++)
-    th[k] = std::thread([&, k]() {
-      try {
-        BF_CUDA(cudaSetDevice(dev));
-        build_hierarchy(&kid[k], w[k], *A[k]);
-        sync(&kid[k]);
-      } catch (...) {
-        err[k] = std::current_exception();
-      }
-    });
-  for (auto &t : th) t.join();
-  for (int k = 0; k < 2; k++) {
-    cudaStreamSynchronize(kid[k].stream);
-    c->h[w[k]] = kid[k].h[w[k]];
-    for (auto &a : kid[k].allocs) c->allocs.push_back(a);
-    for (auto &a : kid[k].pending_free) c->pending_free.push_back(a);
-    for (auto &v : kid[k].dia_offsets) c->dia_offsets.emplace_back(std::move(v));  // buffers keep their address
-    c->dev_bytes += kid[k].dev_bytes;
-    c->launches += kid[k].launches;
-    c->alloc_ms += kid[k].alloc_ms;
-    c->syncs += kid[k].syncs;
-    c->sync_ms += kid[k].sync_ms;
-    cudaStreamDestroy(kid[k].stream);
-  }
-  for (int k = 0; k < 2; k++)
-    if (err[k]) std::rethrow_exception(err[k]);
+  build_hierarchy(c, w0, A0);
+  build_hierarchy(c, w1, A1);
 }
 
 extern "C" {
@@ -349,10 +354,12 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     return BF_ERR_ARG;
   }
   try {
-    int dev = 0;
-    BF_CUDA(cudaGetDevice(&dev));
-    BF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
-    const char *verbose = getenv("BF_VERBOSE");
+    BF_CUDA(cudaGetDevice(&c->device));
+    BF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    c->tune = tuning_from_env();
+    c->use_tma = c->tune.tma;
+    c->use_pdl = c->tune.pdl;
+    const bool verbose = c->tune.verbose;
     auto t0 = std::chrono::steady_clock::now();
     auto lap = [&](const char *what) {
       if (!verbose) return;
@@ -368,8 +375,6 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     lap("ingest");
     build_split(c);
     lap("split");
-    if (getenv("BF_NO_TMA")) c->use_tma = false;
-    if (getenv("BF_NO_PDL")) c->use_pdl = false;
     const int pc = c->opt.precond;
     if (pc == 0) {  // BF (Algorithm 3): S~, the A_ps coupling, hierarchies A_ss and S~
       build_schur(c);
@@ -503,9 +508,9 @@ bf_status bf_solve(bf_handle c, const double *rhs, double *x, double tol, int32_
                    int32_t maxit, int32_t vec_mem, int32_t *iters, double *res_hist,
                    int32_t *converged, double *relres, void *stream) {
   if (!c) return BF_ERR_ARG;
-  if (!rhs || !x || !iters || !converged || !relres || restart < 1 || restart > 512 || maxit < 0 ||
+  if (!rhs || !x || !iters || !converged || !relres || restart < 1 || restart > 256 || maxit < 0 ||
       !(tol >= 0.0) || (vec_mem != 0 && vec_mem != 1)) {
-    c->err = "bf_solve: bad argument (rhs/x/iters/converged/relres non-NULL, 1 <= restart <= 512, maxit >= 0, tol >= 0, vec_mem 0|1)";
+    c->err = "bf_solve: bad argument (rhs/x/iters/converged/relres non-NULL, 1 <= restart <= 256, maxit >= 0, tol >= 0, vec_mem 0|1)";
     return BF_ERR_ARG;
   }
   BF_GUARD_BEGIN

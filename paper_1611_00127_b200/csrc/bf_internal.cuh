@@ -13,6 +13,7 @@
 
 #include <deque>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/bf.h"
@@ -26,12 +27,7 @@ struct DCsr {
   int64_t nnz = 0;
   int32_t rpt = 0, cap = 0;  // TMA tiling: rows per tile, max nonzeros per tile (0: not tiled)
   int32_t g = 1;             // lanes per row in the TMA kernel
-  int32_t stages = 2;        // TMA pipeline depth
-  int32_t nt = 256;          // TMA kernel CTA size (128 for long Galerkin rows: smaller tiles, more CTAs)
   bool short_rows = false;   // thread-per-row kernel (k_csr_short): large P / R with mean row length <= 4
-  int16_t *lidx = nullptr;   // local-index variant (k_csr_lx.cuh): per-nonzero index into its tile's U_t
-  int32_t *ucol = nullptr, *uoff = nullptr;  // concatenated U_t, tile offsets
-  int32_t ucap = 0;
   double *dia_v = nullptr;   // DIA storage of a grid-structured finest-level matrix (k_dia.cuh)
   int32_t dia_k = 0;
   int32_t *dia_off = nullptr;  // host array of dia_k offsets (kept out of the by-value kernel struct)
@@ -60,6 +56,39 @@ struct Hier {
   double *tmat = nullptr; // T (n_dtail x n_dtail, row-major): the exact linear map b -> x of that sub-V-cycle
   bool dense = false;  // coarsest level solved by LU (else 4 l1-Jacobi sweeps)
 };
+
+// Solve-path variants and tiling heuristics.  Every default is the measured choice (DESIGN.md
+// section 8b); the environment overrides (BF_NO_TMA, BF_NO_DTAIL, BF_TAIL_NNZ, ...) exist for
+// the parity tests of the path variants (tests/test_gpu_parity.py VARIANTS) and for tuning
+// experiments.  They are read ONCE per bf_setup into the handle (tuning_from_env), never cached
+// in process-wide statics, so handles are independent.  Not part of the ABI.
+struct Tuning {
+  bool verbose = false;
+  bool tma = true;          // TMA-pipelined CSR kernels (else the warp-staged k_csr)
+  bool pdl = true;          // programmatic dependent launch
+  bool dia = true;          // DIA storage of grid-structured finest-level operators and of J
+  bool tail = true;         // cooperative single-kernel V-cycle tail
+  int64_t tail_nnz = 3000;  // levels with at most this many nonzeros go to the cooperative tail
+  int tail_bps = 1;         // cooperative tail CTAs per SM
+  bool dtail = true;        // dense tail operator below dtail_n rows
+  int dtail_n = 2048;
+  bool rfuse = true;        // fused restriction R (I - beta A D) on the CSR levels
+  bool rfuse_l0 = false;    // ... also on the finest level (measured slower)
+  bool merge_fuse = true;   // S~ finest post-sweep fused with the merge
+  double short_lim = 8.0;   // thread-per-row kernel for P / R with mean row length <= short_lim ...
+  int64_t short_nmin = 65536;  // ... and at least this many rows
+  double stencil_g2 = 8.0;  // stencil rows longer than this on average get 2 lanes per row
+  double tma_g_div = 4.0;   // Galerkin rows: lanes per row ~ mean row length / tma_g_div
+  double tma_tile = 1024.0; // target nonzeros per TMA tile
+  int tma_ctas = 8;         // TMA kernel CTAs per SM (upper bound; shared memory decides)
+  int tma_g_p = 0, tma_g_r = 0;  // forced lanes per row for P / R (0: heuristic)
+  int spgemm = 0;           // 0 auto (thread-per-row, hash, ESC fallback), 1 hash, 2 ESC
+  int ilu_ctas = 4;         // generic ILU sweep CTAs per SM
+  bool ilu_pencil = true;   // pencil-wavefront ILU sweeps on grid-structured J
+  bool ilu_flags = false;   // flag-array sweeps instead of value flags (generic path)
+  int pencil_tk = 8, pencil_tj = 0;  // pencil tile (0: 128 / tk)
+};
+Tuning tuning_from_env();
 
 struct Timer {
   double ms = 0.0;
@@ -114,6 +143,8 @@ struct bf_ctx {
   double *red = nullptr;        // reduction partials
   double *hdev = nullptr;       // reduced coefficients (device)
   double *hpin = nullptr;       // pinned host mirror
+  size_t hpin_bytes = 0;
+  unsigned long long *nonfinite = nullptr;  // first non-finite index (error reporting)
   unsigned int *counter = nullptr;
   cudaEvent_t step_ev[2] = {nullptr, nullptr};  // per-Arnoldi-step completion (pipelined GMRES)
   int red_blocks = 0;
@@ -137,8 +168,11 @@ struct bf_ctx {
   std::vector<PatchNode> apply_patch;
   int64_t apply_graph_kernels = 0;
   int num_sms = 148;
+  int device = 0;
+  bf::Tuning tune;      // solve-path variants / heuristics, read once at bf_setup
   bool use_tma = true;
   bool use_pdl = true;  // programmatic dependent launch for the TMA CSR kernels
+  std::unordered_map<const void *, int> occ_cache;  // resident CTAs per SM of a kernel (this device)
   std::deque<std::vector<int32_t>> dia_offsets;  // storage behind DCsr::dia_off
   double alloc_ms = 0.0;
   double alg_bytes = 0.0;       // running algorithmic-bytes counter (csr_op, vector kernels)
@@ -161,9 +195,9 @@ T *dalloc_t(bf_ctx *c, size_t count) {
   return static_cast<T *>(dalloc(c, count * sizeof(T) + 16));
 }
 void free_csr(bf_ctx *c, DCsr &A);
-constexpr size_t kPinnedBytes = 4096;
-double *pinned_acquire();
-void pinned_release(double *p);
+// pinned host buffers of at least `bytes` (pooled process-wide; *got = the block's size)
+double *pinned_acquire(size_t bytes, size_t *got);
+void pinned_release(double *p, size_t bytes);
 void timer_begin(bf_ctx *c, int k, cudaEvent_t *start);
 void timer_end(bf_ctx *c, int k, cudaEvent_t start, double alg_bytes = 0.0);
 void timer_flush(bf_ctx *c);
@@ -193,7 +227,6 @@ void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vc
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
 double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
-void setup_lx(bf_ctx *c, DCsr &A);                                      // k_vcycle.cu
 void setup_dia(bf_ctx *c, DCsr &A);                                     // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------
@@ -215,6 +248,13 @@ bool cpr_patch_roles(const void *func, int &nargs, std::vector<std::pair<int, in
 void ilu_solve_into(bf_ctx *c, const double *r, double *x);              // x = (LU)^-1 r, caller order
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int restart, int maxit,
            int *iters, double *hist, int *converged, double *relres);   // k_gmres.cu
+
+// resident CTAs per SM of `kernel` at `threads` threads and `smem` dynamic shared memory on the
+// handle's device (cached in the handle)
+int occupancy(bf_ctx *c, const void *kernel, int threads, size_t smem);
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `kernel` raised to `bytes` on the current
+// device (once per kernel and device; thread-safe)
+void ensure_smem_attr(const void *kernel, int bytes);
 
 // number of parameters of a kernel (graph-node argument patching, k_vcycle.cu)
 template <typename... A>

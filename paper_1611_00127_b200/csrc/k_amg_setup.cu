@@ -771,11 +771,11 @@ static void spgemm_esc(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
 static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
 
 static void spgemm(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
-  if (getenv("BF_SPGEMM_ESC")) {
+  if (c->tune.spgemm == 2) {
     spgemm_esc(c, A, B, C);
     return;
   }
-  if (B.n > 0 && (double)B.nnz / B.n <= 6.0 && A.n > 0 && (double)A.nnz / A.n <= 30.0 && !getenv("BF_SPGEMM_HASH")) {
+  if (B.n > 0 && (double)B.nnz / B.n <= 6.0 && A.n > 0 && (double)A.nnz / A.n <= 30.0 && c->tune.spgemm != 1) {
     C.n = A.n;
     C.m = B.m;
     int32_t *cnt = dalloc_t<int32_t>(c, A.n);
@@ -828,12 +828,7 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   dfree(c, cnt);
   C.ci = dalloc_t<int32_t>(c, C.nnz);
   C.v = dalloc_t<double>(c, C.nnz);
-  static bool attr = false;
-  if (!attr) {
-    BF_CUDA(cudaFuncSetAttribute(k_spgemm_hash_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 HASH_WARPS * HASH_WARP_BYTES));
-    attr = true;
-  }
+  ensure_smem_attr((const void *)k_spgemm_hash_fill, HASH_WARPS * HASH_WARP_BYTES);
   k_spgemm_hash_fill<<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES, c->stream>>>(A, B, C);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
@@ -994,7 +989,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   copy_csr(c, A0, h.lv[0].A);
   int l = 0;
   int *nU_d = dalloc_t<int>(c, 4);
-  const bool verbose = getenv("BF_VERBOSE") != nullptr;
+  const bool verbose = c->tune.verbose;
   auto tnow = [&]() {
     if (verbose) sync(c);
     return std::chrono::steady_clock::now();
@@ -1026,12 +1021,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     uint8_t *notmax = dalloc_t<uint8_t>(c, n);
     uint8_t *cnew = dalloc_t<uint8_t>(c, n);
     {
-      static int coop_blocks = 0;
-      if (!coop_blocks) {
-        int per_sm = 0;
-        BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pmis_coop, 256, 0));
-        coop_blocks = std::max(1, per_sm) * c->num_sms;
-      }
+      const int coop_blocks = std::max(1, occupancy(c, (const void *)k_pmis_coop, 256, 0)) * c->num_sms;
       int grid = std::max(1, std::min(coop_blocks, div_up(n, 256)));
       int max_rounds = n + 1;  // each round decides at least the undecided point of largest key
       int *rounds_d = nU_d + 2;
@@ -1137,13 +1127,9 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     L.t = dalloc_t<double>(c, n);
     tile_csr(c, L.A, k == 0);
     if (k == 0) setup_dia(c, L.A);
-    if (k > 0) setup_lx(c, L.A);
     if (k < h.nlev - 1) {
-      const char *gp = getenv("BF_TMA_G_P"), *gr = getenv("BF_TMA_G_R");
-      tile_csr(c, L.P, false, gp ? atoi(gp) : 0);
-      tile_csr(c, L.R, false, gr ? atoi(gr) : 0);
-      setup_lx(c, L.P);
-      setup_lx(c, L.R);
+      tile_csr(c, L.P, false, c->tune.tma_g_p);
+      tile_csr(c, L.R, false, c->tune.tma_g_r);
     }
   }
   BF_CUDA(cudaGetLastError());
@@ -1197,8 +1183,8 @@ static __global__ void k_rfuse_m(DCsr A, const double *__restrict__ d, double be
 
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
   const bf_options &o = c->opt;
-  if (getenv("BF_NO_RFUSE") || o.smoother != 0 || o.nu_pre != 1) return;
-  const bool l0 = getenv("BF_RFUSE_L0") != nullptr;
+  if (!c->tune.rfuse || o.smoother != 0 || o.nu_pre != 1) return;
+  const bool l0 = c->tune.rfuse_l0;
   int lend = h.dtail >= 0 ? h.dtail : (h.tail >= 0 ? h.tail : h.nlev - 1);
   for (int l = l0 ? 0 : 1; l < lend; l++) {
     if (finest_only && l > 0) break;
@@ -1218,7 +1204,7 @@ void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
     spgemm(c, L.R, M, L.Rf);
     dfree(c, M.v);
     tile_csr(c, L.Rf, false);
-    if (getenv("BF_VERBOSE")) {
+    if (c->tune.verbose) {
       sync(c);
       fprintf(stderr, "[bf_setup]   rfuse L%d: R %lld nnz x M %lld nnz -> %lld nnz, %.2f ms\n", l, (long long)L.R.nnz,
               (long long)L.A.nnz, (long long)L.Rf.nnz,

@@ -18,8 +18,7 @@
 namespace bf {
 
 constexpr int TMA_THREADS = 256;
-constexpr int TMA_STAGES = 2;      // stages of the tiling heuristic's smem budget
-constexpr int TMA_MAX_STAGES = 4;
+constexpr int TMA_STAGES = 2;      // TMA pipeline depth (and the tiling heuristic's smem budget)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -80,7 +79,7 @@ __global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int 
                                                          const double *__restrict__ b,
                                                          const double *__restrict__ dinv, double *__restrict__ y,
                                                          double *__restrict__ aux, double alpha, double beta,
-                                                         const double *__restrict__ dir, int contig) {
+                                                         const double *__restrict__ dir) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[ST];
   const int stage_bytes = tma_stage_bytes(cap, rpt);
@@ -109,18 +108,10 @@ __global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int 
     if (bv) tma_bulk_g2s(base + cb, v + v0, bv, &bars[s], pol);
   };
 
-  // tiles of this CTA: a contiguous range (consecutive tiles share most of their x window, so
-  // the gathers hit L1) or, with contig = 0, every gridDim.x-th tile
-  int t, t_end, stride;
-  if (contig) {
-    t = (int)(((int64_t)blockIdx.x * ntiles) / gridDim.x);
-    t_end = (int)(((int64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
-    stride = 1;
-  } else {
-    t = blockIdx.x;
-    t_end = ntiles;
-    stride = gridDim.x;
-  }
+  // tiles of this CTA: every gridDim.x-th tile (contiguous tile ranges per CTA, for L1 reuse of
+  // the x window, measured 1.3 % slower on C3)
+  int t = blockIdx.x;
+  const int t_end = ntiles, stride = gridDim.x;
   if (t >= t_end) {
     pdl_wait();
     return;
@@ -217,19 +208,10 @@ static __global__ void k_tile_max(int n, int rpt, const int32_t *__restrict__ rp
 template <int MODE, int G, int ST, int NT>
 void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                        double *aux, double alpha, double beta, const double *dir) {
-  static bool configured = false;
-  if (!configured) {
-    BF_CUDA(cudaFuncSetAttribute(k_csr_tma<MODE, G, ST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
+  ensure_smem_attr((const void *)k_csr_tma<MODE, G, ST, NT>, 200 * 1024);
   int smem = ST * tma_stage_bytes(A.cap, A.rpt);
   int ntiles = (A.n + A.rpt - 1) / A.rpt;
-  static int max_per_sm = 0;
-  if (!max_per_sm) {
-    const char *e = getenv("BF_TMA_CTAS");
-    max_per_sm = e ? std::max(1, atoi(e)) : 8;
-  }
-  int per_sm = std::max(1, std::min(max_per_sm * (TMA_THREADS / NT), (220 * 1024) / (smem + 1024)));
+  int per_sm = std::max(1, std::min(c->tune.tma_ctas * (TMA_THREADS / NT), (220 * 1024) / (smem + 1024)));
   int grid = std::min(ntiles, c->num_sms * per_sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -241,38 +223,22 @@ void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *
   attr[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static int contig = -1;
-  if (contig < 0) {
-    const char *e = getenv("BF_TMA_CONTIG");
-    contig = e ? atoi(e) : 0;  // contiguous ranges measured 1.3 % slower on C3 (opt-in)
-  }
   BF_CUDA(cudaLaunchKernelEx(&cfg, k_csr_tma<MODE, G, ST, NT>, A.n, A.rpt, ntiles, A.cap, (const int32_t *)A.rp,
-                             (const int32_t *)A.ci, (const double *)A.v, x, b, dinv, y, aux, alpha, beta, dir, contig));
+                             (const int32_t *)A.ci, (const double *)A.v, x, b, dinv, y, aux, alpha, beta, dir));
 }
 
+// two stages and 256-thread CTAs (3-4 stages and 128-thread CTAs for long rows were measured
+// slower on C3)
 template <int MODE, int G>
 void launch_csr_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                     double *aux, double alpha, double beta, const double *dir) {
-  if (A.nt == 128 && G <= 32) {  // long Galerkin rows: 128-thread CTAs, 2 stages
-    launch_csr_tma_st<MODE, G, 2, 128>(c, A, x, b, dinv, y, aux, alpha, beta, dir);
-    return;
-  }
-  switch (A.stages) {
-    case 3: launch_csr_tma_st<MODE, G, 3, TMA_THREADS>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 4: launch_csr_tma_st<MODE, G, 4, TMA_THREADS>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    default: launch_csr_tma_st<MODE, G, 2, TMA_THREADS>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-  }
+  launch_csr_tma_st<MODE, G, TMA_STAGES, TMA_THREADS>(c, A, x, b, dinv, y, aux, alpha, beta, dir);
 }
-
-template <int MODE>
-bool csr_op_lx(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
-               double *aux, double alpha, double beta, const double *dir);
 
 template <int MODE>
 bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir) {
   if (A.cap <= 0) return false;
-  if (csr_op_lx<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return true;
   switch (A.g) {
     case 1: launch_csr_tma<MODE, 1>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
     case 2: launch_csr_tma<MODE, 2>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
@@ -288,5 +254,3 @@ bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, cons
 }
 
 }  // namespace bf
-
-#include "k_csr_lx.cuh"

