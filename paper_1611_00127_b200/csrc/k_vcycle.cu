@@ -42,13 +42,21 @@ struct TailLevel {
   int n, gA, gP, gR;
   const int32_t *Arp, *Aci, *Prp, *Pci, *Rrp, *Rci;
   const double *Av, *Pv, *Rv, *d;
-  double *b, *x, *r, *t;
+  double *b, *x, *r, *t, *dir;
+};
+// smoothing recurrence of one pass (the same for every level of the tail): l1-Jacobi is the
+// degree-1 case c0 = 1; Chebyshev of degree m: first step x += c0 D (b - A x), dir = that step;
+// steps k = 1..m-1: dir = ca[k] dir + cb[k] D (b - A x), x += dir (smooth_pass below)
+struct TailSmoother {
+  int deg, nu_pre, nu_post;
+  double c0, ca[8], cb[8];
 };
 struct TailParams {
   int nl;  // tail levels including the coarsest
   int gL;  // lanes per row of the dense coarse solve
   double beta;
   const double *inv;
+  TailSmoother sm;
   TailLevel lv[TAIL_MAXL];
 };
 
@@ -167,28 +175,52 @@ constexpr int DTAIL_N = 2048;
 constexpr int DTAIL_THREADS = 256;
 
 // one CTA per column `col` of T; per-column level vectors are the TailParams buffers offset by
-// col * n_k (allocated [n0 columns][n_k] per level by build_dense_tail)
+// col * n_k (allocated [n0 columns][n_k] per level by build_dense_tail).  Runs exactly the
+// V(nu_pre, nu_post) cycle of vcycle_level below the first tail level -- smoothing passes from
+// zero, residual, restriction, recursion, exact coarse solve, prolongation, post-smoothing --
+// on the unit vector e_col, for either smoother (any fixed smoother makes the cycle linear).
 __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, double *__restrict__ T) {
   const int col = blockIdx.x, n0 = p.lv[0].n;
   const int tid = threadIdx.x, nth = blockDim.x;
-  auto vb = [&](int k) { return p.lv[k].b + (size_t)col * p.lv[k].n; };
-  auto vx = [&](int k) { return p.lv[k].x + (size_t)col * p.lv[k].n; };
-  auto vr = [&](int k) { return p.lv[k].r + (size_t)col * p.lv[k].n; };
-  auto vt = [&](int k) { return p.lv[k].t + (size_t)col * p.lv[k].n; };
-  {  // b_0 = e_col, x_0 = beta b_0 ./ dl1_0 (the seeded pre-sweep)
-    double *b = vb(0), *x = vx(0);
-    for (int i = tid; i < n0; i += nth) {
-      double bi = i == col ? 1.0 : 0.0;
-      b[i] = bi;
-      x[i] = p.beta * (bi * p.lv[0].d[i]);
+  const TailSmoother &sm = p.sm;
+  auto off = [&](int k) { return (size_t)col * p.lv[k].n; };
+  // t = A x (all rows), then the pointwise smoothing update of step `step` of a pass
+  auto smooth_step = [&](int k, int step, bool from_zero) {
+    const TailLevel &L = p.lv[k];
+    double *b = L.b + off(k), *x = L.x + off(k), *t = L.t + off(k), *dir = L.dir + off(k);
+    if (!from_zero) {
+      int g = L.gA, lig = tid & (g - 1);
+      for (int base = 0; base < L.n; base += nth / g) {
+        int i = base + tid / g;
+        bool ok = i < L.n;
+        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
+        if (ok && lig == 0) t[i] = s;
+      }
+      __syncthreads();
     }
-  }
+    for (int i = tid; i < L.n; i += nth) {
+      double res = (b[i] - (from_zero ? 0.0 : t[i])) * L.d[i];
+      double dn = step == 0 ? sm.c0 * res : sm.ca[step] * dir[i] + sm.cb[step] * res;
+      dir[i] = dn;
+      x[i] = (from_zero ? 0.0 : x[i]) + dn;
+    }
+    __syncthreads();
+  };
+  auto smooth_pass = [&](int k, bool from_zero) {
+    for (int step = 0; step < sm.deg; step++) smooth_step(k, step, from_zero && step == 0);
+  };
+  for (int i = tid; i < n0; i += nth) p.lv[0].b[off(0) + i] = i == col ? 1.0 : 0.0;
   __syncthreads();
   for (int l = 0; l < p.nl - 1; l++) {
     const TailLevel &L = p.lv[l];
     const TailLevel &C = p.lv[l + 1];
-    {  // r = b - A x0
-      double *b = vb(l), *x = vx(l), *r = vr(l);
+    double *b = L.b + off(l), *x = L.x + off(l), *r = L.r + off(l);
+    if (sm.nu_pre == 0) {
+      for (int i = tid; i < L.n; i += nth) x[i] = 0.0;
+      __syncthreads();
+    }
+    for (int s = 0; s < sm.nu_pre; s++) smooth_pass(l, s == 0);
+    {  // r = b - A x
       int g = L.gA, lig = tid & (g - 1);
       for (int base = 0; base < L.n; base += nth / g) {
         int i = base + tid / g;
@@ -198,24 +230,21 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       }
     }
     __syncthreads();
-    {  // b_c = R r ; x0_c = beta b_c ./ dl1_c
-      double *r = vr(l), *bc = vb(l + 1), *xc = vx(l + 1);
+    {  // b_c = R r
+      double *bc = C.b + off(l + 1);
       int g = L.gR, lig = tid & (g - 1);
       for (int base = 0; base < C.n; base += nth / g) {
         int i = base + tid / g;
         bool ok = i < C.n;
         double s = group_row(L.Rrp, L.Rci, L.Rv, r, i, ok, lig, g);
-        if (ok && lig == 0) {
-          bc[i] = s;
-          xc[i] = p.beta * (s * C.d[i]);
-        }
+        if (ok && lig == 0) bc[i] = s;
       }
     }
     __syncthreads();
   }
   {  // coarsest: x = A_L^-1 b
     const TailLevel &L = p.lv[p.nl - 1];
-    double *b = vb(p.nl - 1), *x = vx(p.nl - 1);
+    double *b = L.b + off(p.nl - 1), *x = L.x + off(p.nl - 1);
     for (int i = tid; i < L.n; i += nth) {
       double s = 0.0;
       for (int j = 0; j < L.n; j++) s += p.inv[(size_t)i * L.n + j] * b[j];
@@ -225,8 +254,8 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
   __syncthreads();
   for (int l = p.nl - 2; l >= 0; l--) {
     const TailLevel &L = p.lv[l];
-    const double *e = (l + 1 == p.nl - 1) ? vx(l + 1) : vt(l + 1);
-    double *b = vb(l), *x = vx(l), *t = vt(l);
+    const double *e = p.lv[l + 1].x + off(l + 1);
+    double *x = L.x + off(l);
     {  // x += P e
       int g = L.gP, lig = tid & (g - 1);
       for (int base = 0; base < L.n; base += nth / g) {
@@ -237,19 +266,33 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       }
     }
     __syncthreads();
-    {  // t = x + (b - A x) ./ dl1
-      int g = L.gA, lig = tid & (g - 1);
-      for (int base = 0; base < L.n; base += nth / g) {
-        int i = base + tid / g;
-        bool ok = i < L.n;
-        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
-        if (ok && lig == 0) t[i] = x[i] + (b[i] - s) * L.d[i];
-      }
-    }
-    __syncthreads();
+    for (int s = 0; s < sm.nu_post; s++) smooth_pass(l, false);
   }
-  const double *t0 = vt(0);
-  for (int i = tid; i < n0; i += nth) T[(size_t)i * n0 + col] = t0[i];
+  const double *x0 = p.lv[0].x + off(0);
+  for (int i = tid; i < n0; i += nth) T[(size_t)i * n0 + col] = x0[i];
+}
+
+// the smoothing recurrence of one pass (see TailSmoother)
+static TailSmoother tail_smoother(const bf_options &o) {
+  TailSmoother sm{};
+  sm.nu_pre = o.nu_pre;
+  sm.nu_post = o.nu_post;
+  if (o.smoother == 0) {
+    sm.deg = 1;
+    sm.c0 = 1.0;
+    return sm;
+  }
+  double lo = o.cheb_lo, theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0, sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  sm.deg = o.cheb_degree;
+  sm.c0 = 1.0 / theta;
+  for (int k = 1; k < o.cheb_degree; k++) {
+    double rho_new = 1.0 / (2.0 * sigma - rho);
+    sm.ca[k] = rho_new * rho;
+    sm.cb[k] = 2.0 * rho_new / delta;
+    rho = rho_new;
+  }
+  return sm;
 }
 
 // x = T b: DTAIL_SPLIT warps per row of T (each a contiguous quarter of the row, 8 loads in
@@ -295,7 +338,7 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
   dfree(c, h.tmat);
   h.tmat = nullptr;
   h.dtail = -1;
-  if (!c->tune.dtail || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  if (!c->tune.dtail || !h.dense) return;
   int lim = std::min(c->tune.dtail_n, DTAIL_N);
   int lt = -1;
   for (int l = 1; l < h.nlev - 1; l++)
@@ -309,6 +352,7 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
   p.nl = h.nlev - lt;
   p.beta = 1.0;
   p.inv = h.inv;
+  p.sm = tail_smoother(o);
   std::vector<double *> bufs;
   for (int k = 0; k < p.nl; k++) {
     Level &L = h.lv[lt + k];
@@ -327,12 +371,13 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
     Tl.Rci = L.R.ci;
     Tl.Rv = L.R.v;
     Tl.d = L.d;
-    double *w = dalloc_t<double>(c, (size_t)4 * n0 * L.A.n);  // [b | x | r | t] x n0 columns
+    double *w = dalloc_t<double>(c, (size_t)5 * n0 * L.A.n);  // [b | x | r | t | dir] x n0 columns
     bufs.push_back(w);
     Tl.b = w;
     Tl.x = w + (size_t)n0 * L.A.n;
     Tl.r = w + (size_t)2 * n0 * L.A.n;
     Tl.t = w + (size_t)3 * n0 * L.A.n;
+    Tl.dir = w + (size_t)4 * n0 * L.A.n;
   }
   h.tmat = dalloc_t<double>(c, (size_t)n0 * n0);
   k_tail_columns<<<n0, DTAIL_THREADS, 0, c->stream>>>(p, h.tmat);
@@ -528,7 +573,6 @@ static double x0_beta(const bf_options &o) {
 // want_resid: leave r = b - A x in L.r.
 static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool first, bool want_resid) {
   const bf_options &o = c->opt;
-  int n = L.A.n;
   auto swap_t = [&]() {
     double *tmp = x;
     x = L.t;
@@ -543,16 +587,20 @@ static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool first, bool want_r
     double lo = o.cheb_lo, theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0, sigma = theta / delta;
     double rho = 1.0 / sigma;
     double *dir = L.r;  // direction storage (r is recomputed below when needed)
+    // the first step's direction is the step itself: after a seeded first step (x = x0 from
+    // zero) that is x0, read in place (no copy into dir)
+    const double *dir_in = dir;
     if (first) {
-      BF_CUDA(cudaMemcpyAsync(dir, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      dir_in = x;
     } else {
       csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, dir, 0.0, 1.0 / theta, nullptr);
       swap_t();
     }
     for (int k = 1; k < o.cheb_degree; k++) {
       double rho_new = 1.0 / (2.0 * sigma - rho);
-      csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, dir, rho_new * rho, 2.0 * rho_new / delta, dir);
+      csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, dir, rho_new * rho, 2.0 * rho_new / delta, dir_in);
       swap_t();
+      dir_in = dir;
       rho = rho_new;
     }
   }

@@ -1,6 +1,6 @@
 """Full-size oracle run to convergence (test infrastructure: calls only oracle/ and workload/).
 
-    python tools/oracle_full.py --config 3 [--out profiles/r02_oracle_c3_full.json]
+    python tests/scripts/oracle_full.py --config 3 [--out profiles/r02_oracle_c3_full.json]
 
 Times the CPU oracle (plain C, 1 thread) on the whole BASELINE.json configuration: bf_setup
 equivalent (split, S~, both AMG hierarchies) and GMRES(30) to 1e-8 from x0 = 0, and records the
@@ -14,7 +14,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
@@ -49,7 +49,8 @@ rec = {"config": a.config, "dims": list(prob.dims), "dof": N, "impl": "oracle (p
 print(json.dumps({k: v for k, v in rec.items() if k != "hist_every_30"}), flush=True)
 for frac in (int(f) for f in a.fracs.split(",")):
     s = bench.oracle_sample(J, prob, r["iters"], 30, 1e-8, frac=frac)
-    rec["samples"].append({"frac": frac, "value": s["value"], "ratio_to_full": s["value"] / rec["value_dof_iters_per_s"],
+    rec["samples"].append({"frac": frac, "value_raw": s["raw_value"], "method": bench.SAMPLE_METHOD,
+                           "ratio_to_full": s["raw_value"] / rec["value_dof_iters_per_s"],
                            "sample": s["sample"], "wall_s": s["wall_s"], "setup_s": s["setup_s"],
                            "cycle_s": s["cycle_s"], "partial_s": s["partial_s"]})
     print(json.dumps(rec["samples"][-1]), flush=True)

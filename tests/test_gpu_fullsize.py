@@ -114,6 +114,8 @@ def test_c5_full_size_sampled():
             assert pat and val, (which, l)
             if l < o.nlev(which) - 1:
                 assert np.array_equal(G["cf"], O["cf"]), (which, l)
+                pat, val = csr_equal(G["P"], O["P"])
+                assert pat and val, ("P", which, l)
             del G, O
     lap("hierarchies compared")
     x = seeded_vector(2 * J.n, 55)
@@ -130,3 +132,93 @@ def test_c5_full_size_sampled():
     lap("gpu gmres")
     for f in (0, 1):
         assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+
+
+def _hierarchies_bit_exact(g, o, whiches=(0, 1)):
+    for which in whiches:
+        assert g.num_levels(which) == o.nlev(which)
+        for l in range(o.nlev(which)):
+            G, O = g.level(which, l), o.level(which, l)
+            pat, val = csr_equal(G["A"], O["A"])
+            assert pat and val, ("A", which, l)
+            assert np.array_equal(G["dl1"].view(np.uint64), O["dl1"].view(np.uint64)), ("dl1", which, l)
+            if l < o.nlev(which) - 1:
+                assert np.array_equal(G["cf"], O["cf"]), ("cf", which, l)
+                pat, val = csr_equal(G["P"], O["P"])
+                assert pat and val, ("P", which, l)
+
+
+def _forced(g, o, rhs, k, restart=30):
+    ro = o.gmres(rhs, tol=0.0, restart=restart, maxit=k)
+    x = torch.zeros(rhs.shape[0], dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=0.0, restart=restart, maxit=k)
+    assert r["iters"] == ro["iters"] == k
+    xg = x.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+    assert np.allclose(r["hist"], ro["hist"], rtol=1e-6, atol=0)
+
+
+def test_c2_full_size_to_convergence():
+    """C2 (64^3, 524,288 DOF) at full size, GMRES(30) to 1e-8 from x0 = 0 on both sides: the
+    iteration counts agree within 1 and each field of the solution within 1e-6 (BASELINE.json
+    north_star tolerances, Q33), and the true residual meets the tolerance."""
+    prob, J, rhs = make_system(2)
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    _hierarchies_bit_exact(g, o)
+    ro = o.gmres(rhs, tol=1e-8, restart=30, maxit=1000)
+    x = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
+    r = g.solve(torch_dev(rhs), x, tol=1e-8, restart=30, maxit=1000)
+    assert ro["converged"] and r["converged"]
+    assert abs(r["iters"] - ro["iters"]) <= 1, (r["iters"], ro["iters"])
+    xg = x.cpu().numpy()
+    for f in (0, 1):
+        assert np.linalg.norm(xg[f::2] - ro["x"][f::2]) <= 1e-6 * np.linalg.norm(ro["x"][f::2])
+    assert np.linalg.norm(rhs - o.spmv(xg)) <= 1e-8 * np.linalg.norm(rhs)
+
+
+def test_c4_full_size():
+    """C4 (128^3 layered high-contrast, strong capillarity: the hard gate configuration): split,
+    S~ and both hierarchies bit-exact on every level, SpMV <= 1e-12, BF apply <= 1e-10 and 30
+    forced GMRES iterations <= 1e-6 per field against the oracle."""
+    prob, J, rhs = make_system(4)
+    g = gpu_solver(J, prob.dims)
+    o = oracle.BF(J)
+    for k, name in enumerate(("App", "Aps", "Asp", "Ass", "S")):
+        pat, val = csr_equal(g.block(k), o.matrix(name))
+        assert pat and val, name
+    _hierarchies_bit_exact(g, o)
+    N = 2 * J.n
+    x = seeded_vector(N, 41)
+    y = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.spmv(torch_dev(x), y)
+    yo = o.spmv(x)
+    assert np.linalg.norm(y.cpu().numpy() - yo) <= 1e-12 * np.linalg.norm(yo)
+    z = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(x), z)
+    zo = o.apply(x)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+    _forced(g, o, rhs, 30)
+
+
+def test_c3_chebyshev_full_size(c3):
+    """The Chebyshev(2) smoother on [0.1, 1] (option smoother=1, reading R9) at full C3 size:
+    hierarchies bit-exact, one BF apply <= 1e-10 and 30 forced GMRES iterations <= 1e-6."""
+    prob, J, rhs, g0, o0 = c3
+    opts = dict(smoother=1, cheb_lo=0.1)
+    g = gpu_solver(J, prob.dims, **opts)
+    o = oracle.BF(J, **opts)
+    N = 2 * J.n
+    x = seeded_vector(N, 43)
+    z = torch.empty(N, dtype=torch.float64, device="cuda")
+    g.apply_precond(torch_dev(x), z)
+    zo = o.apply(x)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+    for which in (0, 1):
+        b = seeded_vector(J.n, 44 + which)
+        xv = torch.empty(J.n, dtype=torch.float64, device="cuda")
+        g.vcycle(which, torch_dev(b), xv)
+        xo = o.vcycle(which, b)
+        assert np.linalg.norm(xv.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo)
+    _forced(g, o, rhs, 30)

@@ -624,3 +624,42 @@ def test_gmres_maxit_zero():
     r = bf.gmres(rhs, x0=x0, tol=1e-8, maxit=0)
     assert r["iters"] == 0 and not r["converged"] and np.array_equal(r["x"], x0) and len(r["hist"]) == 1
     assert abs(r["relres"] - np.linalg.norm(rhs - J.to_scipy() @ x0) / np.linalg.norm(rhs)) <= 1e-14
+
+
+# ---------------------------------------------------------------------------- NEXT-4: exact spectra
+def _dense_minv(bf, N):
+    return np.array([bf.apply(e) for e in np.eye(N)]).T
+
+
+def test_spectrum_exact_inner_solves():
+    """The paper's eigenvalue study forms M^-1 with EXACT inner solves (footnote
+    P:L494: Matlab backslash for A_11, A_22 and the modified Schur complement).  The oracle does
+    that with one-level hierarchies (max_coarse >= n: dense LU).  Pins ("dense
+    spectrum of J M^-1 with M exact returns all eigenvalues equal to 1 within 1e-8"):
+      * A_sp = 0: M_bf = J exactly, so every eigenvalue of J M^-1 is 1 (to 1e-10);
+      * A_ss diagonal: S~ = S, J M^-1 = M L3 M^-1 with (L3 - I)^2 = 0, all
+        eigenvalues 1 (defective: a perturbation of size sqrt(eps) is allowed, <= 1e-6);
+      * the general two-phase Jacobian: the spectrum of J M^-1 equals that of the dense
+        J M_bf^-1 of P:L252-257 formed independently from the blocks."""
+    prob, J, rhs = tiny_system((8, 5, 1), config=1)
+    n, N = J.n, 2 * J.n
+    D = J.to_dense()
+    App, Aps, Asp, Ass = D[0::2, 0::2], D[0::2, 1::2], D[1::2, 0::2], D[1::2, 1::2]
+    J0 = bsr_from_dense_blocks(App, Aps, np.zeros_like(Asp), Ass)
+    lam = np.linalg.eigvals(J0.to_dense() @ _dense_minv(oracle.BF(J0, max_coarse=BIG), N))
+    assert np.abs(lam - 1).max() <= 1e-10
+    Jd = bsr_from_dense_blocks(App, Aps, Asp, np.diag(np.diag(Ass)))
+    lam = np.linalg.eigvals(Jd.to_dense() @ _dense_minv(oracle.BF(Jd, max_coarse=BIG), N))
+    assert np.abs(lam - 1).max() <= 1e-6
+    bf = oracle.BF(J, max_coarse=BIG)
+    assert bf.nlev(0) == 1 and bf.nlev(1) == 1
+    lam = np.sort_complex(np.linalg.eigvals(D @ _dense_minv(bf, N)))
+    St = App - Aps @ np.diag(1 / np.diag(Ass)) @ Asp
+    Si, Ai = np.linalg.inv(St), np.linalg.inv(Ass)
+    Mbf = np.block([[Si, -Si @ Aps @ Ai], [np.zeros((n, n)), Ai]])
+    perm = np.concatenate([np.arange(0, N, 2), np.arange(1, N, 2)])
+    Jv = D[np.ix_(perm, perm)]
+    ref = np.sort_complex(np.linalg.eigvals(Jv @ Mbf))
+    assert np.abs(lam - ref).max() <= 1e-8 * np.abs(ref).max()
+    # BF keeps the spectrum away from the origin (P:L503-507)
+    assert np.abs(lam).min() > 0.05

@@ -16,6 +16,9 @@ p.add_argument("--config", type=int, default=3)
 p.add_argument("--dims", type=str, default=None)
 p.add_argument("--maxit", type=int, default=1500)
 p.add_argument("--sets", type=str, default="all")
+p.add_argument("--opts", type=str, default=None,
+               help="';'-separated option sets, e.g. 'smoother=1,cheb_lo=0.1;nu_pre=2,nu_post=2'")
+p.add_argument("--restart", type=int, default=30)
 a = p.parse_args()
 dims = tuple(int(x) for x in a.dims.split(",")) if a.dims else None
 prob, J, rhs = make_system(a.config, dims=dims)
@@ -26,6 +29,10 @@ SETS = [dict(), dict(nu_pre=2, nu_post=2), dict(smoother=1), dict(smoother=1, ch
         dict(theta=0.5), dict(interp_norm=0), dict(orth=1), dict(smoother=1, cheb_lo=0.1)]
 if a.sets != "all":
     SETS = [SETS[int(i)] for i in a.sets.split(",")]
+if a.opts:
+    def _val(v):
+        return float(v) if "." in v or "e" in v else int(v)
+    SETS = [{k: _val(v) for k, v in (kv.split("=") for kv in grp.split(",") if kv)} for grp in a.opts.split(";")]
 t_gen = time.perf_counter()
 for opts in SETS:
     try:
@@ -37,11 +44,11 @@ for opts in SETS:
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             x.zero_()
-            r = bf.bf_solve(h, b, x, 1e-8, 30, a.maxit)
+            r = bf.bf_solve(h, b, x, 1e-8, a.restart, a.maxit)
             torch.cuda.synchronize()
             t2 = time.perf_counter()
             bf.bf_destroy(h)
-        print(f"C{a.config} {str(opts):45s} iters {r['iters']:5d} conv {r['converged']} setup {1e3*(t1-t0):7.1f} ms "
+        print(f"C{a.config} m={a.restart} {str(opts):45s} iters {r['iters']:5d} conv {r['converged']} setup {1e3*(t1-t0):7.1f} ms "
               f"solve {1e3*(t2-t1):8.1f} ms  ms/iter {1e3*(t2-t1)/max(r['iters'],1):.3f}", flush=True)
     except Exception as e:
         print(f"C{a.config} {opts} failed: {e}", flush=True)
