@@ -341,6 +341,8 @@ def run_ours(args):
                 record["conv"].append(r["converged"])
                 record["mid"].append(e_mid)
                 record["launches"] += bf.bf_launch_count(h)
+                if "hier" not in record:
+                    record["hier"] = {name: bf.bf_hierarchy_stats(h, w) for w, name in ((0, "A_ss"), (1, "S~"))}
                 for k in range(4):
                     record["kt"][k] = [a + b for a, b in zip(record["kt"][k], bf.bf_kernel_time(h, k))]
         finally:
@@ -372,6 +374,9 @@ def run_ours(args):
     setup_ms = [starts[i].elapsed_time(rec["mid"][i]) for i in range(args.steps)]
     ends = starts[1:] + [e1]
     solve_ms = [rec["mid"][i].elapsed_time(ends[i]) for i in range(args.steps)]
+    # a timed solve that did not converge makes the line invalid: DOF-iterations of a stalled
+    # solve are not work towards a solution
+    all_converged = all(rec["conv"])
     units = float(sum(N * it for it in rec["iters"]))
     t_ms, units = reduce_over_ranks(dist, t_ms, units, "cuda")
     value = units / (t_ms / 1e3)
@@ -484,8 +489,14 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (J = %.0f MB > 126 MB), no flush" %
                                  ((J.nnzb * 36 + (n + 1) * 4) / 1e6),
                            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+                "valid": all_converged,
+                **({} if all_converged else {"invalid": "a timed GMRES solve did not reach the tolerance"}),
+                "time_to_solution_ms": statistics.median(a + b for a, b in zip(setup_ms, solve_ms)),
+                "setup_ms_median": statistics.median(setup_ms), "solve_ms_median": statistics.median(solve_ms),
+                "iters_median": statistics.median(rec["iters"]),
                 "iters": rec["iters"], "relres": rec["relres"], "converged": rec["conv"],
                 "setup_ms": setup_ms, "solve_ms": solve_ms,
+                "hierarchies": rec.get("hier"),
                 "roofline": roofline, "roofline_other": others,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": rec["launches"], "clocks": clk,
                 "alt_time_to_solution": alt}

@@ -103,6 +103,10 @@ typedef struct {
                                   3 coupled "point" AMG: one V-cycle of the same AMG on J itself as a
                                   point-ordered scalar 2n x 2n matrix (R20;
                                   hierarchy 3) -- the paper's AMG comparison. */
+  int32_t cheb_eig;            /* Chebyshev interval per AMG level (R21): 0 (default) ->
+                                  [cheb_lo, 1], 1 the Gershgorin bound of rho(D_l1^-1 A); k > 0 ->
+                                  [cheb_lo hi_l, hi_l], hi_l = 1.1 x a k-step power-iteration estimate
+                                  of rho(D_l1^-1 A_l) from a fixed hashed start vector (<= 64) */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;
@@ -210,6 +214,10 @@ bf_status bf_num_levels(bf_handle h, int32_t which, int32_t *nlev);
 bf_status bf_get_level(bf_handle h, int32_t which, int32_t level, int32_t *n, int64_t *nnz_A,
                        int64_t *nnz_P, int32_t *A_rowptr, int32_t *A_col, double *A_val,
                        int8_t *cf, int32_t *P_rowptr, int32_t *P_col, double *P_val, double *dl1);
+/* The smoother parameters of level `level` of hierarchy `which`: *cheb_hi = upper end of the
+ * Chebyshev interval [cheb_lo hi, hi] (1 unless opt.cheb_eig > 0, R21), *beta0 = the
+ * scaling of the first smoothing step from zero, x0 = beta0 b ./ dl1.  Either may be NULL. */
+bf_status bf_get_level_smoother(bf_handle h, int32_t which, int32_t level, double *cheb_hi, double *beta0);
 /* which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~ (S~ only for precond 0).  Sizes first; arrays
  * optional (host). */
 bf_status bf_get_block(bf_handle h, int32_t which, int64_t *nnz, int32_t *rowptr, int32_t *col,

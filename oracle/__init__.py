@@ -45,7 +45,7 @@ class Options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
                 ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
-                ("precond", C.c_int32)]
+                ("precond", C.c_int32), ("cheb_eig", C.c_int32)]
 
 
 MAXL = 64
@@ -54,7 +54,7 @@ MAXL = 64
 class AMGs(C.Structure):
     _fields_ = [("nlev", C.c_int32), ("A", CSRs * MAXL), ("P", CSRs * MAXL), ("R", CSRs * MAXL),
                 ("cf", C.POINTER(C.c_int8) * MAXL), ("strong", C.POINTER(C.c_uint8) * MAXL),
-                ("dl1", C.POINTER(C.c_double) * MAXL), ("lu", C.POINTER(C.c_double)),
+                ("dl1", C.POINTER(C.c_double) * MAXL), ("cheb_hi", C.c_double * MAXL), ("lu", C.POINTER(C.c_double)),
                 ("piv", C.POINTER(C.c_int32)), ("opt", Options)]
 
 
@@ -91,7 +91,9 @@ def lib():
         L.or_transpose.argtypes = [P(CSRs), P(CSRs)]
         L.or_matmul.argtypes = [P(CSRs), P(CSRs), P(CSRs)]
         L.or_l1diag.argtypes = [P(CSRs), dp]
-        L.or_smooth.argtypes = [P(CSRs), dp, dp, dp, C.c_int32, C.c_int32, C.c_double]
+        L.or_power_estimate.restype = C.c_double
+        L.or_power_estimate.argtypes = [P(CSRs), dp, C.c_int32, C.c_uint64, C.c_int32]
+        L.or_smooth.argtypes = [P(CSRs), dp, dp, dp, C.c_int32, C.c_int32, C.c_double, C.c_double]
         L.or_amg_setup.argtypes = [P(CSRs), P(Options), P(AMGs)]
         L.or_amg_free.argtypes = [P(AMGs)]
         L.or_vcycle.argtypes = [P(AMGs), dp, dp]
@@ -291,6 +293,12 @@ def l1diag(A: CSR):
     return d
 
 
+def power_estimate(A: CSR, d, steps, seed=0x1611, level=0):
+    s = A.cstruct()
+    d = np.ascontiguousarray(d, np.float64)
+    return float(lib().or_power_estimate(C.byref(s), _p(d, C.c_double), steps, seed, level))
+
+
 def jscalar(J) -> CSR:
     """J as a scalar point-ordered CSR (coupled AMG, reading R20)."""
     rp, ci, v = _bsr_arrays(J)
@@ -326,12 +334,12 @@ def ilu0_solve(J, lu, dinv, r):
     return x
 
 
-def smooth(A: CSR, d, b, x, kind=0, degree=2, lo=0.3):
+def smooth(A: CSR, d, b, x, kind=0, degree=2, lo=0.3, hi=1.0):
     s = A.cstruct()
     d = np.ascontiguousarray(d, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     x = np.array(x, dtype=np.float64)
-    lib().or_smooth(C.byref(s), _p(d, C.c_double), _p(b, C.c_double), _p(x, C.c_double), kind, degree, lo)
+    lib().or_smooth(C.byref(s), _p(d, C.c_double), _p(b, C.c_double), _p(x, C.c_double), kind, degree, lo, hi)
     return x
 
 
@@ -371,6 +379,7 @@ def _level(h: AMGs, l):
     out = dict(A=_from_cstruct(h.A[l]))
     n = h.A[l].nrows
     out["dl1"] = np.ctypeslib.as_array(h.dl1[l], (n,)).copy()
+    out["cheb_hi"] = float(h.cheb_hi[l])
     if l < h.nlev - 1:
         out["P"] = _from_cstruct(h.P[l])
         out["R"] = _from_cstruct(h.R[l])

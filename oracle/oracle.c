@@ -48,6 +48,7 @@ void or_default_options(or_options *o) {
   o->schur_as_printed = 0;/* Q21 */
   o->interp_norm = 1;     /* R8 */
   o->precond = 0;         /* BF, Algorithm 3 */
+  o->cheb_eig = 0;        /* R21: Gershgorin interval end 1 */
 }
 
 void or_csr_free(or_csr *A) {
@@ -458,6 +459,35 @@ void or_l1diag(const or_csr *A, double *d) {
   }
 }
 
+/* rho(D^-1 A) by the power method (R21): v <- D^-1 A v / |D^-1 A v|, estimate |D^-1 A v| for the
+ * normalised v of the previous step; the start vector is a fixed hash of (seed, level, i). */
+double or_power_estimate(const or_csr *A, const double *d, int32_t steps, uint64_t seed, int32_t level) {
+  int32_t n = A->nrows;
+  double *v = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+  double *w = (double *)xmalloc((size_t)n * sizeof(double) + 8);
+  double nv = 0.0;
+  for (int32_t i = 0; i < n; i++) {
+    v[i] = (double)or_h32(seed, level + 4096, i) / 4294967296.0 - 0.5;
+    nv += v[i] * v[i];
+  }
+  nv = sqrt(nv);
+  for (int32_t i = 0; i < n; i++) v[i] = v[i] / nv;
+  double lam = 0.0;
+  for (int32_t k = 0; k < steps; k++) {
+    or_csr_spmv(A, v, w);
+    double nw = 0.0;
+    for (int32_t i = 0; i < n; i++) {
+      w[i] = w[i] / d[i];
+      nw += w[i] * w[i];
+    }
+    lam = sqrt(nw);
+    if (lam == 0.0) break;
+    for (int32_t i = 0; i < n; i++) v[i] = w[i] / lam;
+  }
+  free(v); free(w);
+  return lam;
+}
+
 static void csr_copy(const or_csr *A, or_csr *B) {
   csr_alloc(B, A->nrows, A->ncols, A->nnz);
   memcpy(B->rp, A->rp, ((size_t)A->nrows + 1) * sizeof(int64_t));
@@ -503,6 +533,9 @@ int or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h) {
   for (int32_t k = 0; k < h->nlev; k++) {
     h->dl1[k] = (double *)xmalloc((size_t)h->A[k].nrows * sizeof(double) + 8);
     or_l1diag(&h->A[k], h->dl1[k]);
+    h->cheb_hi[k] = 1.0;
+    if (o->smoother == 1 && o->cheb_eig > 0)
+      h->cheb_hi[k] = 1.1 * or_power_estimate(&h->A[k], h->dl1[k], o->cheb_eig, o->seed, k);
   }
   /* coarsest level: dense LU with partial pivoting if n_L <= max_coarse (Q28) */
   or_csr *AL = &h->A[l];
@@ -561,11 +594,11 @@ static void smooth_l1(const or_csr *A, const double *d, const double *b, double 
   for (int32_t i = 0; i < n; i++) x[i] = x[i] + (b[i] - tmp[i]) / d[i];
 }
 
-/* Chebyshev acceleration of D^-1 A on [lo, 1] (Q27; three-term recurrence) */
+/* Chebyshev acceleration of D^-1 A on [lo hi, hi] (Q27, R21; three-term recurrence) */
 static void smooth_cheb(const or_csr *A, const double *d, const double *b, double *x,
-                        int32_t degree, double lo, double *tmp, double *dir) {
+                        int32_t degree, double lo, double hi, double *tmp, double *dir) {
   int32_t n = A->nrows;
-  double theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0;
+  double theta = hi * (1.0 + lo) / 2.0, delta = hi * (1.0 - lo) / 2.0;
   double sigma = theta / delta;
   double rho = 1.0 / sigma;
   or_csr_spmv(A, x, tmp);
@@ -582,17 +615,17 @@ static void smooth_cheb(const or_csr *A, const double *d, const double *b, doubl
 }
 
 void or_smooth(const or_csr *A, const double *d, const double *b, double *x, int32_t kind,
-               int32_t degree, double lo) {
+               int32_t degree, double lo, double hi) {
   double *tmp = (double *)xmalloc((size_t)A->nrows * sizeof(double) + 8);
   double *dir = (double *)xmalloc((size_t)A->nrows * sizeof(double) + 8);
-  if (kind == 1) smooth_cheb(A, d, b, x, degree, lo, tmp, dir);
+  if (kind == 1) smooth_cheb(A, d, b, x, degree, lo, hi, tmp, dir);
   else smooth_l1(A, d, b, x, tmp);
   free(tmp); free(dir);
 }
 
 static void smooth(const or_amg *h, int32_t l, const double *b, double *x, double *tmp, double *dir) {
   if (h->opt.smoother == 1)
-    smooth_cheb(&h->A[l], h->dl1[l], b, x, h->opt.cheb_degree, h->opt.cheb_lo, tmp, dir);
+    smooth_cheb(&h->A[l], h->dl1[l], b, x, h->opt.cheb_degree, h->opt.cheb_lo, h->cheb_hi[l], tmp, dir);
   else
     smooth_l1(&h->A[l], h->dl1[l], b, x, tmp);
 }
@@ -849,6 +882,8 @@ int or_bf_update(or_bf *b, const double *vals) {
     or_csr_free(&h->A[0]);
     csr_copy(A0[k], &h->A[0]);
     or_l1diag(&h->A[0], h->dl1[0]);
+    if (b->opt.smoother == 1 && b->opt.cheb_eig > 0)   /* R21 on the new finest matrix */
+      h->cheb_hi[0] = 1.1 * or_power_estimate(&h->A[0], h->dl1[0], b->opt.cheb_eig, b->opt.seed, 0);
   }
   if ((b->opt.precond == 1 || b->opt.precond == 2) && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv))
     return 4;

@@ -39,6 +39,9 @@ typedef struct {
                               2: CPR-AMG(2) additive (Algorithm 2) -- P:L159-193, SURVEY 8(f) NEXT-3;
                               3: coupled "point" AMG, one V-cycle on J itself as a scalar matrix in
                                  point ordering (reading R20) */
+  int32_t  cheb_eig;       /* Chebyshev interval per level (R21): 0 -> [cheb_lo, 1] (Gershgorin
+                              bound of D_l1^-1 A); k > 0 -> [cheb_lo hi_l, hi_l], hi_l = 1.1 x the
+                              k-step power-iteration estimate of rho(D_l1^-1 A_l) */
 } or_options;
 
 #define OR_MAX_LEVELS 64
@@ -51,6 +54,7 @@ typedef struct {
   int8_t *cf[OR_MAX_LEVELS];      /* 1 = C, 0 = F (levels l < L) */
   uint8_t *strong[OR_MAX_LEVELS]; /* per-nnz strength flags of A_l (l < L) */
   double *dl1[OR_MAX_LEVELS];     /* l1 diagonal of every level */
+  double cheb_hi[OR_MAX_LEVELS];  /* upper end of each level's Chebyshev interval (R21) */
   double *lu;                     /* dense LU of A_L (row-major n_L x n_L) or NULL */
   int32_t *piv;                   /* pivot rows */
   or_options opt;
@@ -98,9 +102,12 @@ int  or_interp(const or_csr *A, const uint8_t *strong, const int8_t *cf, int32_t
 void or_transpose(const or_csr *P, or_csr *R);
 void or_matmul(const or_csr *A, const or_csr *B, or_csr *C);
 void or_l1diag(const or_csr *A, double *d);
-/* one smoothing pass (kind 0: l1-Jacobi, 1: Chebyshev of `degree` on [lo,1]) with diagonal d */
+/* k-step power-iteration estimate of the spectral radius of D^-1 A (d = l1 diagonal), start vector
+ * v_i = h32(seed, level + 4096, i) / 2^32 - 1/2 (R21) */
+double or_power_estimate(const or_csr *A, const double *d, int32_t steps, uint64_t seed, int32_t level);
+/* one smoothing pass (kind 0: l1-Jacobi, 1: Chebyshev of `degree` on [lo hi, hi]) with diagonal d */
 void or_smooth(const or_csr *A, const double *d, const double *b, double *x, int32_t kind,
-               int32_t degree, double lo);
+               int32_t degree, double lo, double hi);
 int  or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h);
 void or_amg_free(or_amg *h);
 void or_vcycle(const or_amg *h, const double *b, double *x);

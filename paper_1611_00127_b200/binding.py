@@ -24,7 +24,7 @@ STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE
 # every symbol declared in include/bf.h
 EXPORTS = ["bf_default_options", "bf_setup", "bf_solve", "bf_update", "bf_destroy", "bf_last_error", "bf_spmv",
            "bf_assemble", "bf_assemble_nnzb", "bf_newton_update",
-           "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_block",
+           "bf_apply_precond", "bf_vcycle", "bf_num_levels", "bf_get_level", "bf_get_level_smoother", "bf_get_block",
            "bf_get_ilu", "bf_ilu_solve", "bf_kernel_time", "bf_launch_count", "bf_device_bytes"]
 
 
@@ -46,7 +46,7 @@ class bf_options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
                 ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
-                ("timing", C.c_int32), ("precond", C.c_int32)]
+                ("timing", C.c_int32), ("precond", C.c_int32), ("cheb_eig", C.c_int32)]
 
 
 class bf_twophase(C.Structure):
@@ -81,6 +81,7 @@ def _load():
     L.bf_num_levels.argtypes = [vp, i32, P(i32)]
     L.bf_get_level.argtypes = [vp, i32, i32, P(i32), P(i64), P(i64), vp, vp, vp, vp, vp, vp, vp, vp]
     L.bf_get_block.argtypes = [vp, i32, P(i64), vp, vp, vp]
+    L.bf_get_level_smoother.argtypes = [vp, i32, i32, dp, dp]
     L.bf_get_ilu.argtypes = [vp, vp, vp, P(i32)]
     L.bf_ilu_solve.argtypes = [vp, vp, vp, i32, vp]
     L.bf_kernel_time.argtypes = [vp, i32, dp, P(i64), dp]
@@ -249,6 +250,30 @@ def bf_get_level(h, which, level):
     return out
 
 
+def bf_get_level_smoother(h, which, level):
+    """(cheb_hi, beta0) of a level (reading R21)."""
+    hi, b0 = C.c_double(), C.c_double()
+    _check(lib.bf_get_level_smoother(h, which, level, C.byref(hi), C.byref(b0)), h)
+    return hi.value, b0.value
+
+
+def bf_level_sizes(h, which, level):
+    """(n, nnz(A_l), nnz(P_l)) of level `level` of hierarchy `which` (sizes only, no copies)."""
+    n, nA, nP = C.c_int32(), C.c_int64(), C.c_int64()
+    _check(lib.bf_get_level(h, which, level, C.byref(n), C.byref(nA), C.byref(nP), *([None] * 8)), h)
+    return n.value, nA.value, nP.value
+
+
+def bf_hierarchy_stats(h, which):
+    """Per-level sizes and the operator / grid complexities of hierarchy `which`."""
+    lv = [bf_level_sizes(h, which, l) for l in range(bf_num_levels(h, which))]
+    if not lv:
+        return None
+    return {"levels": [{"n": n, "nnz_A": a, "nnz_P": p} for n, a, p in lv],
+            "operator_complexity": sum(a for _, a, _ in lv) / lv[0][1],
+            "grid_complexity": sum(n for n, _, _ in lv) / lv[0][0]}
+
+
 def bf_get_block(h, which):
     """which: 0 A_pp, 1 A_ps, 2 A_sp, 3 A_ss, 4 S~ -> (row_ptr, col, val) host arrays."""
     nnz = C.c_int64()
@@ -338,6 +363,9 @@ class BFSolver:
 
     def block(self, which):
         return bf_get_block(self.h, which)
+
+    def cheb_hi(self, which, l):
+        return bf_get_level_smoother(self.h, which, l)[0]
 
     def ilu(self, nnzb):
         return bf_get_ilu(self.h, nnzb, self.n)

@@ -320,6 +320,7 @@ bf_status bf_default_options(bf_options *o) {
   o->interp_norm = 1;
   o->timing = 0;
   o->precond = 0;
+  o->cheb_eig = 0;
   return BF_OK;
 }
 
@@ -332,6 +333,7 @@ static const char *check_options(const bf_options *o) {
   if (o->smoother == 1 && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
   if (o->smoother == 1 && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
   if (o->orth != 0 && o->orth != 1) return "orth must be 0 or 1";
+  if (o->cheb_eig < 0 || o->cheb_eig > 64) return "cheb_eig in [0, 64]";
   if (o->precond < 0 || o->precond > 3)
     return "precond must be 0 (BF), 1 (CPR-AMG(1)), 2 (CPR-AMG(2)) or 3 (coupled AMG)";
   return nullptr;
@@ -370,18 +372,31 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
               c->sync_ms);
       t0 = t1;
     };
-    validate_and_ingest(c, J);
-    setup_bsr_dia(c);
+    NvtxRange r_setup("bf_setup");
+    {
+      NvtxRange r("bf_setup: ingest + validate (a1)");
+      validate_and_ingest(c, J);
+      setup_bsr_dia(c);
+    }
     lap("ingest");
-    build_split(c);
+    {
+      NvtxRange r("bf_setup: field split (a2)");
+      build_split(c);
+    }
     lap("split");
     const int pc = c->opt.precond;
     if (pc == 0) {  // BF (Algorithm 3): S~, the A_ps coupling, hierarchies A_ss and S~
-      build_schur(c);
+      {
+        NvtxRange r("bf_setup: S~ (a3)");
+        build_schur(c);
+      }
       lap("schur");
       tile_csr(c, c->blk[1]);
       setup_dia(c, c->blk[1]);
-      build_two_hierarchies(c, 0, c->blk[3], 1, c->blk[4]);
+      {
+        NvtxRange r("bf_setup: AMG A_ss + S~ (a4)");
+        build_two_hierarchies(c, 0, c->blk[3], 1, c->blk[4]);
+      }
       lap("amg A_ss + S~");
     } else if (pc == 3) {  // coupled point AMG on J
       build_jscalar(c, c->jsc);
@@ -420,6 +435,7 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
     return BF_ERR_ARG;
   }
   BF_GUARD_BEGIN
+  NvtxRange r_update("bf_update");
   c->stream = (cudaStream_t)stream;
   c->err.clear();
   reingest_values(c, vals, mem);  // validation first: the handle is untouched on BF_ERR_NONFINITE
@@ -514,6 +530,7 @@ bf_status bf_solve(bf_handle c, const double *rhs, double *x, double tol, int32_
     return BF_ERR_ARG;
   }
   BF_GUARD_BEGIN
+  NvtxRange r_solve("bf_solve");
   c->stream = (cudaStream_t)stream;
   c->err.clear();
   cudaEvent_t t0;
@@ -625,6 +642,13 @@ bf_status bf_get_level(bf_handle c, int32_t which, int32_t level, int32_t *n, in
   BF_CUDA(cudaStreamSynchronize(c->stream));
   return BF_OK;
   BF_GUARD_END(c)
+}
+
+bf_status bf_get_level_smoother(bf_handle c, int32_t which, int32_t level, double *cheb_hi, double *beta0) {
+  if (!c || which < 0 || which > 3 || level < 0 || level >= c->h[which].nlev) return BF_ERR_ARG;
+  if (cheb_hi) *cheb_hi = c->h[which].lv[level].cheb_hi;
+  if (beta0) *beta0 = c->h[which].lv[level].beta0;
+  return BF_OK;
 }
 
 bf_status bf_get_block(bf_handle c, int32_t which, int64_t *nnz, int32_t *rowptr, int32_t *col, double *val) {

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/bf.h"
+#include <nvtx3/nvToolsExt.h>
 
 #define BF_MAXL 64
 
@@ -42,6 +43,8 @@ struct Level {
   double *dl1 = nullptr;
   double *b = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
   double *d = nullptr;  // 1 / dl1 (smoother scaling)
+  double cheb_hi = 1.0;  // upper end of the Chebyshev interval [cheb_lo hi, hi] (reading R21)
+  double beta0 = 1.0;    // first smoothing step from zero: x0 = beta0 b ./ dl1 (1/theta for Chebyshev)
 };
 
 struct Hier {
@@ -205,6 +208,14 @@ void sync(bf_ctx *c);  // counted, timed cudaStreamSynchronize
 void release_all(bf_ctx *c);  // return every block of c to the cache (after a sync)
 
 #define BF_CUDA(x) ::bf::cuda_check((x), #x)
+
+// NVTX range for profilers (ncu --nvtx / nsys); a no-op without an attached tool
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 #define BF_LAUNCH(c) ((c)->launches++)
 
 // ---- scans (k_util.cu) ------------------------------------------------------------
@@ -223,6 +234,7 @@ void build_schur(bf_ctx *c);                                            // k_spl
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg_setup.cu
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);
+void set_level_beta(const bf_options &o, Level &L);                      // k_vcycle.cu
 void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vcycle.cu
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
 double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu

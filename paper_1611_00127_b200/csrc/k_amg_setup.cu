@@ -17,6 +17,7 @@
 #include "bf_internal.cuh"
 
 #include <algorithm>
+#include <vector>
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
@@ -983,6 +984,87 @@ static void copy_csr(bf_ctx *c, const DCsr &A, DCsr &B) {
   BF_CUDA(cudaMemcpyAsync(B.v, A.v, sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice, c->stream));
 }
 
+// ---------------------------------------------------------------------------------------
+// Power-iteration estimate of rho(D_l1^-1 A) for the Chebyshev interval of a level (reading
+// R21; the oracle's or_power_estimate): v_0 = hashed start vector / |.|, then k times
+// w = D^-1 A v, lambda = |w|, v = w / lambda.  The norms are fixed-order two-level reductions
+// (the same result run to run); against the oracle they differ only by summation order.
+// ---------------------------------------------------------------------------------------
+constexpr int POW_BLOCKS = 256;
+static __global__ void k_pow_init(int n, uint64_t seed, int level, double *v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (double)h32(seed, level + 4096, i) / 4294967296.0 - 0.5;
+}
+static __global__ void k_pow_apply(DCsr A, const double *__restrict__ dl1, const double *__restrict__ v,
+                                   double *__restrict__ w) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  double s = 0.0;
+  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) s += A.v[q] * v[A.ci[q]];
+  w[i] = s / dl1[i];
+}
+static __global__ void __launch_bounds__(256) k_pow_partial(int n, const double *__restrict__ w, double *part) {
+  __shared__ double sm[256];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s += w[i] * w[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+static __global__ void k_pow_norm(const double *__restrict__ part, double *nrm) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < POW_BLOCKS; b++) s += part[b];
+    *nrm = sqrt(s);
+  }
+}
+static __global__ void k_pow_scale(int n, const double *__restrict__ w, const double *__restrict__ nrm, double *v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double s = *nrm;
+  if (i < n) v[i] = s > 0.0 ? w[i] / s : 0.0;
+}
+
+// Level::cheb_hi and Level::beta0 of every level of h (the Chebyshev interval, R21)
+static void set_cheb_intervals(bf_ctx *c, Hier &h, int only_level = -1) {
+  const bf_options &o = c->opt;
+  std::vector<int> lv;
+  for (int k = 0; k < h.nlev; k++)
+    if (only_level < 0 || k == only_level) lv.push_back(k);
+  if (o.smoother == 1 && o.cheb_eig > 0) {
+    double *nrm = dalloc_t<double>(c, 2 * lv.size() + 2);
+    double *part = dalloc_t<double>(c, POW_BLOCKS);
+    for (size_t q = 0; q < lv.size(); q++) {
+      Level &L = h.lv[lv[q]];
+      int n = L.A.n;
+      double *v = dalloc_t<double>(c, n), *w = dalloc_t<double>(c, n);
+      k_pow_init<<<div_up(n, 256), 256, 0, c->stream>>>(n, o.seed, lv[q], w);
+      k_pow_partial<<<POW_BLOCKS, 256, 0, c->stream>>>(n, w, part);
+      k_pow_norm<<<1, 32, 0, c->stream>>>(part, nrm + 2 * q);
+      k_pow_scale<<<div_up(n, 256), 256, 0, c->stream>>>(n, w, nrm + 2 * q, v);
+      for (int s = 0; s < o.cheb_eig; s++) {
+        k_pow_apply<<<div_up(n, 256), 256, 0, c->stream>>>(L.A, L.dl1, v, w);
+        k_pow_partial<<<POW_BLOCKS, 256, 0, c->stream>>>(n, w, part);
+        k_pow_norm<<<1, 32, 0, c->stream>>>(part, nrm + 2 * q + 1);
+        k_pow_scale<<<div_up(n, 256), 256, 0, c->stream>>>(n, w, nrm + 2 * q + 1, v);
+      }
+      c->launches += 4 + 4 * o.cheb_eig;
+      dfree(c, v);
+      dfree(c, w);
+    }
+    std::vector<double> hn(2 * lv.size() + 2);
+    BF_CUDA(cudaMemcpyAsync(hn.data(), nrm, sizeof(double) * 2 * lv.size(), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    dfree(c, nrm);
+    dfree(c, part);
+    for (size_t q = 0; q < lv.size(); q++) h.lv[lv[q]].cheb_hi = 1.1 * hn[2 * q + 1];
+  }
+  for (int k : lv) set_level_beta(o, h.lv[k]);
+}
+
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   Hier &h = c->h[which];
   const bf_options &o = c->opt;
@@ -1156,6 +1238,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
                                               " (n=" + std::to_string(nL) + ") singular at pivot " +
                                               std::to_string(hs));
   }
+  set_cheb_intervals(c, h);
   plan_tail(c, h);
   build_dense_tail(c, h);
   build_rfuse(c, h, false);
@@ -1236,6 +1319,7 @@ void refresh_finest(bf_ctx *c, int which, const DCsr &A0) {
   dfree(c, diag);
   tile_csr(c, L.A, true);
   setup_dia(c, L.A);
+  set_cheb_intervals(c, h, 0);
   plan_tail(c, h);
   if (h.lv[0].Rf.n) build_rfuse(c, h, true);  // the finest level's fused restriction uses A_0
 }

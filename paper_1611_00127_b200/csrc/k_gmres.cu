@@ -59,10 +59,172 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double *pa
 // The three passes are launched with programmatic dependent launch: the first grid-stride
 // iteration's basis loads (V_0..V_j are complete before the predecessor kernel started) are
 // issued before pdl_wait(); w and h (the predecessor's outputs) are read after it.
+//
+// Vectors are read as double2 (N = 2 n_cells is even and every basis vector starts 16-B
+// aligned), and a thread handles UNR(NV) grid-stride elements per iteration with all their
+// loads issued before the first FMA: for short bases (the first Arnoldi steps of a cycle) a
+// single element per thread leaves too few bytes in flight to cover the DRAM latency
+// (round 1 measured k_dots<1> at 25 % of the copy bandwidth).
+template <int NV>
+struct Unr {
+  static constexpr int U = NV <= 2 ? 4 : (NV <= 5 ? 2 : 1);
+};
 
 // pass 1: out[i] = V_i . w, i < NV
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double *__restrict__ V,
+__device__ __forceinline__ void dots_v2(int64_t N, const double *__restrict__ V,
+                                                      const double *__restrict__ w, double *partial,
+                                                      double *out, unsigned int *counter) {
+  constexpr int U = Unr<NV>::U;
+  const int64_t N2 = N >> 1;
+  const double2 *__restrict__ V2 = reinterpret_cast<const double2 *>(V);
+  const double2 *__restrict__ w2 = reinterpret_cast<const double2 *>(w);
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) acc[i] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double2 v[U][NV];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (t0 + u * stride < N2) {
+#pragma unroll
+      for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t0 + u * stride);
+    }
+  pdl_wait();
+  for (int64_t t = t0; t < N2; t += U * stride) {
+    if (t != t0) {
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (t + u * stride < N2) {
+#pragma unroll
+          for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t + u * stride);
+        }
+    }
+    double2 wt[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) wt[u] = t + u * stride < N2 ? __ldcs(w2 + t + u * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u * stride < N2) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] += v[u][i].x * wt[u].x + v[u][i].y * wt[u].y;
+      }
+  }
+  block_reduce_store<NV>(acc, partial, out, NV, counter);
+}
+
+// pass 2: w <- w - sum_i h_i V_i ; out[i] = V_i . w (new w)
+template <int NV>
+__device__ __forceinline__ void axpy_dots_v2(int64_t N, const double *__restrict__ V, double *w,
+                                                           const double *__restrict__ h, double *partial,
+                                                           double *out, unsigned int *counter) {
+  constexpr int U = Unr<NV>::U;
+  __shared__ double hs[NV];
+  const int64_t N2 = N >> 1;
+  const double2 *__restrict__ V2 = reinterpret_cast<const double2 *>(V);
+  double2 *w2 = reinterpret_cast<double2 *>(w);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double2 v[U][NV];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (t0 + u * stride < N2) {
+#pragma unroll
+      for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t0 + u * stride);
+    }
+  pdl_wait();
+  if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) acc[i] = 0.0;
+  for (int64_t t = t0; t < N2; t += U * stride) {
+    double2 wt[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) wt[u] = t + u * stride < N2 ? w2[t + u * stride] : make_double2(0.0, 0.0);
+    if (t != t0) {
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (t + u * stride < N2) {
+#pragma unroll
+          for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t + u * stride);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u * stride < N2) {
+        double2 a = wt[u];
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          a.x -= hs[i] * v[u][i].x;
+          a.y -= hs[i] * v[u][i].y;
+        }
+        w2[t + u * stride] = a;
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] += v[u][i].x * a.x + v[u][i].y * a.y;
+      }
+  }
+  block_reduce_store<NV>(acc, partial, out, NV, counter);
+}
+
+// pass 3: y = w - sum_i h_i V_i written to `y` (may be the next basis slot); out[0] = ||y||^2
+template <int NV>
+__device__ __forceinline__ void axpy_norm_v2(int64_t N, const double *__restrict__ V,
+                                                           const double *__restrict__ w,
+                                                           const double *__restrict__ h, double *__restrict__ y,
+                                                           double *partial, double *out, unsigned int *counter) {
+  constexpr int U = Unr<NV>::U;
+  __shared__ double hs[NV];
+  const int64_t N2 = N >> 1;
+  const double2 *__restrict__ V2 = reinterpret_cast<const double2 *>(V);
+  const double2 *__restrict__ w2 = reinterpret_cast<const double2 *>(w);
+  double2 *__restrict__ y2 = reinterpret_cast<double2 *>(y);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double2 v[U][NV];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (t0 + u * stride < N2) {
+#pragma unroll
+      for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t0 + u * stride);
+    }
+  pdl_wait();
+  if (threadIdx.x < NV) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double acc[1] = {0.0};
+  for (int64_t t = t0; t < N2; t += U * stride) {
+    if (t != t0) {
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (t + u * stride < N2) {
+#pragma unroll
+          for (int i = 0; i < NV; i++) v[u][i] = __ldcs(V2 + (size_t)i * N2 + t + u * stride);
+        }
+    }
+    double2 wt[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) wt[u] = t + u * stride < N2 ? __ldcs(w2 + t + u * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u * stride < N2) {
+        double2 a = wt[u];
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          a.x -= hs[i] * v[u][i].x;
+          a.y -= hs[i] * v[u][i].y;
+        }
+        y2[t + u * stride] = a;
+        acc[0] += a.x * a.x + a.y * a.y;
+      }
+  }
+  block_reduce_store<1>(acc, partial, out, 1, counter);
+}
+
+// scalar bodies (bases longer than 8 vectors: NV loads per element already keep enough bytes in flight)
+// pass 1: out[i] = V_i . w, i < NV
+template <int NV>
+__device__ __forceinline__ void dots_s(int64_t N, const double *__restrict__ V,
                                                       const double *__restrict__ w, double *partial,
                                                       double *out, unsigned int *counter) {
   double acc[NV];
@@ -90,7 +252,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double
 
 // pass 2: w <- w - sum_i h_i V_i ; out[i] = V_i . w (new w)
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_dots(int64_t N, const double *__restrict__ V, double *w,
+__device__ __forceinline__ void axpy_dots_s(int64_t N, const double *__restrict__ V, double *w,
                                                            const double *__restrict__ h, double *partial,
                                                            double *out, unsigned int *counter) {
   __shared__ double hs[NV];
@@ -124,7 +286,7 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_dots(int64_t N, const d
 
 // pass 3: y = w - sum_i h_i V_i written to `y` (may be the next basis slot); out[0] = ||y||^2
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const double *__restrict__ V,
+__device__ __forceinline__ void axpy_norm_s(int64_t N, const double *__restrict__ V,
                                                            const double *__restrict__ w,
                                                            const double *__restrict__ h, double *__restrict__ y,
                                                            double *partial, double *out, unsigned int *counter) {
@@ -152,6 +314,30 @@ __global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const d
     acc[0] += wt * wt;
   }
   block_reduce_store<1>(acc, partial, out, 1, counter);
+}
+
+// the kernels: double2 bodies with UNR-fold unrolling for short bases, scalar bodies otherwise
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS, 2) k_dots(int64_t N, const double *__restrict__ V,
+                                                      const double *__restrict__ w, double *partial,
+                                                      double *out, unsigned int *counter) {
+  if constexpr (NV <= 8) dots_v2<NV>(N, V, w, partial, out, counter);
+  else dots_s<NV>(N, V, w, partial, out, counter);
+}
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_dots(int64_t N, const double *__restrict__ V, double *w,
+                                                           const double *__restrict__ h, double *partial,
+                                                           double *out, unsigned int *counter) {
+  if constexpr (NV <= 8) axpy_dots_v2<NV>(N, V, w, h, partial, out, counter);
+  else axpy_dots_s<NV>(N, V, w, h, partial, out, counter);
+}
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS, 2) k_axpy_norm(int64_t N, const double *__restrict__ V,
+                                                           const double *__restrict__ w,
+                                                           const double *__restrict__ h, double *__restrict__ y,
+                                                           double *partial, double *out, unsigned int *counter) {
+  if constexpr (NV <= 8) axpy_norm_v2<NV>(N, V, w, h, y, partial, out, counter);
+  else axpy_norm_s<NV>(N, V, w, h, y, partial, out, counter);
 }
 
 // w <- w - sum_i h_i V_i (one block of a basis longer than MAXNV; no reduction)
@@ -459,6 +645,7 @@ void gmres(bf_ctx *c, const double *b, double *x, double tol, int m, int maxit, 
     c->timing_skip = false;
   };
   for (;;) {
+    NvtxRange r_cycle("gmres cycle");
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int k = 0;

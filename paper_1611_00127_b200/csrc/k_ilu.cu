@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(256) k_cpr_resid(int n, const int32_t *__restr
                                                    double *__restrict__ bp, double *__restrict__ xp,
                                                    const double *__restrict__ dp, double *__restrict__ bs,
                                                    double *__restrict__ xs, const double *__restrict__ ds,
-                                                   double beta, int ip) {
+                                                   double beta_p, double beta_s, int ip) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double w0 = 0.0, w1 = 0.0;
@@ -770,10 +770,10 @@ __global__ void __launch_bounds__(256) k_cpr_resid(int n, const int32_t *__restr
   double2 ri = r[i];
   double tp = (ip ? ri.y : ri.x) - w0, ts = (ip ? ri.x : ri.y) - w1;
   bp[i] = tp;
-  xp[i] = beta * (tp * dp[i]);
+  xp[i] = beta_p * (tp * dp[i]);
   if (bs) {
     bs[i] = ts;
-    xs[i] = beta * (ts * ds[i]);
+    xs[i] = beta_s * (ts * ds[i]);
   }
 }
 
@@ -954,7 +954,6 @@ static void ilu_solve(bf_ctx *c, double *r, const double *nrm2) {
 }
 
 void vcycle_from_invariant(bf_ctx *c, int which);  // k_vcycle.cu
-double x0_beta_of(const bf_options &o);             // k_vcycle.cu
 
 void amg_apply(bf_ctx *c, const double *v, double *z, const double *nrm2);
 
@@ -974,7 +973,7 @@ void cpr_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
       n, c->brp, c->bci, reinterpret_cast<const double2 *>(c->bv), reinterpret_cast<const double2 *>(c->jdia), o,
       reinterpret_cast<const double2 *>(c->ilu_u), reinterpret_cast<const double2 *>(v), hp.lv[0].b, hp.lv[0].x,
       hp.lv[0].d, additive ? hs.lv[0].b : nullptr, additive ? hs.lv[0].x : nullptr,
-      additive ? hs.lv[0].d : nullptr, x0_beta_of(c->opt), c->var_order);  // step 3
+      additive ? hs.lv[0].d : nullptr, hp.lv[0].beta0, additive ? hs.lv[0].beta0 : 1.0, c->var_order);  // step 3
   BF_LAUNCH(c);
   vcycle_from_invariant(c, 2);  // step 4
   if (additive) vcycle_from_invariant(c, 0);  // Alg. 2 step 5
@@ -1131,7 +1130,7 @@ void amg_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   Level &L = c->h[3].lv[0];
   k_jsc_split<<<div_up(n, 256), 256, 0, c->stream>>>(n, c->var_order, reinterpret_cast<double2 *>(const_cast<double *>(v)),
                                                       nrm2, reinterpret_cast<double2 *>(L.b),
-                                                      reinterpret_cast<const double2 *>(L.d), x0_beta_of(c->opt),
+                                                      reinterpret_cast<const double2 *>(L.d), L.beta0,
                                                       reinterpret_cast<double2 *>(L.x));
   BF_LAUNCH(c);
   vcycle_from_invariant(c, 3);

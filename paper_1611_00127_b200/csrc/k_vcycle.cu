@@ -16,6 +16,19 @@
 
 namespace bf {
 
+// Chebyshev interval of level L: [lo hi, hi] on D_l1^-1 A (reading R21): theta = hi (1+lo)/2,
+// delta = hi (1-lo)/2; the first step from zero is x0 = (1/theta) b ./ dl1 (Level::beta0)
+static void cheb_params(const bf_options &o, const Level &L, double &theta, double &delta) {
+  theta = L.cheb_hi * (1.0 + o.cheb_lo) / 2.0;
+  delta = L.cheb_hi * (1.0 - o.cheb_lo) / 2.0;
+}
+
+void set_level_beta(const bf_options &o, Level &L) {
+  double theta, delta;
+  cheb_params(o, L, theta, delta);
+  L.beta0 = o.smoother == 1 ? 1.0 / theta : 1.0;
+}
+
 // coarsest-level solve x = A_L^-1 b with the inverse formed at setup from the pivoted LU
 // (one CTA, thread per row; replaces 2 n dependent substitution steps)
 __global__ void k_coarse_inv(int n, const double *__restrict__ inv, const double *__restrict__ b,
@@ -38,25 +51,25 @@ __global__ void k_coarse_inv(int n, const double *__restrict__ inv, const double
 constexpr int TAIL_MAXL = 12;
 constexpr int TAIL_THREADS = 512;
 
+// smoothing recurrence of one pass of a level: l1-Jacobi is the degree-1 case c0 = 1;
+// Chebyshev of degree m: first step x += c0 D (b - A x), dir = that step; steps k = 1..m-1:
+// dir = ca[k] dir + cb[k] D (b - A x), x += dir (smooth_pass below)
+struct TailSmoother {
+  int deg, nu_pre, nu_post;
+  double c0, ca[8], cb[8];
+};
 struct TailLevel {
   int n, gA, gP, gR;
   const int32_t *Arp, *Aci, *Prp, *Pci, *Rrp, *Rci;
   const double *Av, *Pv, *Rv, *d;
   double *b, *x, *r, *t, *dir;
-};
-// smoothing recurrence of one pass (the same for every level of the tail): l1-Jacobi is the
-// degree-1 case c0 = 1; Chebyshev of degree m: first step x += c0 D (b - A x), dir = that step;
-// steps k = 1..m-1: dir = ca[k] dir + cb[k] D (b - A x), x += dir (smooth_pass below)
-struct TailSmoother {
-  int deg, nu_pre, nu_post;
-  double c0, ca[8], cb[8];
+  TailSmoother sm;
 };
 struct TailParams {
   int nl;  // tail levels including the coarsest
   int gL;  // lanes per row of the dense coarse solve
   double beta;
   const double *inv;
-  TailSmoother sm;
   TailLevel lv[TAIL_MAXL];
 };
 
@@ -182,11 +195,12 @@ constexpr int DTAIL_THREADS = 256;
 __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, double *__restrict__ T) {
   const int col = blockIdx.x, n0 = p.lv[0].n;
   const int tid = threadIdx.x, nth = blockDim.x;
-  const TailSmoother &sm = p.sm;
+  const TailSmoother &sm0 = p.lv[0].sm;  // nu_pre / nu_post (the same on every level)
   auto off = [&](int k) { return (size_t)col * p.lv[k].n; };
   // t = A x (all rows), then the pointwise smoothing update of step `step` of a pass
   auto smooth_step = [&](int k, int step, bool from_zero) {
     const TailLevel &L = p.lv[k];
+    const TailSmoother &sm = L.sm;
     double *b = L.b + off(k), *x = L.x + off(k), *t = L.t + off(k), *dir = L.dir + off(k);
     if (!from_zero) {
       int g = L.gA, lig = tid & (g - 1);
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
     __syncthreads();
   };
   auto smooth_pass = [&](int k, bool from_zero) {
-    for (int step = 0; step < sm.deg; step++) smooth_step(k, step, from_zero && step == 0);
+    for (int step = 0; step < p.lv[k].sm.deg; step++) smooth_step(k, step, from_zero && step == 0);
   };
   for (int i = tid; i < n0; i += nth) p.lv[0].b[off(0) + i] = i == col ? 1.0 : 0.0;
   __syncthreads();
@@ -215,11 +229,11 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
     const TailLevel &L = p.lv[l];
     const TailLevel &C = p.lv[l + 1];
     double *b = L.b + off(l), *x = L.x + off(l), *r = L.r + off(l);
-    if (sm.nu_pre == 0) {
+    if (sm0.nu_pre == 0) {
       for (int i = tid; i < L.n; i += nth) x[i] = 0.0;
       __syncthreads();
     }
-    for (int s = 0; s < sm.nu_pre; s++) smooth_pass(l, s == 0);
+    for (int s = 0; s < sm0.nu_pre; s++) smooth_pass(l, s == 0);
     {  // r = b - A x
       int g = L.gA, lig = tid & (g - 1);
       for (int base = 0; base < L.n; base += nth / g) {
@@ -266,14 +280,14 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       }
     }
     __syncthreads();
-    for (int s = 0; s < sm.nu_post; s++) smooth_pass(l, false);
+    for (int s = 0; s < sm0.nu_post; s++) smooth_pass(l, false);
   }
   const double *x0 = p.lv[0].x + off(0);
   for (int i = tid; i < n0; i += nth) T[(size_t)i * n0 + col] = x0[i];
 }
 
-// the smoothing recurrence of one pass (see TailSmoother)
-static TailSmoother tail_smoother(const bf_options &o) {
+// the smoothing recurrence of one pass on level L (see TailSmoother)
+static TailSmoother tail_smoother(const bf_options &o, const Level &L) {
   TailSmoother sm{};
   sm.nu_pre = o.nu_pre;
   sm.nu_post = o.nu_post;
@@ -282,7 +296,9 @@ static TailSmoother tail_smoother(const bf_options &o) {
     sm.c0 = 1.0;
     return sm;
   }
-  double lo = o.cheb_lo, theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0, sigma = theta / delta;
+  double theta, delta;
+  cheb_params(o, L, theta, delta);
+  double sigma = theta / delta;
   double rho = 1.0 / sigma;
   sm.deg = o.cheb_degree;
   sm.c0 = 1.0 / theta;
@@ -352,7 +368,6 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
   p.nl = h.nlev - lt;
   p.beta = 1.0;
   p.inv = h.inv;
-  p.sm = tail_smoother(o);
   std::vector<double *> bufs;
   for (int k = 0; k < p.nl; k++) {
     Level &L = h.lv[lt + k];
@@ -371,6 +386,7 @@ void build_dense_tail(bf_ctx *c, Hier &h) {
     Tl.Rci = L.R.ci;
     Tl.Rv = L.R.v;
     Tl.d = L.d;
+    Tl.sm = tail_smoother(o, L);
     double *w = dalloc_t<double>(c, (size_t)5 * n0 * L.A.n);  // [b | x | r | t | dir] x n0 columns
     bufs.push_back(w);
     Tl.b = w;
@@ -558,10 +574,6 @@ void setup_dia(bf_ctx *c, DCsr &A) {
   BF_CUDA(cudaGetLastError());
 }
 
-// beta of the first smoothing step from x = 0: x0 = beta b ./ dl1
-static double x0_beta(const bf_options &o) {
-  return o.smoother == 1 ? 2.0 / (1.0 + o.cheb_lo) : 1.0;  // Chebyshev: 1/theta, theta = (1+lo)/2
-}
 
 // Level invariant on entry to vcycle_level(l): L.b holds the right-hand side and L.x holds
 // x0 = beta b ./ dl1 (written by whichever kernel produced b: the split, the A_ps coupling,
@@ -583,8 +595,10 @@ static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool first, bool want_r
       csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, nullptr, 0.0, 1.0, nullptr);
       swap_t();
     }
-  } else {  // Chebyshev acceleration of D^-1 A on [lo, 1] (three-term recurrence)
-    double lo = o.cheb_lo, theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0, sigma = theta / delta;
+  } else {  // Chebyshev acceleration of D^-1 A on [lo hi, hi] (three-term recurrence)
+    double theta, delta;
+    cheb_params(o, L, theta, delta);
+    double sigma = theta / delta;
     double rho = 1.0 / sigma;
     double *dir = L.r;  // direction storage (r is recomputed below when needed)
     // the first step's direction is the step itself: after a seeded first step (x = x0 from
@@ -657,9 +671,9 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   Level &Lc = h.lv[l + 1];
   // b_c = R r, and x0_c = beta b_c ./ dl1_c for the next level
   if (L.Rf.n) {  // b_c = R (I - beta A D) b: residual of the seeded pre-sweep + restriction in one product
-    csr_op<OP_SPMV_X0>(c, L.Rf, L.b, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
+    csr_op<OP_SPMV_X0>(c, L.Rf, L.b, nullptr, Lc.d, Lc.b, Lc.x, 0.0, Lc.beta0, nullptr);
   } else {
-    csr_op<OP_SPMV_X0>(c, L.R, L.r, nullptr, Lc.d, Lc.b, Lc.x, 0.0, x0_beta(o), nullptr);
+    csr_op<OP_SPMV_X0>(c, L.R, L.r, nullptr, Lc.d, Lc.b, Lc.x, 0.0, Lc.beta0, nullptr);
   }
   vcycle_level(c, h, l + 1);
   csr_op<OP_ADD>(c, L.P, Lc.x, nullptr, nullptr, x, nullptr, 0.0, 0.0, nullptr);  // x += P e
@@ -672,7 +686,6 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
   }
 }
 
-double x0_beta_of(const bf_options &o) { return x0_beta(o); }
 
 // V-cycle of hierarchy `which` whose finest level already holds b and x0 (level invariant)
 void vcycle_from_invariant(bf_ctx *c, int which) { vcycle_level(c, c->h[which], 0); }
@@ -682,7 +695,7 @@ void vcycle(bf_ctx *c, int which, const double *b, double *x) {
   Level &L0 = h.lv[0];
   int n = L0.A.n;
   BF_CUDA(cudaMemcpyAsync(L0.b, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-  k_x0<<<div_up(n, 256), 256, 0, c->stream>>>(n, x0_beta(c->opt), L0.b, L0.d, L0.x);
+  k_x0<<<div_up(n, 256), 256, 0, c->stream>>>(n, L0.beta0, L0.b, L0.d, L0.x);
   BF_LAUNCH(c);
   vcycle_level(c, h, 0);
   BF_CUDA(cudaMemcpyAsync(x, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -752,11 +765,11 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   // Alg. 3 step 2: A_ss s = R_s r_k by one V-cycle
   c->alg_bytes += 48.0 * n + 32.0 * n;  // split (v in; vp, vs, x0 out; dl1 in) + merge (p, s in; z out)
   k_split_vec<<<div_up(n, 256), 256, 0, c->stream>>>(n, ip, const_cast<double *>(v), c->vp, hs.lv[0].b,
-                                                     hs.lv[0].d, x0_beta(c->opt), hs.lv[0].x, nrm2);
+                                                     hs.lv[0].d, hs.lv[0].beta0, hs.lv[0].x, nrm2);
   BF_LAUNCH(c);
   vcycle_level(c, hs, 0);
   // step 3: r = R_p r_k - A_ps s
-  csr_op<OP_SUB_X0>(c, c->blk[1], hs.lv[0].x, c->vp, hS.lv[0].d, hS.lv[0].b, hS.lv[0].x, 0.0, x0_beta(c->opt),
+  csr_op<OP_SUB_X0>(c, c->blk[1], hs.lv[0].x, c->vp, hS.lv[0].d, hS.lv[0].b, hS.lv[0].x, 0.0, hS.lv[0].beta0,
                     nullptr);
   // step 4: S~ p = r by one V-cycle.  With one l1-Jacobi post-sweep on a DIA finest level,
   // that sweep and the merge z = R_p^T p + R_s^T s are one kernel (k_dia_smooth_merge)

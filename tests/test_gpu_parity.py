@@ -133,13 +133,17 @@ def test_options_parity():
     """Non-default options are implemented identically on both sides."""
     prob, J, rhs = make_system(2, dims=(10, 9, 8))
     for opts in (dict(smoother=1), dict(interp_norm=0), dict(orth=1), dict(nu_pre=2, nu_post=2),
-                 dict(theta=0.5, max_coarse=30), dict(schur_as_printed=1), dict(nu_pre=0)):
+                 dict(theta=0.5, max_coarse=30), dict(schur_as_printed=1), dict(nu_pre=0),
+                 dict(smoother=1, cheb_lo=0.1, cheb_eig=10), dict(smoother=1, cheb_degree=3, cheb_eig=4, nu_pre=2)):
         o = oracle.BF(J, **opts)
         g = gpu_solver(J, prob.dims, **opts)
         for which in (0, 1):
             assert g.num_levels(which) == o.nlev(which)
             for l in range(o.nlev(which) - 1):
                 assert np.array_equal(g.level(which, l)["cf"], o.level(which, l)["cf"]), opts
+            # the Chebyshev interval ends of R21 (power-iteration estimates) agree to rounding
+            for l in range(o.nlev(which)):
+                assert abs(g.cheb_hi(which, l) - o.level(which, l)["cheb_hi"]) <= 1e-12, (opts, which, l)
         v = seeded_vector(2 * J.n, 3)
         zo = o.apply(v)
         z = np.zeros(2 * J.n)

@@ -663,3 +663,31 @@ def test_spectrum_exact_inner_solves():
     assert np.abs(lam - ref).max() <= 1e-8 * np.abs(ref).max()
     # BF keeps the spectrum away from the origin
     assert np.abs(lam).min() > 0.05
+
+
+def test_chebyshev_interval_from_power_estimate():
+    """Reading R21: the Chebyshev interval of a level is [cheb_lo hi, hi] with hi = 1.1 x a k-step
+    power-iteration estimate of rho(D_l1^-1 A).  Pins: (1) the estimate of the 1D Poisson matrix
+    with d = 4 converges to the closed form (1 + cos(pi/(n+1)))/2; (2) on diag(lambda),
+    lambda in [lo hi, hi] with hi = 2, one degree-m pass reduces the error by 1/T_m((1+lo)/(1-lo))
+    (the recurrence is scale-invariant in hi); (3) every level of a hierarchy built with
+    cheb_eig = k carries hi = 1.1 x the estimate, and k = 0 keeps the Gershgorin end hi = 1."""
+    n = 10
+    A = CSR.from_scipy(lap1d(n))
+    est = oracle.power_estimate(A, 4.0 * np.ones(n), 400, seed=7, level=0)
+    assert abs(est - (1 + np.cos(np.pi / (n + 1))) / 2) <= 1e-9
+    lo, hi = 0.2, 2.0
+    lam = np.linspace(lo * hi, hi, 1001)
+    D = CSR.from_scipy(sp.diags(lam).tocsr())
+    for m in (2, 3):
+        x = oracle.smooth(D, np.ones_like(lam), np.zeros_like(lam), np.ones_like(lam), kind=1, degree=m, lo=lo, hi=hi)
+        Tm = np.cosh(m * np.arccosh((1 + lo) / (1 - lo)))
+        assert abs(np.max(np.abs(x)) - 1 / Tm) <= 1e-12
+    prob, J, rhs = tiny_system((12, 10, 1), config=1)
+    bf = oracle.BF(J, smoother=1, cheb_eig=12)
+    for w in (0, 1):
+        for l in range(bf.nlev(w)):
+            L = bf.level(w, l)
+            est = oracle.power_estimate(L["A"], L["dl1"], 12, seed=0x1611, level=l)
+            assert L["cheb_hi"] == 1.1 * est
+    assert all(oracle.BF(J, smoother=1).level(0, l)["cheb_hi"] == 1.0 for l in range(2))

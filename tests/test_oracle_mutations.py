@@ -37,6 +37,10 @@ MUTANTS = [
     ("strength: sign of the diagonal ignored", "strong[q] = (uint8_t)(m > 0.0 && A->ci[q] != i && -sg * A->v[q] >= thr);",
      "strong[q] = (uint8_t)(m > 0.0 && A->ci[q] != i && -A->v[q] >= thr);", 1),
     ("l1 diagonal without absolute values", "s = s + fabs(A->v[q]);", "s = s + A->v[q];", 1),
+    ("Chebyshev interval ignores the estimated upper end hi (R21)",
+     "double theta = hi * (1.0 + lo) / 2.0, delta = hi * (1.0 - lo) / 2.0;",
+     "double theta = (1.0 + lo) / 2.0, delta = (1.0 - lo) / 2.0;", 1),
+    ("power estimate without the D^-1 scaling", "w[i] = w[i] / d[i];", "w[i] = w[i];", 1),
     ("Chebyshev recurrence coefficient 2 rho_new / delta halved",
      "dir[i] = rho_new * rho * dir[i] + (2.0 * rho_new / delta) * ((b[i] - tmp[i]) / d[i]);",
      "dir[i] = rho_new * rho * dir[i] + (rho_new / delta) * ((b[i] - tmp[i]) / d[i]);", 1),
