@@ -107,6 +107,9 @@ typedef struct {
                                   [cheb_lo, 1], 1 the Gershgorin bound of rho(D_l1^-1 A); k > 0 ->
                                   [cheb_lo hi_l, hi_l], hi_l = 1.1 x a k-step power-iteration estimate
                                   of rho(D_l1^-1 A_l) from a fixed hashed start vector (<= 64) */
+  int32_t smoother_p;          /* smoother of the pressure-type hierarchies (1 S~ of BF, 2 A_pp of CPR);
+                                  -1: the same as `smoother`, which always covers the transport-type
+                                  ones (0 A_ss, 3 J) -- DESIGN.md R22 */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;

@@ -49,6 +49,14 @@ void or_default_options(or_options *o) {
   o->interp_norm = 1;     /* R8 */
   o->precond = 0;         /* BF, Algorithm 3 */
   o->cheb_eig = 0;        /* R21: Gershgorin interval end 1 */
+  o->smoother_p = -1;     /* R22 */
+}
+
+/* options of one hierarchy: the pressure-type hierarchies (S~, A_pp) take smoother_p (R22) */
+static or_options hier_options(const or_options *o, int pressure) {
+  or_options h = *o;
+  if (pressure && o->smoother_p >= 0) h.smoother = o->smoother_p;
+  return h;
 }
 
 void or_csr_free(or_csr *A) {
@@ -799,16 +807,17 @@ void or_jscalar(int32_t n, const int64_t *rp, const int32_t *ci, const double *v
 static int build_precond(or_bf *b) {
   const or_options *o = &b->opt;
   int st = 0;
+  const or_options ot = hier_options(o, 0), op = hier_options(o, 1);
   if (o->precond == 3) {
     or_jscalar(b->n, b->brp, b->bci, b->bv, &b->Jsc);
-    return or_amg_setup(&b->Jsc, o, &b->hJ);
+    return or_amg_setup(&b->Jsc, &ot, &b->hJ);
   }
   if (o->precond == 0 || o->precond == 2) {
-    st = or_amg_setup(&b->Ass, o, &b->hss);
+    st = or_amg_setup(&b->Ass, &ot, &b->hss);
     if (st) return st;
   }
-  if (o->precond == 0) return or_amg_setup(&b->S, o, &b->hS);
-  st = or_amg_setup(&b->App, o, &b->hpp);
+  if (o->precond == 0) return or_amg_setup(&b->S, &op, &b->hS);
+  st = or_amg_setup(&b->App, &op, &b->hpp);
   if (st) return st;
   return or_ilu0(b->n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv) ? 4 : 0;
 }
@@ -874,16 +883,17 @@ int or_bf_update(or_bf *b, const double *vals) {
     or_amg *h = hs[k];
     if (h->nlev == 0) continue;                      /* not used by this preconditioner */
     if (h->nlev <= 1) {
+      or_options oh = h->opt;                       /* this hierarchy's options (R22) */
       or_amg_free(h);
-      st = or_amg_setup(A0[k], &b->opt, h);
+      st = or_amg_setup(A0[k], &oh, h);
       if (st) return st;
       continue;
     }
     or_csr_free(&h->A[0]);
     csr_copy(A0[k], &h->A[0]);
     or_l1diag(&h->A[0], h->dl1[0]);
-    if (b->opt.smoother == 1 && b->opt.cheb_eig > 0)   /* R21 on the new finest matrix */
-      h->cheb_hi[0] = 1.1 * or_power_estimate(&h->A[0], h->dl1[0], b->opt.cheb_eig, b->opt.seed, 0);
+    if (h->opt.smoother == 1 && h->opt.cheb_eig > 0)   /* R21 on the new finest matrix */
+      h->cheb_hi[0] = 1.1 * or_power_estimate(&h->A[0], h->dl1[0], h->opt.cheb_eig, h->opt.seed, 0);
   }
   if ((b->opt.precond == 1 || b->opt.precond == 2) && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv))
     return 4;

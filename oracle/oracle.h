@@ -42,6 +42,8 @@ typedef struct {
   int32_t  cheb_eig;       /* Chebyshev interval per level (R21): 0 -> [cheb_lo, 1] (Gershgorin
                               bound of D_l1^-1 A); k > 0 -> [cheb_lo hi_l, hi_l], hi_l = 1.1 x the
                               k-step power-iteration estimate of rho(D_l1^-1 A_l) */
+  int32_t  smoother_p;     /* smoother of the pressure-type hierarchies (S~ for BF, A_pp for CPR);
+                              -1: the same as `smoother` (which then covers A_ss and J) -- R22 */
 } or_options;
 
 #define OR_MAX_LEVELS 64

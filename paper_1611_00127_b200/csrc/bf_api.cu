@@ -321,6 +321,7 @@ bf_status bf_default_options(bf_options *o) {
   o->timing = 0;
   o->precond = 0;
   o->cheb_eig = 0;
+  o->smoother_p = -1;
   return BF_OK;
 }
 
@@ -329,9 +330,11 @@ static const char *check_options(const bf_options *o) {
   if (o->max_levels < 1 || o->max_levels > BF_MAXL) return "max_levels must be in [1, 64]";
   if (o->max_coarse < 1 || o->max_coarse > 128) return "max_coarse must be in [1, 128]";
   if (o->smoother != 0 && o->smoother != 1) return "smoother must be 0 or 1";
+  if (o->smoother_p < -1 || o->smoother_p > 1) return "smoother_p must be -1, 0 or 1";
   if (o->nu_pre < 0 || o->nu_post < 0 || o->nu_pre > 8 || o->nu_post > 8) return "nu_pre/nu_post in [0, 8]";
-  if (o->smoother == 1 && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
-  if (o->smoother == 1 && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
+  const bool cheb = o->smoother == 1 || o->smoother_p == 1;
+  if (cheb && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";
+  if (cheb && !(o->cheb_lo > 0.0 && o->cheb_lo < 1.0)) return "cheb_lo in (0, 1)";
   if (o->orth != 0 && o->orth != 1) return "orth must be 0 or 1";
   if (o->cheb_eig < 0 || o->cheb_eig > 64) return "cheb_eig in [0, 64]";
   if (o->precond < 0 || o->precond > 3)

@@ -43,12 +43,14 @@ struct Level {
   double *dl1 = nullptr;
   double *b = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
   double *d = nullptr;  // 1 / dl1 (smoother scaling)
+  int smoother = 0;      // 0 l1-Jacobi, 1 Chebyshev: the hierarchy's smoother (reading R22)
   double cheb_hi = 1.0;  // upper end of the Chebyshev interval [cheb_lo hi, hi] (reading R21)
   double beta0 = 1.0;    // first smoothing step from zero: x0 = beta0 b ./ dl1 (1/theta for Chebyshev)
 };
 
 struct Hier {
   int nlev = 0;
+  int smoother = 0;       // this hierarchy's smoother (opt.smoother or, pressure-type, opt.smoother_p; R22)
   Level lv[BF_MAXL];
   double *lu = nullptr;  // nL x nL row-major LU (unit lower L below the diagonal)
   int32_t *piv = nullptr;
@@ -235,6 +237,10 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);
 void set_level_beta(const bf_options &o, Level &L);                      // k_vcycle.cu
+// smoother of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp, 3 J): pressure-type ones take smoother_p (R22)
+inline int hier_smoother(const bf_options &o, int which) {
+  return ((which == 1 || which == 2) && o.smoother_p >= 0) ? o.smoother_p : o.smoother;
+}
 void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vcycle.cu
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
 double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu

@@ -1034,7 +1034,7 @@ static void set_cheb_intervals(bf_ctx *c, Hier &h, int only_level = -1) {
   std::vector<int> lv;
   for (int k = 0; k < h.nlev; k++)
     if (only_level < 0 || k == only_level) lv.push_back(k);
-  if (o.smoother == 1 && o.cheb_eig > 0) {
+  if (h.smoother == 1 && o.cheb_eig > 0) {
     double *nrm = dalloc_t<double>(c, 2 * lv.size() + 2);
     double *part = dalloc_t<double>(c, POW_BLOCKS);
     for (size_t q = 0; q < lv.size(); q++) {
@@ -1068,6 +1068,7 @@ static void set_cheb_intervals(bf_ctx *c, Hier &h, int only_level = -1) {
 void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   Hier &h = c->h[which];
   const bf_options &o = c->opt;
+  h.smoother = hier_smoother(o, which);
   copy_csr(c, A0, h.lv[0].A);
   int l = 0;
   int *nU_d = dalloc_t<int>(c, 4);
@@ -1194,6 +1195,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   h.nlev = l + 1;
   for (int k = 0; k < h.nlev; k++) {
     Level &L = h.lv[k];
+    L.smoother = h.smoother;
     int n = L.A.n;
     double *diag = dalloc_t<double>(c, n);
     k_diag<<<div_up(n, 256), 256, 0, c->stream>>>(L.A, diag);
@@ -1266,7 +1268,7 @@ static __global__ void k_rfuse_m(DCsr A, const double *__restrict__ d, double be
 
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
   const bf_options &o = c->opt;
-  if (!c->tune.rfuse || o.smoother != 0 || o.nu_pre != 1) return;
+  if (!c->tune.rfuse || h.smoother != 0 || o.nu_pre != 1) return;
   const bool l0 = c->tune.rfuse_l0;
   int lend = h.dtail >= 0 ? h.dtail : (h.tail >= 0 ? h.tail : h.nlev - 1);
   for (int l = l0 ? 0 : 1; l < lend; l++) {

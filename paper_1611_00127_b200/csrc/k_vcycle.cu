@@ -26,7 +26,7 @@ static void cheb_params(const bf_options &o, const Level &L, double &theta, doub
 void set_level_beta(const bf_options &o, Level &L) {
   double theta, delta;
   cheb_params(o, L, theta, delta);
-  L.beta0 = o.smoother == 1 ? 1.0 / theta : 1.0;
+  L.beta0 = L.smoother == 1 ? 1.0 / theta : 1.0;
 }
 
 // coarsest-level solve x = A_L^-1 b with the inverse formed at setup from the pivoted LU
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
 void plan_tail(bf_ctx *c, Hier &h) {
   const bf_options &o = c->opt;
   h.tail = -1;
-  if (!c->tune.tail || o.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  if (!c->tune.tail || h.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
   int64_t lim = c->tune.tail_nnz;
   int l = h.nlev - 1;
   while (l - 1 >= 0 && h.lv[l - 1].A.nnz <= lim && h.nlev - (l - 1) <= TAIL_MAXL) l--;
@@ -291,7 +291,7 @@ static TailSmoother tail_smoother(const bf_options &o, const Level &L) {
   TailSmoother sm{};
   sm.nu_pre = o.nu_pre;
   sm.nu_post = o.nu_post;
-  if (o.smoother == 0) {
+  if (L.smoother == 0) {
     sm.deg = 1;
     sm.c0 = 1.0;
     return sm;
@@ -590,7 +590,7 @@ static void smooth_pass(bf_ctx *c, Level &L, double *&x, bool first, bool want_r
     x = L.t;
     L.t = tmp;
   };
-  if (o.smoother == 0) {  // x <- x + (b - A x) ./ dl1
+  if (L.smoother == 0) {  // x <- x + (b - A x) ./ dl1
     if (!first) {
       csr_op<OP_SMOOTH>(c, L.A, x, L.b, L.d, L.t, nullptr, 0.0, 1.0, nullptr);
       swap_t();
@@ -647,7 +647,7 @@ static void vcycle_level(bf_ctx *c, Hier &h, int l) {
       BF_LAUNCH(c);
       BF_CUDA(cudaGetLastError());
     } else {  // stalled coarsening: 4 l1-Jacobi sweeps from zero (x0 = b ./ dl1 is the first)
-      if (o.smoother == 1) {  // x0 was seeded for Chebyshev: reseed for l1-Jacobi
+      if (L.smoother == 1) {  // x0 was seeded for Chebyshev: reseed for l1-Jacobi
         k_x0<<<div_up(n, 256), 256, 0, c->stream>>>(n, 1.0, L.b, L.d, L.x);
         BF_LAUNCH(c);
       }
@@ -774,7 +774,7 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   // step 4: S~ p = r by one V-cycle.  With one l1-Jacobi post-sweep on a DIA finest level,
   // that sweep and the merge z = R_p^T p + R_s^T s are one kernel (k_dia_smooth_merge)
   Level &S0 = hS.lv[0];
-  c->fuse_post0 = c->tune.merge_fuse && c->opt.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
+  c->fuse_post0 = c->tune.merge_fuse && hS.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
                   hS.nlev > 1 && hS.dtail != 0 && hS.tail != 0;
   vcycle_level(c, hS, 0);
   if (c->fuse_post0) {
