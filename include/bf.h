@@ -110,6 +110,8 @@ typedef struct {
   int32_t smoother_p;          /* smoother of the pressure-type hierarchies (1 S~ of BF, 2 A_pp of CPR);
                                   -1: the same as `smoother`, which always covers the transport-type
                                   ones (0 A_ss, 3 J) -- DESIGN.md R22 */
+  int32_t cheb_levels;         /* a Chebyshev hierarchy smooths its levels l < cheb_levels with Chebyshev
+                                  and the coarser ones with l1-Jacobi; 0: every level (R22) */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;

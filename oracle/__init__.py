@@ -45,7 +45,8 @@ class Options(C.Structure):
                 ("smoother", C.c_int32), ("nu_pre", C.c_int32), ("nu_post", C.c_int32),
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
                 ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
-                ("precond", C.c_int32), ("cheb_eig", C.c_int32), ("smoother_p", C.c_int32)]
+                ("precond", C.c_int32), ("cheb_eig", C.c_int32), ("smoother_p", C.c_int32),
+                ("cheb_levels", C.c_int32)]
 
 
 MAXL = 64

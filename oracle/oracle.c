@@ -50,6 +50,7 @@ void or_default_options(or_options *o) {
   o->precond = 0;         /* BF, Algorithm 3 */
   o->cheb_eig = 0;        /* R21: Gershgorin interval end 1 */
   o->smoother_p = -1;     /* R22 */
+  o->cheb_levels = 0;     /* R22 */
 }
 
 /* options of one hierarchy: the pressure-type hierarchies (S~, A_pp) take smoother_p (R22) */
@@ -81,6 +82,11 @@ static double diag_sign(const or_csr *A, int32_t i) {
   for (int64_t q = A->rp[i]; q < A->rp[i + 1]; q++)
     if (A->ci[q] == i) return A->v[q] < 0.0 ? -1.0 : 1.0;
   return 1.0;
+}
+
+/* the smoother of level l (R22): Chebyshev on the levels l < cheb_levels of a Chebyshev hierarchy */
+static int level_cheb(const or_options *o, int32_t l) {
+  return o->smoother == 1 && (o->cheb_levels == 0 || l < o->cheb_levels);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -542,7 +548,7 @@ int or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h) {
     h->dl1[k] = (double *)xmalloc((size_t)h->A[k].nrows * sizeof(double) + 8);
     or_l1diag(&h->A[k], h->dl1[k]);
     h->cheb_hi[k] = 1.0;
-    if (o->smoother == 1 && o->cheb_eig > 0)
+    if (level_cheb(o, k) && o->cheb_eig > 0)
       h->cheb_hi[k] = 1.1 * or_power_estimate(&h->A[k], h->dl1[k], o->cheb_eig, o->seed, k);
   }
   /* coarsest level: dense LU with partial pivoting if n_L <= max_coarse (Q28) */
@@ -632,7 +638,7 @@ void or_smooth(const or_csr *A, const double *d, const double *b, double *x, int
 }
 
 static void smooth(const or_amg *h, int32_t l, const double *b, double *x, double *tmp, double *dir) {
-  if (h->opt.smoother == 1)
+  if (level_cheb(&h->opt, l))
     smooth_cheb(&h->A[l], h->dl1[l], b, x, h->opt.cheb_degree, h->opt.cheb_lo, h->cheb_hi[l], tmp, dir);
   else
     smooth_l1(&h->A[l], h->dl1[l], b, x, tmp);
@@ -892,7 +898,7 @@ int or_bf_update(or_bf *b, const double *vals) {
     or_csr_free(&h->A[0]);
     csr_copy(A0[k], &h->A[0]);
     or_l1diag(&h->A[0], h->dl1[0]);
-    if (h->opt.smoother == 1 && h->opt.cheb_eig > 0)   /* R21 on the new finest matrix */
+    if (level_cheb(&h->opt, 0) && h->opt.cheb_eig > 0)   /* R21 on the new finest matrix */
       h->cheb_hi[0] = 1.1 * or_power_estimate(&h->A[0], h->dl1[0], h->opt.cheb_eig, h->opt.seed, 0);
   }
   if ((b->opt.precond == 1 || b->opt.precond == 2) && or_ilu0(n, b->brp, b->bci, b->bv, b->ilu, b->ilu_dinv))

@@ -44,6 +44,8 @@ typedef struct {
                               k-step power-iteration estimate of rho(D_l1^-1 A_l) */
   int32_t  smoother_p;     /* smoother of the pressure-type hierarchies (S~ for BF, A_pp for CPR);
                               -1: the same as `smoother` (which then covers A_ss and J) -- R22 */
+  int32_t  cheb_levels;    /* Chebyshev hierarchies smooth levels l < cheb_levels with Chebyshev and the
+                              coarser ones with l1-Jacobi; 0: every level (R22) */
 } or_options;
 
 #define OR_MAX_LEVELS 64

@@ -1034,7 +1034,9 @@ static void set_cheb_intervals(bf_ctx *c, Hier &h, int only_level = -1) {
   std::vector<int> lv;
   for (int k = 0; k < h.nlev; k++)
     if (only_level < 0 || k == only_level) lv.push_back(k);
-  if (h.smoother == 1 && o.cheb_eig > 0) {
+  bool any_cheb = false;
+  for (int k : lv) any_cheb |= h.lv[k].smoother == 1;
+  if (any_cheb && o.cheb_eig > 0) {
     double *nrm = dalloc_t<double>(c, 2 * lv.size() + 2);
     double *part = dalloc_t<double>(c, POW_BLOCKS);
     for (size_t q = 0; q < lv.size(); q++) {
@@ -1060,7 +1062,8 @@ static void set_cheb_intervals(bf_ctx *c, Hier &h, int only_level = -1) {
     sync(c);
     dfree(c, nrm);
     dfree(c, part);
-    for (size_t q = 0; q < lv.size(); q++) h.lv[lv[q]].cheb_hi = 1.1 * hn[2 * q + 1];
+    for (size_t q = 0; q < lv.size(); q++)
+      if (h.lv[lv[q]].smoother == 1) h.lv[lv[q]].cheb_hi = 1.1 * hn[2 * q + 1];
   }
   for (int k : lv) set_level_beta(o, h.lv[k]);
 }
@@ -1195,7 +1198,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   h.nlev = l + 1;
   for (int k = 0; k < h.nlev; k++) {
     Level &L = h.lv[k];
-    L.smoother = h.smoother;
+    L.smoother = (h.smoother == 1 && (o.cheb_levels == 0 || k < o.cheb_levels)) ? 1 : 0;  // R22
     int n = L.A.n;
     double *diag = dalloc_t<double>(c, n);
     k_diag<<<div_up(n, 256), 256, 0, c->stream>>>(L.A, diag);
@@ -1268,7 +1271,7 @@ static __global__ void k_rfuse_m(DCsr A, const double *__restrict__ d, double be
 
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
   const bf_options &o = c->opt;
-  if (!c->tune.rfuse || h.smoother != 0 || o.nu_pre != 1) return;
+  if (!c->tune.rfuse || o.nu_pre != 1) return;
   const bool l0 = c->tune.rfuse_l0;
   int lend = h.dtail >= 0 ? h.dtail : (h.tail >= 0 ? h.tail : h.nlev - 1);
   for (int l = l0 ? 0 : 1; l < lend; l++) {
@@ -1276,6 +1279,7 @@ void build_rfuse(bf_ctx *c, Hier &h, bool finest_only) {
     Level &L = h.lv[l];
     free_csr(c, L.Rf);
     if (L.A.dia_v && !l0) continue;
+    if (L.smoother != 0) continue;  // Rf fuses ONE l1-Jacobi pre-sweep from zero
     DCsr M;
     M.n = L.A.n;
     M.m = L.A.m;

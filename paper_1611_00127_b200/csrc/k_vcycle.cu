@@ -165,10 +165,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
 void plan_tail(bf_ctx *c, Hier &h) {
   const bf_options &o = c->opt;
   h.tail = -1;
-  if (!c->tune.tail || h.smoother != 0 || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
+  if (!c->tune.tail || o.nu_pre != 1 || o.nu_post != 1 || !h.dense) return;
   int64_t lim = c->tune.tail_nnz;
   int l = h.nlev - 1;
-  while (l - 1 >= 0 && h.lv[l - 1].A.nnz <= lim && h.nlev - (l - 1) <= TAIL_MAXL) l--;
+  // the cooperative tail implements l1-Jacobi V(1,1): only levels smoothed by l1-Jacobi (R22)
+  while (l - 1 >= 0 && h.lv[l - 1].A.nnz <= lim && h.nlev - (l - 1) <= TAIL_MAXL && h.lv[l - 1].smoother == 0) l--;
   if (l < h.nlev - 1) h.tail = l;
 }
 
@@ -774,7 +775,7 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
   // step 4: S~ p = r by one V-cycle.  With one l1-Jacobi post-sweep on a DIA finest level,
   // that sweep and the merge z = R_p^T p + R_s^T s are one kernel (k_dia_smooth_merge)
   Level &S0 = hS.lv[0];
-  c->fuse_post0 = c->tune.merge_fuse && hS.smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
+  c->fuse_post0 = c->tune.merge_fuse && hS.lv[0].smoother == 0 && c->opt.nu_post == 1 && S0.A.dia_v && S0.A.dia_k <= 16 &&
                   hS.nlev > 1 && hS.dtail != 0 && hS.tail != 0;
   vcycle_level(c, hS, 0);
   if (c->fuse_post0) {
