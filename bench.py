@@ -451,10 +451,10 @@ def run_ours(args):
     alt = None
     if not args.no_e2e:
         alt = []
-        for name, kw in (("BF, chebyshev(2) on [0.3,1] smoother (option smoother=1)", dict(smoother=1)),
-                         ("BF, chebyshev(2) on [0.1,1] smoother (options smoother=1, cheb_lo=0.1)",
-                          dict(smoother=1, cheb_lo=0.1)),
-                         ("CPR-AMG(1) combinative, ILU(0) + A_pp V-cycle (option precond=1)", dict(precond=1)),
+        for name, kw in (("BF, l1-Jacobi V(1,1) on both hierarchies (round-1 default; option smoother=0)",
+                          dict(smoother=0)),
+                         ("BF, Chebyshev(2) on [0.15,1] on both hierarchies (options smoother_p=-1, cheb_lo=0.15)",
+                          dict(smoother_p=-1, cheb_lo=0.15)),
                          ("CPR-AMG(2) additive, ILU(0) + A_pp, A_ss V-cycles (option precond=2)", dict(precond=2))):
             o2 = bf.bf_default_options(timing=1, **kw)
             torch.cuda.synchronize()

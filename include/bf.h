@@ -80,10 +80,11 @@ typedef struct {
   double theta;                /* strength threshold (R4), default 0.25 */
   int32_t max_levels;          /* default 25 */
   int32_t max_coarse;          /* coarsest level dense-LU size limit, default 64, max 128 */
-  int32_t smoother;            /* 0 l1-Jacobi (default), 1 Chebyshev (R5) */
+  int32_t smoother;            /* smoother of the A_ss hierarchy (0): 0 l1-Jacobi, 1 Chebyshev (default;
+                                  DESIGN.md R9, R22) */
   int32_t nu_pre, nu_post;     /* smoothing passes, default 1, 1 */
   int32_t cheb_degree;         /* Chebyshev degree, default 2 */
-  double cheb_lo;              /* Chebyshev interval [cheb_lo, 1] on D_l1^-1 A, default 0.3 */
+  double cheb_lo;              /* Chebyshev interval [cheb_lo, 1] on D_l1^-1 A, default 0.1 */
   uint64_t seed;               /* PMIS hash seed, default 0x1611 */
   int32_t orth;                /* 0 CGS2 (default), 1 CGS1 */
   int32_t schur_as_printed;    /* 0: A_sp (default, R1); 1: literal P:L239 (A_pp), diagnostics only */
@@ -107,9 +108,9 @@ typedef struct {
                                   [cheb_lo, 1], 1 the Gershgorin bound of rho(D_l1^-1 A); k > 0 ->
                                   [cheb_lo hi_l, hi_l], hi_l = 1.1 x a k-step power-iteration estimate
                                   of rho(D_l1^-1 A_l) from a fixed hashed start vector (<= 64) */
-  int32_t smoother_p;          /* smoother of the pressure-type hierarchies (1 S~ of BF, 2 A_pp of CPR);
-                                  -1: the same as `smoother`, which always covers the transport-type
-                                  ones (0 A_ss, 3 J) -- DESIGN.md R22 */
+  int32_t smoother_p;          /* smoother of every other hierarchy (1 S~ of BF, 2 A_pp of CPR, 3 J of the
+                                  coupled AMG): default 0 (l1-Jacobi); -1: the same as `smoother`
+                                  -- DESIGN.md R22 */
   int32_t cheb_levels;         /* a Chebyshev hierarchy smooths its levels l < cheb_levels with Chebyshev
                                   and the coarser ones with l1-Jacobi; 0: every level (R22) */
 } bf_options;

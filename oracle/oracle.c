@@ -38,22 +38,22 @@ void or_default_options(or_options *o) {
   o->theta = 0.25;        /* Q24 */
   o->max_levels = 25;     /* Q28 */
   o->max_coarse = 64;     /* Q28 */
-  o->smoother = 0;        /* Q27: l1-Jacobi */
+  o->smoother = 1;        /* Q27, R22: Chebyshev(2) on [0.1, 1] for A_ss ... */
   o->nu_pre = 1;
   o->nu_post = 1;
   o->cheb_degree = 2;
-  o->cheb_lo = 0.3;
+  o->cheb_lo = 0.1;
   o->seed = 0x1611ULL;
   o->orth = 0;            /* Q30: CGS2 */
   o->schur_as_printed = 0;/* Q21 */
   o->interp_norm = 1;     /* R8 */
   o->precond = 0;         /* BF, Algorithm 3 */
   o->cheb_eig = 0;        /* R21: Gershgorin interval end 1 */
-  o->smoother_p = -1;     /* R22 */
+  o->smoother_p = 0;      /* ... and l1-Jacobi for S~ / A_pp / J (R22) */
   o->cheb_levels = 0;     /* R22 */
 }
 
-/* options of one hierarchy: the pressure-type hierarchies (S~, A_pp) take smoother_p (R22) */
+/* options of one hierarchy: every hierarchy but A_ss (S~, A_pp, J) takes smoother_p (R22) */
 static or_options hier_options(const or_options *o, int pressure) {
   or_options h = *o;
   if (pressure && o->smoother_p >= 0) h.smoother = o->smoother_p;
@@ -816,7 +816,7 @@ static int build_precond(or_bf *b) {
   const or_options ot = hier_options(o, 0), op = hier_options(o, 1);
   if (o->precond == 3) {
     or_jscalar(b->n, b->brp, b->bci, b->bv, &b->Jsc);
-    return or_amg_setup(&b->Jsc, &ot, &b->hJ);
+    return or_amg_setup(&b->Jsc, &op, &b->hJ);
   }
   if (o->precond == 0 || o->precond == 2) {
     st = or_amg_setup(&b->Ass, &ot, &b->hss);

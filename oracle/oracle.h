@@ -27,10 +27,10 @@ typedef struct {
   double   theta;          /* strength threshold (Q24), 0.25 */
   int32_t  max_levels;     /* 25 (Q28) */
   int32_t  max_coarse;     /* 64 (Q28) */
-  int32_t  smoother;       /* 0 l1-Jacobi, 1 Chebyshev (Q27) */
+  int32_t  smoother;       /* 0 l1-Jacobi, 1 Chebyshev (Q27): the A_ss hierarchy (R22; default 1) */
   int32_t  nu_pre, nu_post;/* 1, 1 */
   int32_t  cheb_degree;    /* 2 */
-  double   cheb_lo;        /* 0.3 */
+  double   cheb_lo;        /* 0.1 (R22) */
   uint64_t seed;           /* PMIS hash seed (Q25) */
   int32_t  orth;           /* 0 CGS2, 1 CGS1 (Q30) */
   int32_t  schur_as_printed; /* 0: A_sp (Q21); 1: literal P:L239 (A_pp) */
@@ -42,8 +42,8 @@ typedef struct {
   int32_t  cheb_eig;       /* Chebyshev interval per level (R21): 0 -> [cheb_lo, 1] (Gershgorin
                               bound of D_l1^-1 A); k > 0 -> [cheb_lo hi_l, hi_l], hi_l = 1.1 x the
                               k-step power-iteration estimate of rho(D_l1^-1 A_l) */
-  int32_t  smoother_p;     /* smoother of the pressure-type hierarchies (S~ for BF, A_pp for CPR);
-                              -1: the same as `smoother` (which then covers A_ss and J) -- R22 */
+  int32_t  smoother_p;     /* smoother of every other hierarchy (S~ of BF, A_pp of CPR, J of the coupled
+                              AMG), default 0 (l1-Jacobi); -1: the same as `smoother` -- R22 */
   int32_t  cheb_levels;    /* Chebyshev hierarchies smooth levels l < cheb_levels with Chebyshev and the
                               coarser ones with l1-Jacobi; 0: every level (R22) */
 } or_options;

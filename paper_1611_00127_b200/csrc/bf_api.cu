@@ -309,11 +309,11 @@ bf_status bf_default_options(bf_options *o) {
   o->theta = 0.25;
   o->max_levels = 25;
   o->max_coarse = 64;
-  o->smoother = 0;
+  o->smoother = 1;  // R22: Chebyshev(2) on [0.1, 1] for A_ss, l1-Jacobi for S~ (and A_pp, J)
   o->nu_pre = 1;
   o->nu_post = 1;
   o->cheb_degree = 2;
-  o->cheb_lo = 0.3;
+  o->cheb_lo = 0.1;
   o->seed = 0x1611ULL;
   o->orth = 0;
   o->schur_as_printed = 0;
@@ -321,7 +321,7 @@ bf_status bf_default_options(bf_options *o) {
   o->timing = 0;
   o->precond = 0;
   o->cheb_eig = 0;
-  o->smoother_p = -1;
+  o->smoother_p = 0;
   o->cheb_levels = 0;
   return BF_OK;
 }

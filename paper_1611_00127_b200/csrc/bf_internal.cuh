@@ -237,9 +237,9 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0);             // k_amg
 void free_hierarchy(bf_ctx *c, Hier &h);
 void plan_tail(bf_ctx *c, Hier &h);
 void set_level_beta(const bf_options &o, Level &L);                      // k_vcycle.cu
-// smoother of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp, 3 J): pressure-type ones take smoother_p (R22)
+// smoother of hierarchy `which` (0 A_ss, 1 S~, 2 A_pp, 3 J): all but A_ss take smoother_p (R22)
 inline int hier_smoother(const bf_options &o, int which) {
-  return ((which == 1 || which == 2) && o.smoother_p >= 0) ? o.smoother_p : o.smoother;
+  return (which != 0 && o.smoother_p >= 0) ? o.smoother_p : o.smoother;
 }
 void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vcycle.cu
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu

@@ -54,6 +54,12 @@ def test_default_options_without_gpu():
     o = bf_default_options()
     assert o.theta == 0.25 and o.max_coarse == 64 and o.nu_pre == 1 and o.interp_norm == 1
     assert o.precond == 0  # BF (Algorithm 3); 1, 2 CPR-AMG(1)/(2), 3 coupled AMG
+    # R22: Chebyshev(2) on [0.1, 1] for A_ss, l1-Jacobi for S~ (and A_pp, J); the oracle agrees
+    assert (o.smoother, o.smoother_p, o.cheb_degree, o.cheb_lo, o.cheb_levels, o.cheb_eig) == (1, 0, 2, 0.1, 0, 0)
+    import oracle
+    oo = oracle.default_options()
+    for f, _ in oracle.Options._fields_:
+        assert getattr(oo, f) == getattr(o, f), f
     # the binding's struct mirrors include/bf.h field by field (a missing field would shift the rest)
     import ctypes
     from paper_1611_00127_b200 import binding

@@ -202,11 +202,14 @@ def test_c4_full_size():
     _forced(g, o, rhs, 30)
 
 
-def test_c3_chebyshev_full_size(c3):
-    """The Chebyshev(2) smoother on [0.1, 1] (option smoother=1, reading R9) at full C3 size:
-    hierarchies bit-exact, one BF apply <= 1e-10 and 30 forced GMRES iterations <= 1e-6."""
+@pytest.mark.parametrize("opts", [dict(smoother=0), dict(smoother=1, smoother_p=-1, cheb_lo=0.15)],
+                         ids=["l1-everywhere", "chebyshev-everywhere"])
+def test_c3_other_smoothers_full_size(c3, opts):
+    """The other smoother configurations at full C3 size (the default, Chebyshev(2) on A_ss and
+    l1-Jacobi on S~ (reading R22), is covered by the tests above): l1-Jacobi on both hierarchies
+    (round 1's default) and Chebyshev(2) on both: one BF apply and each V-cycle <= 1e-10 and 30
+    forced GMRES iterations <= 1e-6 against the oracle."""
     prob, J, rhs, g0, o0 = c3
-    opts = dict(smoother=1, cheb_lo=0.1)
     g = gpu_solver(J, prob.dims, **opts)
     o = oracle.BF(J, **opts)
     N = 2 * J.n

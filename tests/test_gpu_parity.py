@@ -132,7 +132,7 @@ def test_host_pointers_and_layout_options():
 def test_options_parity():
     """Non-default options are implemented identically on both sides."""
     prob, J, rhs = make_system(2, dims=(10, 9, 8))
-    for opts in (dict(smoother=1), dict(interp_norm=0), dict(orth=1), dict(nu_pre=2, nu_post=2),
+    for opts in (dict(smoother=0), dict(smoother=1, smoother_p=-1, cheb_lo=0.3), dict(interp_norm=0), dict(orth=1), dict(nu_pre=2, nu_post=2),
                  dict(theta=0.5, max_coarse=30), dict(schur_as_printed=1), dict(nu_pre=0),
                  dict(smoother=1, cheb_lo=0.1, cheb_eig=10), dict(smoother=1, cheb_degree=3, cheb_eig=4, nu_pre=2),
                  dict(smoother=1, smoother_p=0, cheb_lo=0.1), dict(smoother=0, smoother_p=1, cheb_levels=2),

@@ -373,12 +373,16 @@ def test_poisson_convergence_factor():
     PMIS + classical interpolation + l1-Jacobi (l1-Jacobi on the Laplacian is Jacobi damped by
     1/2, smoothing factor 3/4): 2D <= 0.75, 3D <= 0.70, growth <= +0.05 per refinement."""
     for d, sizes, bound in ((2, (32, 64, 128), 0.75), (3, (16, 32), 0.70)):
-        f = []
+        f, fc = [], []
         for m in sizes:
             A = lap(m, d)
-            f.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A))))
+            f.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=0)))
+            fc.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=1, cheb_lo=0.1)))
         assert max(f) <= bound, (d, f)
         assert all(f[i + 1] <= f[i] + 0.05 for i in range(len(f) - 1)), (d, f)
+        # Chebyshev(2) on [0.1, 1] (R22) is the stronger smoother at every size (2D: 0.52 / 0.60 / 0.72
+        # against l1-Jacobi's 0.70 / 0.72 / 0.74; its advantage shrinks with refinement)
+        assert all(c < a for c, a in zip(fc, f)), (d, fc, f)
 
 
 # ---------------------------------------------------------------------------- GMRES / whole solve
@@ -684,7 +688,7 @@ def test_chebyshev_interval_from_power_estimate():
         Tm = np.cosh(m * np.arccosh((1 + lo) / (1 - lo)))
         assert abs(np.max(np.abs(x)) - 1 / Tm) <= 1e-12
     prob, J, rhs = tiny_system((12, 10, 1), config=1)
-    bf = oracle.BF(J, smoother=1, cheb_eig=12)
+    bf = oracle.BF(J, smoother=1, smoother_p=-1, cheb_eig=12)
     for w in (0, 1):
         for l in range(bf.nlev(w)):
             L = bf.level(w, l)
