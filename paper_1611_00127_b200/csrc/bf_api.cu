@@ -214,6 +214,7 @@ Tuning tuning_from_env() {
   t.tail = !env_flag("BF_NO_TAIL");
   t.tail_nnz = (int64_t)env_num("BF_TAIL_NNZ", (double)t.tail_nnz);
   t.tail_bps = std::max(1, (int)env_num("BF_TAIL_BPS", t.tail_bps));
+  t.reorder = !env_flag("BF_NO_REORDER");
   t.dtail = !env_flag("BF_NO_DTAIL");
   t.dtail_n = (int)env_num("BF_DTAIL_N", t.dtail_n);
   t.rfuse = !env_flag("BF_NO_RFUSE");
@@ -635,13 +636,16 @@ bf_status bf_get_level(bf_handle c, int32_t which, int32_t level, int32_t *n, in
   BF_GUARD_BEGIN
   const Level &L = c->h[which].lv[level];
   bool coarsest = level == c->h[which].nlev - 1;
-  if (n) *n = L.A.n;
-  if (nnz_A) *nnz_A = L.A.nnz;
-  if (nnz_P) *nnz_P = coarsest ? 0 : L.P.nnz;
-  copy_csr_out(c, L.A, A_rowptr, A_col, A_val);
+  // the construction (= oracle) numbering: the copies kept when the solve-phase operators were renumbered
+  const DCsr &A = L.A_io.n ? L.A_io : L.A;
+  const DCsr &P = L.P_io.n ? L.P_io : L.P;
+  if (n) *n = A.n;
+  if (nnz_A) *nnz_A = A.nnz;
+  if (nnz_P) *nnz_P = coarsest ? 0 : P.nnz;
+  copy_csr_out(c, A, A_rowptr, A_col, A_val);
   if (!coarsest) {
-    if (cf) BF_CUDA(cudaMemcpyAsync(cf, L.cf, L.A.n, cudaMemcpyDeviceToHost, c->stream));
-    copy_csr_out(c, L.P, P_rowptr, P_col, P_val);
+    if (cf) BF_CUDA(cudaMemcpyAsync(cf, L.cf, A.n, cudaMemcpyDeviceToHost, c->stream));
+    copy_csr_out(c, P, P_rowptr, P_col, P_val);
   }
   if (dl1) BF_CUDA(cudaMemcpyAsync(dl1, L.dl1, sizeof(double) * L.A.n, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));

@@ -37,7 +37,10 @@ struct DCsr {
 };
 
 struct Level {
-  DCsr A, P, R;
+  DCsr A, P, R;          // the solve-phase operators (coarse levels renumbered for locality, below)
+  DCsr A_io, P_io;       // the hierarchy in the construction (= oracle) numbering when A / P were
+                         // renumbered (k_amg_setup.cu reorder_levels); empty otherwise
+  int32_t *perm = nullptr;  // solve-phase position -> construction index of this level's points
   DCsr Rf;  // fused restriction R (I - beta A D^-1) of the seeded pre-smoother's residual (k_amg_setup.cu)
   int8_t *cf = nullptr;
   double *dl1 = nullptr;
@@ -75,6 +78,7 @@ struct Tuning {
   bool tail = true;         // cooperative single-kernel V-cycle tail
   int64_t tail_nnz = 3000;  // levels with at most this many nonzeros go to the cooperative tail
   int tail_bps = 1;         // cooperative tail CTAs per SM
+  bool reorder = true;      // coarse levels renumbered in (x/8, y, z)-Morton order for gather locality
   bool dtail = true;        // dense tail operator below dtail_n rows
   int dtail_n = 2048;
   bool rfuse = true;        // fused restriction R (I - beta A D) on the CSR levels
@@ -225,6 +229,7 @@ struct NvtxRange {
 int64_t exclusive_scan_i32(bf_ctx *c, const int32_t *counts, int32_t *out, int32_t n);
 int64_t exclusive_scan_i64(bf_ctx *c, const int64_t *counts, int64_t *out, int64_t n);
 void sort_pairs_u64_f64(bf_ctx *c, uint64_t *keys, double *vals, int64_t count, int end_bit);
+void sort_pairs_u64_i32(bf_ctx *c, uint64_t *keys, int32_t *vals, int64_t count, int end_bit);
 
 // ---- setup kernels -----------------------------------------------------------------
 void validate_and_ingest(bf_ctx *c, const bf_bsr2 *J);                 // k_split.cu

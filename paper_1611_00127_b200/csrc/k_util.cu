@@ -65,4 +65,25 @@ void sort_pairs_u64_f64(bf_ctx *c, uint64_t *keys, double *vals, int64_t count, 
   dfree(c, v2);
 }
 
+// stable radix sort of (key, int32 value) pairs by the low end_bit bits of the key (in place)
+void sort_pairs_u64_i32(bf_ctx *c, uint64_t *keys, int32_t *vals, int64_t count, int end_bit) {
+  if (count <= 1) return;
+  uint64_t *k2 = dalloc_t<uint64_t>(c, count);
+  int32_t *v2 = dalloc_t<int32_t>(c, count);
+  cub::DoubleBuffer<uint64_t> kb(keys, k2);
+  cub::DoubleBuffer<int32_t> vb(vals, v2);
+  size_t tmp = 0;
+  BF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, count, 0, end_bit, c->stream));
+  void *t = dalloc(c, tmp + 16);
+  BF_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, count, 0, end_bit, c->stream));
+  c->launches += 4;
+  if (kb.Current() != keys) {
+    BF_CUDA(cudaMemcpyAsync(keys, kb.Current(), sizeof(uint64_t) * count, cudaMemcpyDeviceToDevice, c->stream));
+    BF_CUDA(cudaMemcpyAsync(vals, vb.Current(), sizeof(int32_t) * count, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  dfree(c, t);
+  dfree(c, k2);
+  dfree(c, v2);
+}
+
 }  // namespace bf

@@ -794,14 +794,21 @@ void bf_apply(bf_ctx *c, const double *v, double *z, const double *nrm2) {
 
 // algorithmic bytes of one BF apply, SURVEY.md 8(d)'s per-unit figures on the actual
 // hierarchies: per level l < L of each V(1,1) 24 nnz(A_l) + 24 nnz(P_l) + 116 n_l + 12 n_{l+1},
+// plus 12 nnz(A_l) + 36 n_l per extra sweep (a pass of a degree-m smoother is m sweeps, the first
+// one from zero free: m (nu_pre + nu_post) products with A_l per level, of which V(1,1) counts 2),
 // the coarsest solve 8 n_L^2, the A_ps coupling 12 nnz(A_ps) + 36 n, split + merge 64 n.
 // Independent of the kernels' own storage (DIA, fused restriction), like the J SpMV's 36 B/block.
 double apply_model_bytes(bf_ctx *c) {
+  const bf_options &o = c->opt;
   double bytes = 12.0 * c->blk[1].nnz + 36.0 * c->n + 64.0 * c->n;
   for (int w = 0; w < 2; w++) {
     Hier &h = c->h[w];
-    for (int l = 0; l + 1 < h.nlev; l++)
-      bytes += 24.0 * h.lv[l].A.nnz + 24.0 * h.lv[l].P.nnz + 116.0 * h.lv[l].A.n + 12.0 * h.lv[l + 1].A.n;
+    for (int l = 0; l + 1 < h.nlev; l++) {
+      const int m = h.lv[l].smoother == 1 ? o.cheb_degree : 1;
+      const double extra = std::max(0, m * (o.nu_pre + o.nu_post) - 2);
+      bytes += 24.0 * h.lv[l].A.nnz + 24.0 * h.lv[l].P.nnz + 116.0 * h.lv[l].A.n + 12.0 * h.lv[l + 1].A.n +
+               extra * (12.0 * h.lv[l].A.nnz + 36.0 * h.lv[l].A.n);
+    }
     bytes += 8.0 * h.nL * h.nL;
   }
   return bytes;

@@ -346,6 +346,7 @@ VARIANTS = {
     "rfuse-l0": {"BF_RFUSE_L0": "1"},
     "plain": {"BF_NO_DTAIL": "1", "BF_NO_RFUSE": "1", "BF_NO_TAIL": "1", "BF_NO_DIA": "1", "BF_NO_TMA": "1"},
     "coop-tail-big": {"BF_NO_DTAIL": "1", "BF_TAIL_NNZ": "200000"},
+    "no-reorder": {"BF_NO_REORDER": "1"},
 }
 
 

@@ -40,7 +40,11 @@ def load(path):
 
 def summarise(path):
     ls = load(path)
-    first = next(i for i, d in enumerate(ls) if d["name"] in SPMV)
+    # the last step's solve only (with --warm k the list holds k+1 setups + solves): from the first J
+    # SpMV after the last setup kernel
+    last_setup = max((i for i, d in enumerate(ls) if d["name"].startswith(("k_pmis", "k_spgemm", "k_interp"))),
+                     default=-1)
+    first = next(i for i, d in enumerate(ls) if i > last_setup and d["name"] in SPMV)
     by = collections.defaultdict(float)
     cnt = collections.Counter()
     for d in ls[first:]:
