@@ -1155,6 +1155,39 @@ static __global__ void k_perm_fill(int n, const int32_t *__restrict__ rp, const 
   }
 }
 
+// the same with a warp per row: each entry's position is its rank among the row's new column
+// indices (distinct within a row), from a shared-memory copy of the row; rows longer than
+// PERM_WARP_MAX take the serial path above (flagged in `longrow`)
+constexpr int PERM_WARP_MAX = 256;
+static __global__ void __launch_bounds__(256) k_perm_fill_warp(int n, const int32_t *__restrict__ rp,
+                                                               const int32_t *__restrict__ ci,
+                                                               const double *__restrict__ v,
+                                                               const int32_t *__restrict__ rperm,
+                                                               const int32_t *__restrict__ cinv,
+                                                               const int32_t *__restrict__ brp, int32_t *bci,
+                                                               double *bv, int *longrow) {
+  __shared__ int32_t cols[8][PERM_WARP_MAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp;
+  if (i >= n) return;
+  const int r = rperm ? rperm[i] : i;
+  const int q0 = rp[r], len = rp[r + 1] - q0, o = brp[i];
+  if (len > PERM_WARP_MAX) {
+    if (lane == 0) *longrow = 1;
+    return;
+  }
+  int32_t *sc = cols[warp];
+  for (int e = lane; e < len; e += 32) sc[e] = cinv ? cinv[ci[q0 + e]] : ci[q0 + e];
+  __syncwarp();
+  for (int e = lane; e < len; e += 32) {
+    const int col = sc[e];
+    int rank = 0;
+    for (int k = 0; k < len; k++) rank += sc[k] < col;
+    bci[o + rank] = col;
+    bv[o + rank] = v[q0 + e];
+  }
+}
+
 static void permute_csr(bf_ctx *c, const DCsr &A, const int32_t *rperm, const int32_t *cinv, DCsr &B) {
   B = DCsr();
   B.n = A.n;
@@ -1166,15 +1199,27 @@ static void permute_csr(bf_ctx *c, const DCsr &A, const int32_t *rperm, const in
   dfree(c, cnt);
   B.ci = dalloc_t<int32_t>(c, B.nnz);
   B.v = dalloc_t<double>(c, B.nnz);
-  k_perm_fill<<<div_up(A.n, 128), 128, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, rperm, cinv, B.rp, B.ci, B.v);
-  c->launches += 2;
+  int *longrow = dalloc_t<int>(c, 1);
+  BF_CUDA(cudaMemsetAsync(longrow, 0, sizeof(int), c->stream));
+  k_perm_fill_warp<<<div_up(A.n, 8), 256, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, rperm, cinv, B.rp, B.ci, B.v,
+                                                          longrow);
+  int hl = 0;
+  BF_CUDA(cudaMemcpyAsync(&hl, longrow, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, longrow);
+  if (hl)  // a row longer than the warp kernel's buffer: the serial kernel redoes every row
+    k_perm_fill<<<div_up(A.n, 128), 128, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, rperm, cinv, B.rp, B.ci, B.v);
+  c->launches += 2 + hl;
   BF_CUDA(cudaGetLastError());
 }
 
 static void reorder_levels(bf_ctx *c, int which, Hier &h) {
   const int64_t ncell = (int64_t)c->nx * c->ny * c->nz;
   const int shift = which == 3 ? 1 : 0;
-  const int last = h.nlev - 2;  // levels 1 .. last are renumbered
+  // levels 1 .. last are renumbered: not the coarsest, and not the small latency-bound levels
+  // (below 16K rows nothing is gained and every renumbered level costs setup time)
+  int last = h.nlev - 2;
+  while (last >= 1 && h.lv[last].A.n < 16384) last--;
   if (!c->tune.reorder || last < 1 || c->nx <= 0 || ((int64_t)h.lv[0].A.n >> shift) != ncell ||
       (shift && (h.lv[0].A.n & 1)))
     return;

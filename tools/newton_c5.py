@@ -13,8 +13,12 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", type=int, default=5)
 p.add_argument("--dims", type=str, default=None)
 p.add_argument("--steps", type=int, default=5)
-p.add_argument("--maxit", type=int, default=600)
+p.add_argument("--maxit", type=int, default=2500)
+p.add_argument("--restart", type=int, default=200)
+p.add_argument("--opts", type=str, default="", help="bf_options, e.g. cheb_degree=3,cheb_lo=0.05")
 a = p.parse_args()
+_val = lambda v: float(v) if ("." in v or "e" in v) else int(v)
+OPT = bf.bf_default_options(**{k: _val(v) for k, v in (kv.split("=") for kv in a.opts.split(",") if kv)})
 dims = tuple(int(x) for x in a.dims.split(",")) if a.dims else None
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
 ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -29,28 +33,28 @@ def solve(k, J, rhs):
     x = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
     e0, e1, e2 = ev(), ev(), ev()
     e0.record()
-    h = bf.bf_setup(rp, ci, v, dims_k)
+    h = bf.bf_setup(rp, ci, v, dims_k, opt=OPT)
     e1.record()
-    r = bf.bf_solve(h, b, x, 1e-8, 30, a.maxit)
+    r = bf.bf_solve(h, b, x, 1e-8, a.restart, a.maxit)
     e2.record()
     torch.cuda.synchronize()
     out.update(full_setup_ms=e0.elapsed_time(e1), full_solve_ms=e1.elapsed_time(e2), full_iters=r["iters"],
-               full_relres=r["relres"])
+               full_relres=r["relres"], full_converged=r["converged"])
     bf.bf_destroy(h)
     # (b) reuse: setup once at k = 0, bf_update afterwards
     x2 = torch.zeros(2 * J.n, dtype=torch.float64, device="cuda")
     e0, e1, e2 = ev(), ev(), ev()
     e0.record()
     if reuse["h"] is None:
-        reuse["h"] = bf.bf_setup(rp, ci, v, dims_k)
+        reuse["h"] = bf.bf_setup(rp, ci, v, dims_k, opt=OPT)
     else:
         bf.bf_update(reuse["h"], v)
     e1.record()
-    r2 = bf.bf_solve(reuse["h"], b, x2, 1e-8, 30, a.maxit)
+    r2 = bf.bf_solve(reuse["h"], b, x2, 1e-8, a.restart, a.maxit)
     e2.record()
     torch.cuda.synchronize()
     out.update(reuse_setup_ms=e0.elapsed_time(e1), reuse_solve_ms=e1.elapsed_time(e2), reuse_iters=r2["iters"],
-               reuse_relres=r2["relres"])
+               reuse_relres=r2["relres"], reuse_converged=r2["converged"])
     rec.append(out)
     print(json.dumps(out), file=sys.stderr, flush=True)
     return x.cpu().numpy()
@@ -63,10 +67,12 @@ for k, prob, J, rhs, fn in newton_sequence(a.config, a.steps, solve, dims=dims):
     dims_k = prob.dims
     fnorms.append(fn)
 tot = lambda key: sum(r[key] for r in rec)
-print(json.dumps({"config": a.config, "dims": dims_k, "steps": a.steps, "dof": 2 * prob.n, "newton_F_norms": fnorms,
+print(json.dumps({"config": a.config, "dims": dims_k, "steps": a.steps, "dof": 2 * prob.n, "restart": a.restart,
+                  "opts": a.opts, "newton_F_norms": fnorms,
                   "full_total_ms": tot("full_setup_ms") + tot("full_solve_ms"),
                   "reuse_total_ms": tot("reuse_setup_ms") + tot("reuse_solve_ms"),
                   "full_setup_ms": tot("full_setup_ms"), "reuse_setup_ms": tot("reuse_setup_ms"),
                   "full_iters": [r["full_iters"] for r in rec], "reuse_iters": [r["reuse_iters"] for r in rec],
                   "full_relres": [r["full_relres"] for r in rec], "reuse_relres": [r["reuse_relres"] for r in rec],
+                  "full_converged": [r["full_converged"] for r in rec], "reuse_converged": [r["reuse_converged"] for r in rec],
                   "wall_s": time.perf_counter() - t0}))
