@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbf.so")
+# BF_LIB=checked loads the checked build (device-side bounds / progress checks, build.py --checked)
+LIB_PATH = os.path.join(_HERE, "libbf_checked.so" if os.environ.get("BF_LIB") == "checked" else "libbf.so")
 
 BF_OK = 0
 STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_PATTERN", 3: "BF_ERR_NONFINITE", 4: "BF_ERR_ZERO_DIAG",

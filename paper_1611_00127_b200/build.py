@@ -20,6 +20,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 SO = os.path.join(PKG, "libbf.so")
+# the checked variant (-DBF_CHECKED: device-side bounds / progress checks, matrix validation; see
+# bf_internal.cuh) for the memory-safety runs; loaded instead of libbf.so when BF_LIB=checked
+SO_CHECKED = os.path.join(PKG, "libbf_checked.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -43,15 +46,17 @@ def _deps_mtime():
     return max(os.path.getmtime(f) for f in files)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _deps_mtime():
-        return SO
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    so = SO_CHECKED if checked else SO
+    bdir = BUILD + ("_checked" if checked else "")
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= _deps_mtime():
+        return so
+    os.makedirs(bdir, exist_ok=True)
     nv = nvcc()
 
     def compile_one(f):
-        obj = os.path.join(BUILD, f[:-3] + ".o")
-        flags = list(NVFLAGS)
+        obj = os.path.join(bdir, f[:-3] + ".o")
+        flags = list(NVFLAGS) + (["-DBF_CHECKED"] if checked else [])
         if f in NOFMA:
             flags.append("--fmad=false")
         cmd = [nv, *flags, "-c", os.path.join(CSRC, f), "-o", obj]
@@ -65,14 +70,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = SO + ".tmp%d" % os.getpid()
+    tmp = so + ".tmp%d" % os.getpid()
     cmd = [nv, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

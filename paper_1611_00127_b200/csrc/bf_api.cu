@@ -13,6 +13,7 @@
 #include <string>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("bf_api.cu")
 
 static thread_local std::string g_setup_err;
 
@@ -197,6 +198,96 @@ void timer_flush(bf_ctx *c) {
     }
     t.pending.clear();
   }
+}
+
+// ---- checked build --------------------------------------------------------------------
+#ifdef BF_CHECKED
+static std::vector<std::pair<unsigned (*)(), const char *>> &check_registry() {
+  static std::vector<std::pair<unsigned (*)(), const char *>> r;
+  return r;
+}
+int register_check_reader(unsigned (*reader)(), const char *tu) {
+  check_registry().emplace_back(reader, tu);
+  return 1;
+}
+static __global__ void k_check_csr(DCsr A, int *bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && (A.rp[0] != 0 || A.rp[A.n] != A.nnz)) atomicCAS(bad, 0, -1);
+  if (i >= A.n) return;
+  int lo = A.rp[i], hi = A.rp[i + 1];
+  if (hi < lo || lo < 0 || hi > A.nnz) {
+    atomicCAS(bad, 0, i + 1);
+    return;
+  }
+  for (int q = lo; q < hi; q++)
+    if (A.ci[q] < 0 || A.ci[q] >= A.m || (q > lo && A.ci[q] <= A.ci[q - 1])) atomicCAS(bad, 0, i + 1);
+}
+#endif
+
+void check_csr(bf_ctx *c, const DCsr &A, const char *what) {
+#ifdef BF_CHECKED
+  if (A.n == 0 || !A.rp) return;
+  int *bad = dalloc_t<int>(c, 1);
+  BF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  k_check_csr<<<div_up(A.n, 256), 256, 0, c->stream>>>(A, bad);
+  int hb = 0;
+  BF_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(c, bad);
+  if (hb)
+    throw Error(BF_ERR_CUDA, std::string("checked build: malformed CSR ") + what +
+                                 (hb < 0 ? " (row pointer ends)" : " at row " + std::to_string(hb - 1)));
+#else
+  (void)c, (void)A, (void)what;
+#endif
+}
+
+void check_device_flags(bf_ctx *c, const char *call) {
+#ifdef BF_CHECKED
+  BF_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto &r : check_registry()) {
+    unsigned line = r.first();
+    if (line)
+      throw Error(BF_ERR_CUDA, std::string("checked build: device check failed in ") + r.second + " line " +
+                                   std::to_string(line) + " during " + call);
+  }
+#else
+  (void)c, (void)call;
+#endif
+}
+
+#ifdef BF_CHECKED
+// self-test of the checking mechanism (BF_CHECK_SELFTEST=1, checked build only): one gather one
+// past the end of a vector of m entries must be reported by the next check_device_flags
+static __global__ void k_check_selftest(const double *x, int m, double *y) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) y[0] = x[BF_COL(m, m)];
+}
+#endif
+
+// checked build: every matrix the handle holds is well formed
+static void check_handle(bf_ctx *c) {
+#ifdef BF_CHECKED
+  if (getenv("BF_CHECK_SELFTEST")) {
+    k_check_selftest<<<1, 32, 0, c->stream>>>(c->xd, 2 * c->n, c->w);
+    BF_CUDA(cudaGetLastError());
+  }
+  static const char *bn[5] = {"A_pp", "A_ps", "A_sp", "A_ss", "S~"};
+  for (int b = 0; b < 5; b++) check_csr(c, c->blk[b], bn[b]);
+  check_csr(c, c->jsc, "J scalar");
+  for (int w = 0; w < 4; w++)
+    for (int l = 0; l < c->h[w].nlev; l++) {
+      const Level &L = c->h[w].lv[l];
+      std::string t = "hierarchy " + std::to_string(w) + " level " + std::to_string(l) + " ";
+      check_csr(c, L.A, (t + "A").c_str());
+      check_csr(c, L.P, (t + "P").c_str());
+      check_csr(c, L.R, (t + "R").c_str());
+      check_csr(c, L.Rf, (t + "Rf").c_str());
+      check_csr(c, L.A_io, (t + "A (construction order)").c_str());
+      check_csr(c, L.P_io, (t + "P (construction order)").c_str());
+    }
+#else
+  (void)c;
+#endif
 }
 
 static bool env_flag(const char *name) { return getenv(name) != nullptr; }
@@ -421,6 +512,8 @@ bf_status bf_setup(const bf_bsr2 *J, const bf_options *opt, void *stream, bf_han
     alloc_solve_workspace(c, 30);
     BF_CUDA(cudaStreamSynchronize(c->stream));
     lap("workspace");
+    check_handle(c);
+    check_device_flags(c, "bf_setup");
   } catch (const Error &e) {
     g_setup_err = e.msg;
     bf_status st = e.st;
@@ -467,6 +560,8 @@ bf_status bf_update(bf_handle c, const double *vals, int32_t mem, void *stream) 
     build_ilu(c);  // numeric refactorization on the kept schedule
   }
   sync(c);
+  check_handle(c);
+  check_device_flags(c, "bf_update");
   return BF_OK;
   BF_GUARD_END(c)
 }
@@ -554,6 +649,7 @@ bf_status bf_solve(bf_handle c, const double *rhs, double *x, double tol, int32_
   timer_end(c, 3, t0);
   BF_CUDA(cudaStreamSynchronize(c->stream));
   timer_flush(c);
+  check_device_flags(c, "bf_solve");
   return BF_OK;
   BF_GUARD_END(c)
 }
@@ -572,6 +668,7 @@ bf_status bf_spmv(bf_handle c, const double *x, double *y, int32_t vec_mem, void
     BF_CUDA(cudaMemcpyAsync(y, yd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
   timer_flush(c);
+  check_device_flags(c, "bf_spmv");
   return BF_OK;
   BF_GUARD_END(c)
 }
@@ -590,6 +687,7 @@ bf_status bf_apply_precond(bf_handle c, const double *r, double *z, int32_t vec_
     BF_CUDA(cudaMemcpyAsync(z, zd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
   timer_flush(c);
+  check_device_flags(c, "bf_apply_precond");
   return BF_OK;
   BF_GUARD_END(c)
 }
@@ -613,6 +711,7 @@ bf_status bf_vcycle(bf_handle c, int32_t which, const double *b, double *x, int3
   vcycle(c, which, bd, xd);
   if (!vec_mem) BF_CUDA(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
+  check_device_flags(c, "bf_vcycle");
   return BF_OK;
   BF_GUARD_END(c)
 }
@@ -699,6 +798,7 @@ bf_status bf_ilu_solve(bf_handle c, const double *r, double *x, int32_t vec_mem,
   if (!vec_mem)
     BF_CUDA(cudaMemcpyAsync(x, xd, sizeof(double) * 2 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
   BF_CUDA(cudaStreamSynchronize(c->stream));
+  check_device_flags(c, "bf_ilu_solve");
   return BF_OK;
   BF_GUARD_END(c)
 }

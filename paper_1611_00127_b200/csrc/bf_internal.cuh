@@ -204,6 +204,10 @@ T *dalloc_t(bf_ctx *c, size_t count) {
   return static_cast<T *>(dalloc(c, count * sizeof(T) + 16));
 }
 void free_csr(bf_ctx *c, DCsr &A);
+// checked build: validate row pointers / column range / ascending columns of A on the device
+void check_csr(bf_ctx *c, const DCsr &A, const char *what);
+// checked build: read every translation unit's device-check flag (throws on a failed check)
+void check_device_flags(bf_ctx *c, const char *call);
 // pinned host buffers of at least `bytes` (pooled process-wide; *got = the block's size)
 double *pinned_acquire(size_t bytes, size_t *got);
 void pinned_release(double *p, size_t bytes);
@@ -310,3 +314,39 @@ inline void launch_pdl(bf_ctx *c, void (*kernel)(KArgs...), dim3 grid, dim3 bloc
 }
 
 }  // namespace bf
+
+// ---- checked build (-DBF_CHECKED, libbf_checked.so) ---------------------------------------
+// compute-sanitizer is closed on the GPU pool this was developed on, so memory safety is shown
+// with the library's own checks: BF_CHK(cond) records the source line of the first failed
+// device-side check in a per-translation-unit flag (the access is then clamped, never made);
+// every public call of a checked build reads all flags after its work and fails with
+// BF_ERR_CUDA "device check failed ..." if one is set.  check_csr() validates a built matrix
+// (row pointers, column range and order) on the device.  In the normal build all of it
+// compiles to nothing.
+#ifdef BF_CHECKED
+static __device__ unsigned int bf_chk_line = 0;
+#define BF_CHK(cond) ((cond) ? true : (atomicCAS(&bf_chk_line, 0u, (unsigned)__LINE__), false))
+namespace bf {
+int register_check_reader(unsigned (*reader)(), const char *tu);
+}  // namespace bf
+static unsigned bf_chk_read() {
+  unsigned v = 0, z = 0;
+  cudaMemcpyFromSymbol(&v, bf_chk_line, sizeof v);
+  if (v) cudaMemcpyToSymbol(bf_chk_line, &z, sizeof z);
+  return v;
+}
+#define BF_CHECK_TU(name) static int bf_chk_registered = ::bf::register_check_reader(&bf_chk_read, name);
+#else
+#define BF_CHK(cond) true
+#define BF_CHECK_TU(name)
+#endif
+// a gathered column index, bounds-checked (and clamped) in the checked build
+#define BF_COL(col, m) (BF_CHK((unsigned)(col) < (unsigned)(m)) ? (col) : 0)
+// a polling loop of the sync-free sweeps: bounded in the checked build (a dependency that never
+// completes is reported instead of hanging the GPU)
+#ifdef BF_CHECKED
+#define BF_SPIN_OK(s) BF_CHK(++(s) < (1u << 26))
+#else
+#define BF_SPIN_OK(s) true
+#endif
+

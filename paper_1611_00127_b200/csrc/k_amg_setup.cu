@@ -15,6 +15,7 @@
 #include <string>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_amg_setup.cu")
 
 #include <algorithm>
 #include <vector>
@@ -413,6 +414,7 @@ __global__ void k_transpose_scatter(DCsr P, const int32_t *__restrict__ Rrp, int
   for (int q = P.rp[i]; q < P.rp[i + 1]; q++) {
     int J = P.ci[q];
     int p = Rrp[J] + atomicAdd(&cursor[J], 1);
+    if (!BF_CHK(p < Rrp[J + 1])) continue;
     R.ci[p] = i;
     R.v[p] = P.v[q];
   }
@@ -667,12 +669,15 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DC
         // cannot return -1 here: the count kernel admitted this row (<= HASH_MAX distinct columns
         // in a table of the same size), otherwise the whole product went to the ESC path
         int s = hash_insert(keys, cc, mask, ins);
-        double acc = ins ? 0.0 : vals[s];
-        vals[s] = __dadd_rn(acc, __dmul_rn(a, cv));
+        if (BF_CHK(s >= 0)) {
+          double acc = ins ? 0.0 : vals[s];
+          vals[s] = __dadd_rn(acc, __dmul_rn(a, cv));
+        }
       }
       for (int t = cbs + 32 + lane; t < cbe; t += 32) {  // rows of B longer than 32 (rare)
         bool ins;
         int s = hash_insert(keys, B.ci[t], mask, ins);
+        if (!BF_CHK(s >= 0)) continue;
         double acc = ins ? 0.0 : vals[s];
         vals[s] = __dadd_rn(acc, __dmul_rn(a, B.v[t]));
       }
@@ -696,6 +701,7 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DC
   for (int e = lane; e < n; e += 32) {
     int key = ckeys[e], rank = 0;
     for (int u = 0; u < n; u++) rank += ckeys[u] < key;
+    if (!BF_CHK(base + rank < C.rp[i + 1])) continue;
     C.ci[base + rank] = key;
     C.v[base + rank] = cvals[e];
   }
@@ -742,6 +748,7 @@ __global__ void k_spgemm_tpr_fill(DCsr A, DCsr B, DCsr C) {
       int J = B.ci[t], u = 0;
       while (u < len && cols[u] != J) u++;
       if (u == len) {
+        if (!BF_CHK(len < TPR_CAP)) continue;
         cols[len] = J;
         acc[len] = 0.0;
         len++;
@@ -1183,6 +1190,7 @@ static __global__ void __launch_bounds__(256) k_perm_fill_warp(int n, const int3
     const int col = sc[e];
     int rank = 0;
     for (int k = 0; k < len; k++) rank += sc[k] < col;
+    if (!BF_CHK(rank < len)) continue;
     bci[o + rank] = col;
     bv[o + rank] = v[q0 + e];
   }

@@ -12,6 +12,7 @@
 #include <cmath>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_assemble.cu")
 
 namespace bf {
 

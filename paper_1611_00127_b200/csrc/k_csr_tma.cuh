@@ -72,7 +72,7 @@ __host__ __device__ inline int tma_stage_bytes(int cap, int rpt) {
 }
 
 template <int MODE, int G, int ST, int NT>
-__global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int cap,
+__global__ void __launch_bounds__(NT) k_csr_tma(int n, int m, int rpt, int ntiles, int cap,
                                                          const int32_t *__restrict__ rp,
                                                          const int32_t *__restrict__ ci,
                                                          const double *__restrict__ v, const double *__restrict__ x,
@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int 
     unsigned char *base = smem_raw + s * stage_bytes;
     uint32_t br = 4u * ((r1 - r0 + 1 + 3) & ~3);  // r0 is a multiple of 4 (rpt is)
     uint32_t bc = 4u * (c1 - c0), bv = 8u * (v1 - v0);
+    if (!BF_CHK(br <= (uint32_t)rb && rb + bc <= (uint32_t)cb && cb + bv <= (uint32_t)stage_bytes)) bc = bv = 0;
     mbar_expect_tx(&bars[s], br + bc + bv);
     tma_bulk_g2s(base, rp + r0, br, &bars[s], pol);
     if (bc) tma_bulk_g2s(base + rb, ci + c0, bc, &bars[s], pol);
@@ -154,16 +155,16 @@ __global__ void __launch_bounds__(NT) k_csr_tma(int n, int rpt, int ntiles, int 
 #pragma unroll
         for (int e = 0; e < 8; e++) {
           int q = lo + sub + e * G;
-          xv[e] = q < hi ? __ldg(x + sc[q]) : 0.0;
+          xv[e] = q < hi ? __ldg(x + BF_COL(sc[q], m)) : 0.0;
           av[e] = q < hi ? sv[q] : 0.0;
         }
 #pragma unroll
         for (int e = 0; e < 8; e++)
           if (lo + sub + e * G < hi) acc += av[e] * xv[e];
-        for (int q = lo + sub + 8 * G; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+        for (int q = lo + sub + 8 * G; q < hi; q += G) acc += sv[q] * __ldg(x + BF_COL(sc[q], m));
       } else {
 #pragma unroll 4
-        for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + sc[q]);
+        for (int q = lo + sub; q < hi; q += G) acc += sv[q] * __ldg(x + BF_COL(sc[q], m));
       }
       if (G > 1) {
 #pragma unroll
@@ -223,7 +224,7 @@ void launch_csr_tma_st(bf_ctx *c, const DCsr &A, const double *x, const double *
   attr[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BF_CUDA(cudaLaunchKernelEx(&cfg, k_csr_tma<MODE, G, ST, NT>, A.n, A.rpt, ntiles, A.cap, (const int32_t *)A.rp,
+  BF_CUDA(cudaLaunchKernelEx(&cfg, k_csr_tma<MODE, G, ST, NT>, A.n, A.m, A.rpt, ntiles, A.cap, (const int32_t *)A.rp,
                              (const int32_t *)A.ci, (const double *)A.v, x, b, dinv, y, aux, alpha, beta, dir));
 }
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_gmres.cu")
 
 namespace bf {
 

@@ -29,6 +29,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_ilu.cu")
 
 namespace bf {
 
@@ -63,7 +64,9 @@ __global__ void k_ilu_levels(int n, const int32_t *__restrict__ rp, const int32_
     int i = base + (threadIdx.x & 31);
     bool done = i >= n;
     int lo = done ? 0 : rp[i], hi = done ? 0 : rp[i + 1];
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       if (!done) {
         int lev = 0;
         bool ready = true;
@@ -135,7 +138,9 @@ __global__ void k_ilu_factor(int n, const int32_t *__restrict__ perm, const int3
     bool done = t >= (unsigned)n;
     int i = done ? 0 : perm[t];
     int lo = done ? 0 : rp[i], hi = done ? 0 : rp[i + 1], di = done ? 0 : dpos[i];
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       if (!done) {
         bool ready = true;
         for (int q = lo; q < di && ready; q++) ready = ld_acquire(flag + ci[q]) != 0;
@@ -272,7 +277,9 @@ __global__ void __launch_bounds__(256) k_ilu_fwd(int n, const int32_t *__restric
       y0 = ip ? a.y : a.x;
       y1 = ip ? a.x : a.y;
     }
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       if (!done && deps_ready(dc, lo, di, ci, flag, target)) {
         dep_subtract(dc, lo, di, ci, lu, y, y0, y1);
         y[i] = make_double2(y0, y1);
@@ -310,7 +317,9 @@ __global__ void __launch_bounds__(256) k_ilu_bwd(int n, const int32_t *__restric
       d01 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i);
       d23 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i + 1);
     }
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       if (!done && deps_ready(dc, lo, hi, ci, flag, target)) {
         dep_subtract(dc, lo, hi, ci, lu, x, t0, t1);
         x[i] = make_double2(d01.x * t0 + d01.y * t1, d23.x * t0 + d23.y * t1);
@@ -407,7 +416,9 @@ __global__ void __launch_bounds__(256) k_ilu_fwd_v(int n, const int32_t *__restr
       y0 = ip ? a.y : a.x;
       y1 = ip ? a.x : a.y;
     }
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       double2 vals[PF];
       bool ok = !done && vdeps_ready(dc, lo, di, ci, y, vals);
       if (!done && !ok && backoff) __nanosleep(backoff);
@@ -445,7 +456,9 @@ __global__ void __launch_bounds__(256) k_ilu_bwd_v(int n, const int32_t *__restr
       d01 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i);
       d23 = __ldg(reinterpret_cast<const double2 *>(dinv) + 2 * (size_t)i + 1);
     }
+    [[maybe_unused]] unsigned spins = 0;  // checked build: a dependency that never completes is reported
     while (!__all_sync(FULL, done)) {
+      if (!BF_SPIN_OK(spins)) done = true;
       double2 vals[PF];
       bool ok = !done && vdeps_ready(dc, lo, hi, ci, x, vals);
       if (!done && !ok && backoff) __nanosleep(backoff);
@@ -622,9 +635,9 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
       int iw = min(lag, g.nx - 1);
       int c = base + (BWD ? g.nx - 1 - iw : iw);
       if (kw > 0 && kk == 0)
-        while (!ready2(ld_poll(out + (c + dk)))) __nanosleep(backoff);
+        for (unsigned spins = 0; !ready2(ld_poll(out + (c + dk))) && BF_SPIN_OK(spins);) __nanosleep(backoff);
       if (jw > 0 && jj == 0)
-        while (!ready2(ld_poll(out + (c + dj)))) __nanosleep(backoff);
+        for (unsigned spins = 0; !ready2(ld_poll(out + (c + dj))) && BF_SPIN_OK(spins);) __nanosleep(backoff);
     }
     xfetch(0, pk0, pj0);
     xfetch(1, pk1, pj1);
@@ -662,7 +675,8 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
             vk = sbuf[((s - 1) & 1) * 128 + (kk - 1) * g.TJ + jj];
           } else {
             vk = pk;
-            while (!ready2(vk)) {  // not yet published: back off so waiting tiles do not flood L2
+            [[maybe_unused]] unsigned spins = 0;
+            while (!ready2(vk) && BF_SPIN_OK(spins)) {  // not yet published: back off so waiting tiles do not flood L2
               __nanosleep(backoff);
               vk = ld_poll(out + (c + dk));
             }
@@ -673,7 +687,8 @@ __global__ void __launch_bounds__(128) k_ilu_pencil(PencilGeom g, const double2 
             vj = sbuf[((s - 1) & 1) * 128 + kk * g.TJ + jj - 1];
           } else {
             vj = pj;
-            while (!ready2(vj)) {
+            [[maybe_unused]] unsigned spins = 0;
+            while (!ready2(vj) && BF_SPIN_OK(spins)) {
               __nanosleep(backoff);
               vj = ld_poll(out + (c + dj));
             }

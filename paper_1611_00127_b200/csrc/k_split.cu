@@ -11,6 +11,7 @@
 #include <string>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_split.cu")
 
 namespace bf {
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_spmv.cu")
 #include "k_spmv.cuh"
 
 namespace bf {
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(BSR_WARPS * 32) k_bsr2_spmv(int n, const int32
     int ce = min(cs + BSR_CAP, e);
 #pragma unroll 4
     for (int k = cs + lane; k < ce; k += 32) {
-      int col = __ldcs(ci + k);
+      int col = BF_COL(__ldcs(ci + k), n);
       double2 v01 = __ldcs(v + 2 * (size_t)k);      // (a_pp, a_ps)
       double2 v23 = __ldcs(v + 2 * (size_t)k + 1);  // (a_sp, a_ss)
       double2 xc = __ldg(x + col);

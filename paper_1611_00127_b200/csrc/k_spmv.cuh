@@ -26,7 +26,7 @@ constexpr int CSR_WARPS = 8;
 constexpr int CSR_CAP = 256;
 
 template <int MODE, int G>
-__global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, const int32_t *__restrict__ rp,
+__global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, int m, const int32_t *__restrict__ rp,
                                                         const int32_t *__restrict__ ci,
                                                         const double *__restrict__ v, const double *__restrict__ x,
                                                         const double *__restrict__ b,
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, const int32_t *__
     int lo = max(my_lo, cs), hi = min(my_hi, ce);
 #pragma unroll 4
     for (int k = lo + sub; k < hi; k += G) {
-      int col = sc[k - cs];
+      int col = BF_COL(sc[k - cs], m);
       acc += sv[k - cs] * __ldg(x + col);
     }
     __syncwarp();
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, const int32_t *__
 // entries are contiguous, so the streaming loads of a warp coalesce.
 constexpr int SHORT_K = 8;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_csr_short(int n, const int32_t *__restrict__ rp,
+__global__ void __launch_bounds__(256) k_csr_short(int n, int m, const int32_t *__restrict__ rp,
                                                    const int32_t *__restrict__ ci,
                                                    const double *__restrict__ v, const double *__restrict__ x,
                                                    const double *__restrict__ b, const double *__restrict__ dinv,
@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(256) k_csr_short(int n, const int32_t *__restr
   double acc = 0.0;
 #pragma unroll
   for (int e = 0; e < SHORT_K; e++)
-    if (lo + e < hi) acc += val[e] * __ldg(x + col[e]);
-  for (int q = lo + SHORT_K; q < hi; q++) acc += __ldcs(v + q) * __ldg(x + __ldcs(ci + q));
+    if (lo + e < hi) acc += val[e] * __ldg(x + BF_COL(col[e], m));
+  for (int q = lo + SHORT_K; q < hi; q++) acc += __ldcs(v + q) * __ldg(x + BF_COL(__ldcs(ci + q), m));
   if (MODE == OP_SPMV) {
     y[r] = acc;
   } else if (MODE == OP_SPMV_X0) {
@@ -188,7 +188,7 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
   c->alg_bytes += csr_op_bytes<MODE>(A, dir != nullptr, aux != nullptr);
   if (csr_op_dia<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (A.short_rows) {
-    launch_pdl(c, k_csr_short<MODE>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.rp, A.ci, A.v, x, b, dinv, y, aux,
+    launch_pdl(c, k_csr_short<MODE>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y, aux,
                alpha, beta, dir);
     BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
@@ -200,7 +200,7 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
   int blocks = div_up(A.n, rows_per_block);
 #define BF_CSR_CASE(g)                                                                                  \
   case g:                                                                                               \
-    k_csr<MODE, g><<<blocks, CSR_WARPS * 32, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, x, b, dinv, y, aux, alpha, \
+    k_csr<MODE, g><<<blocks, CSR_WARPS * 32, 0, c->stream>>>(A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y, aux, alpha, \
                                                              beta, dir);                                \
     break;
   switch (G) {

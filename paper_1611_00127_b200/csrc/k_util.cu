@@ -5,6 +5,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_util.cu")
 
 namespace bf {
 

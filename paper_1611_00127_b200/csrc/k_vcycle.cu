@@ -4,6 +4,7 @@
 // staged dense coarse solve; and the BF preconditioner apply, Algorithm 3:
 //   s = V_Ass(R_s v);  r' = R_p v - A_ps s;  p = V_S~(r');  z = R_p^T p + R_s^T s.
 #include "bf_internal.cuh"
+BF_CHECK_TU("k_vcycle.cu")
 #include "k_spmv.cuh"
 #include "k_dia.cuh"
 
@@ -77,11 +78,11 @@ struct TailParams {
 // the group); ok = this group has a row
 __device__ __forceinline__ double group_row(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                             const double *__restrict__ v, const double *x, int r, bool ok,
-                                            int lig, int g) {
+                                            int lig, int g, int m) {
   double s = 0.0;
   if (ok) {
     int e = rp[r + 1];
-    for (int q = rp[r] + lig; q < e; q += g) s += v[q] * x[ci[q]];
+    for (int q = rp[r] + lig; q < e; q += g) s += v[q] * x[BF_COL(ci[q], m)];
   }
   for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, g);
   return s;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
       for (int base = 0; base < L.n; base += nth / g) {
         int r = base + tid / g;
         bool ok = r < L.n;
-        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g);
+        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g, L.n);
         if (ok && lig == 0) L.r[r] = L.b[r] - s;
       }
     }
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
       for (int base = 0; base < C.n; base += nth / g) {
         int r = base + tid / g;
         bool ok = r < C.n;
-        double s = group_row(L.Rrp, L.Rci, L.Rv, L.r, r, ok, lig, g);
+        double s = group_row(L.Rrp, L.Rci, L.Rv, L.r, r, ok, lig, g, L.n);
         if (ok && lig == 0) {
           C.b[r] = s;
           C.x[r] = p.beta * (s * C.d[r]);
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
       for (int base = 0; base < L.n; base += nth / g) {
         int r = base + tid / g;
         bool ok = r < L.n;
-        double s = group_row(L.Prp, L.Pci, L.Pv, e, r, ok, lig, g);
+        double s = group_row(L.Prp, L.Pci, L.Pv, e, r, ok, lig, g, C.n);
         if (ok && lig == 0) L.x[r] += s;
       }
     }
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailParams p) {
       for (int base = 0; base < L.n; base += nth / g) {
         int r = base + tid / g;
         bool ok = r < L.n;
-        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g);
+        double s = group_row(L.Arp, L.Aci, L.Av, L.x, r, ok, lig, g, L.n);
         if (ok && lig == 0) L.t[r] = L.x[r] + (L.b[r] - s) * L.d[r];
       }
     }
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       for (int base = 0; base < L.n; base += nth / g) {
         int i = base + tid / g;
         bool ok = i < L.n;
-        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
+        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g, L.n);
         if (ok && lig == 0) t[i] = s;
       }
       __syncthreads();
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       for (int base = 0; base < L.n; base += nth / g) {
         int i = base + tid / g;
         bool ok = i < L.n;
-        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g);
+        double s = group_row(L.Arp, L.Aci, L.Av, x, i, ok, lig, g, L.n);
         if (ok && lig == 0) r[i] = b[i] - s;
       }
     }
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       for (int base = 0; base < C.n; base += nth / g) {
         int i = base + tid / g;
         bool ok = i < C.n;
-        double s = group_row(L.Rrp, L.Rci, L.Rv, r, i, ok, lig, g);
+        double s = group_row(L.Rrp, L.Rci, L.Rv, r, i, ok, lig, g, L.n);
         if (ok && lig == 0) bc[i] = s;
       }
     }
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(DTAIL_THREADS) k_tail_columns(TailParams p, do
       for (int base = 0; base < L.n; base += nth / g) {
         int i = base + tid / g;
         bool ok = i < L.n;
-        double s = group_row(L.Prp, L.Pci, L.Pv, e, i, ok, lig, g);
+        double s = group_row(L.Prp, L.Pci, L.Pv, e, i, ok, lig, g, p.lv[l + 1].n);
         if (ok && lig == 0) x[i] += s;
       }
     }
