@@ -194,7 +194,8 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
     BF_CUDA(cudaGetLastError());
     return;
   }
-  if (c->use_tma && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
+  if (c->use_tma && A.nnz >= c->tune.tma_min_nnz && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir))
+    return;
   int G = lanes_for(c, A);
   int rows_per_block = (32 / G) * CSR_WARPS;
   int blocks = div_up(A.n, rows_per_block);

@@ -23,6 +23,7 @@ def newton_sequence(config, steps, solve, dims=None, gravity=True, chop=0.2):
         J = jacobian(prob, p, sn)
         R = residual(prob, p, sn).reshape(-1)
         rhs = np.ascontiguousarray(-R)
+        prob._p_cur, prob._sn_cur = p, sn     # the state u_k of this Jacobian (diagnostics)
         yield k, prob, J, rhs, float(np.linalg.norm(R))
         delta = np.asarray(solve(k, J, rhs), dtype=np.float64)
         dS = delta[1::2]
