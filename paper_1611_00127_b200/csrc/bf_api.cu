@@ -318,6 +318,7 @@ Tuning tuning_from_env() {
   t.tma_tile = env_num("BF_TMA_TILE", t.tma_tile);
   t.tma_ctas = std::max(1, (int)env_num("BF_TMA_CTAS", t.tma_ctas));
   t.tma_min_nnz = (int64_t)env_num("BF_TMA_MIN_NNZ", (double)t.tma_min_nnz);
+  t.spread_small = !env_flag("BF_NO_SPREAD");
   t.tma_g_p = (int)env_num("BF_TMA_G_P", 0);
   t.tma_g_r = (int)env_num("BF_TMA_G_R", 0);
   t.spgemm = env_flag("BF_SPGEMM_ESC") ? 2 : (env_flag("BF_SPGEMM_HASH") ? 1 : 0);

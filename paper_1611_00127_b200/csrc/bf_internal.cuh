@@ -91,6 +91,7 @@ struct Tuning {
   double tma_tile = 1024.0; // target nonzeros per TMA tile
   int tma_ctas = 8;         // TMA kernel CTAs per SM (upper bound; shared memory decides)
   int64_t tma_min_nnz = 0;  // matrices with fewer nonzeros use the warp-staged kernel (no TMA pipeline)
+  bool spread_small = true; // small matrices: >= 2 TMA tiles per SM (more lanes per row)
   int tma_g_p = 0, tma_g_r = 0;  // forced lanes per row for P / R (0: heuristic)
   int spgemm = 0;           // 0 auto (thread-per-row, hash, ESC fallback), 1 hash, 2 ESC
   int ilu_ctas = 4;         // generic ILU sweep CTAs per SM

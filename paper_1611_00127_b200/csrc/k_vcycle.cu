@@ -507,13 +507,22 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
     // measured (C3, with the fused restriction): mean / 4 beats mean / 3, 5, 8
     while (g < 32 && 2 * g <= mean / c->tune.tma_g_div) g <<= 1;
   }
-  A.g = g;
   // measured: ~1024 nonzeros per tile beats 2048 (more CTAs per SM for the gathers)
   const double tile = c->tune.tma_tile;
   int rpt = 256;
   // ~1024 nonzeros per tile, but at least one full pass of the CTA (256/g rows) so that no
   // thread idles (stencil rows, g = 1, always take 256-row tiles)
   while (rpt > 8 && rpt > TMA_THREADS / g && rpt * mean > tile) rpt >>= 1;
+  // small (coarse-level) matrices: spread the tiles over all SMs (>= 2 tiles per SM) instead of a
+  // few CTAs walking long chains of dependent loads; the CTA's threads then take more lanes per
+  // row, g = 256 / rows per tile (ncu: the 7.6K-row restriction of C3's A_ss level 3 ran on 30
+  // CTAs at 17 us for 1 MB)
+  if (force_g <= 0 && !stencil && c->tune.spread_small) {
+    const int64_t want = 2 * (int64_t)c->num_sms;
+    while (rpt > 8 && (A.n + rpt - 1) / rpt < want) rpt >>= 1;
+    while (g < 32 && (int64_t)g * rpt < TMA_THREADS) g <<= 1;
+  }
+  A.g = g;
   int *mx = dalloc_t<int>(c, 1);
   for (;; rpt >>= 1) {
     BF_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
