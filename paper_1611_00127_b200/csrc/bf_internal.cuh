@@ -34,6 +34,12 @@ struct DCsr {
   int32_t *dia_off = nullptr;  // host array of dia_k offsets (kept out of the by-value kernel struct)
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
+  // windowed form (k_csr_win.cuh): super-tiles of wk TMA tiles share one shared-memory window of x
+  int32_t wk = 0;            // TMA tiles per super-tile (0: not windowed)
+  int32_t wmax_used = 0;     // largest window of any super-tile (doubles)
+  uint16_t *lc = nullptr;    // per nonzero: position of its column in the super-tile's window
+  int32_t *wn = nullptr;     // per super-tile: window length
+  int32_t *wcol = nullptr;   // per super-tile: WIN_MAX slots, the sorted distinct columns
 };
 
 struct Level {
@@ -92,6 +98,10 @@ struct Tuning {
   int tma_ctas = 8;         // TMA kernel CTAs per SM (upper bound; shared memory decides)
   int64_t tma_min_nnz = 0;  // matrices with fewer nonzeros use the warp-staged kernel (no TMA pipeline)
   bool spread_small = true; // small matrices: >= 2 TMA tiles per SM (more lanes per row)
+  bool win = true;          // shared-memory x windows for the renumbered Galerkin levels (k_csr_win.cuh)
+  int win_rows = 512;       // rows per super-tile (rounded to whole TMA tiles)
+  int64_t win_nmin = 16384; // matrices with fewer rows are not windowed
+  double win_ratio = 0.5;   // windows are dropped if they hold more than this many entries per nonzero
   int tma_g_p = 0, tma_g_r = 0;  // forced lanes per row for P / R (0: heuristic)
   int spgemm = 0;           // 0 auto (thread-per-row, hash, ESC fallback), 1 hash, 2 ESC
   int ilu_ctas = 4;         // generic ILU sweep CTAs per SM
@@ -256,6 +266,9 @@ void build_dense_tail(bf_ctx *c, Hier &h);                               // k_vc
 void build_rfuse(bf_ctx *c, Hier &h, bool finest_only);                 // k_amg_setup.cu
 double apply_model_bytes(bf_ctx *c);                                    // k_vcycle.cu
 void tile_csr(bf_ctx *c, DCsr &A, bool stencil = false, int force_g = 0);  // k_vcycle.cu
+void window_csr(bf_ctx *c, DCsr &A);                                    // k_vcycle.cu
+void free_window(bf_ctx *c, DCsr &A);                                   // k_vcycle.cu
+void build_windows(bf_ctx *c, Hier &h);                                 // k_vcycle.cu
 void setup_dia(bf_ctx *c, DCsr &A);                                     // k_vcycle.cu
 
 // ---- solve kernels -------------------------------------------------------------

@@ -1476,6 +1476,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
   plan_tail(c, h);
   build_dense_tail(c, h);
   build_rfuse(c, h, false);
+  build_windows(c, h);
 }
 
 // ---------------------------------------------------------------------------------------

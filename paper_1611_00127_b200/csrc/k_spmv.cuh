@@ -164,6 +164,9 @@ bool csr_op_tma(bf_ctx *c, const DCsr &A, const double *x, const double *b, cons
 template <int MODE>
 bool csr_op_dia(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir);
+template <int MODE>
+bool csr_op_win(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
+                double *aux, double alpha, double beta, const double *dir);
 
 // algorithmic bytes of one csr_op (each operand once: int32 index, f64 value; x counted once
 // per column); accumulated into c->alg_bytes so a captured BF apply knows its own traffic
@@ -194,6 +197,7 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
     BF_CUDA(cudaGetLastError());
     return;
   }
+  if (A.wk && c->use_tma && csr_op_win<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (c->use_tma && A.nnz >= c->tune.tma_min_nnz && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir))
     return;
   int G = lanes_for(c, A);
@@ -220,4 +224,5 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
 }  // namespace bf
 
 #include "k_csr_tma.cuh"
+#include "k_csr_win.cuh"
 #include "k_dia.cuh"

@@ -542,6 +542,151 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   dfree(c, mx);
 }
 
+// ---- shared-memory x windows (k_csr_win.cuh) ------------------------------------------------
+// one CTA per super-tile: distinct columns by a shared-memory hash table, bitonic sort, then every
+// nonzero's local index by binary search
+static __global__ void __launch_bounds__(256) k_win_build(int n, int rows, const int32_t *__restrict__ rp,
+                                                          const int32_t *__restrict__ ci, int32_t *__restrict__ wn,
+                                                          int32_t *__restrict__ wcol, uint16_t *__restrict__ lc,
+                                                          int *__restrict__ stat, unsigned long long *total) {
+  extern __shared__ int32_t win_sm[];
+  int32_t *table = win_sm, *uniq = win_sm + WIN_HASH;
+  __shared__ int cnt;
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int r0 = s * rows, r1 = min(n, r0 + rows);
+  const int q0 = rp[r0], q1 = rp[r1];
+  for (int i = tid; i < WIN_HASH; i += 256) table[i] = -1;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  for (int q = q0 + tid; q < q1; q += 256) {
+    const int col = ci[q];
+    unsigned slot = ((unsigned)col * 2654435761u) >> 18;  // 14 bits
+    for (int probe = 0; probe < WIN_HASH; probe++) {
+      int old = atomicCAS(&table[slot], -1, col);
+      if (old == -1 || old == col) break;
+      slot = (slot + 1) & (WIN_HASH - 1);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < WIN_HASH; i += 256)
+    if (table[i] != -1) {
+      int pos = atomicAdd(&cnt, 1);
+      if (pos < WIN_MAX) uniq[pos] = table[i];
+    }
+  __syncthreads();
+  const int c = cnt;
+  if (c > WIN_MAX) {  // the super-tile needs a larger window than shared memory holds
+    if (tid == 0) {
+      stat[0] = 1;
+      wn[s] = 0;
+    }
+    return;
+  }
+  int p2 = 2;
+  while (p2 < c) p2 <<= 1;
+  for (int i = c + tid; i < p2; i += 256) uniq[i] = 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= p2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < p2; i += 256) {
+        int l = i ^ j;
+        if (l > i) {
+          int a = uniq[i], b = uniq[l];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            uniq[i] = b;
+            uniq[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < c; i += 256) wcol[(size_t)s * WIN_MAX + i] = uniq[i];
+  if (tid == 0) {
+    wn[s] = c;
+    atomicMax(&stat[1], c);
+    atomicAdd(total, (unsigned long long)c);
+  }
+  for (int q = q0 + tid; q < q1; q += 256) {
+    const int col = ci[q];
+    int lo = 0, hi = c - 1;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (uniq[mid] < col) lo = mid + 1;
+      else hi = mid;
+    }
+    if (BF_CHK(uniq[lo] == col)) lc[q] = (uint16_t)lo;
+  }
+}
+
+void free_window(bf_ctx *c, DCsr &A) {
+  dfree(c, A.lc);
+  dfree(c, A.wn);
+  dfree(c, A.wcol);
+  A.lc = nullptr;
+  A.wn = nullptr;
+  A.wcol = nullptr;
+  A.wk = 0;
+  A.wmax_used = 0;
+}
+
+// Give a TMA-tiled matrix its shared-memory windows (super-tiles of wk tiles ~ win_rows rows);
+// halves the super-tile while some window exceeds WIN_MAX, gives up (plain TMA kernel) if single
+// tiles do, or if the windows hold too many entries per nonzero (no locality to exploit).
+void window_csr(bf_ctx *c, DCsr &A) {
+  free_window(c, A);
+  if (!c->tune.win || !c->use_tma || A.cap <= 0 || A.short_rows || A.dia_v || A.n < c->tune.win_nmin ||
+      A.nnz < c->tune.tma_min_nnz || A.nnz <= 0)
+    return;
+  ensure_smem_attr((const void *)k_win_build, (WIN_HASH + WIN_MAX) * 4 + 1024);
+  int *stat = dalloc_t<int>(c, 4);
+  unsigned long long *total = reinterpret_cast<unsigned long long *>(stat + 2);
+  A.lc = dalloc_t<uint16_t>(c, (size_t)A.nnz + 8);
+  for (int K = std::max(1, c->tune.win_rows / A.rpt);; K >>= 1) {
+    const int rows = K * A.rpt;
+    const int nsuper = (A.n + rows - 1) / rows;
+    A.wn = dalloc_t<int32_t>(c, nsuper);
+    A.wcol = dalloc_t<int32_t>(c, (size_t)nsuper * WIN_MAX);
+    BF_CUDA(cudaMemsetAsync(stat, 0, 16, c->stream));
+    k_win_build<<<nsuper, 256, (WIN_HASH + WIN_MAX) * 4, c->stream>>>(A.n, rows, A.rp, A.ci, A.wn, A.wcol, A.lc, stat,
+                                                                      total);
+    BF_LAUNCH(c);
+    int hs[4] = {0, 0, 0, 0};
+    BF_CUDA(cudaMemcpyAsync(hs, stat, 16, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    unsigned long long tot;
+    memcpy(&tot, hs + 2, sizeof tot);
+    if (!hs[0]) {
+      if ((double)tot > c->tune.win_ratio * (double)A.nnz) break;  // no reuse: not worth a window
+      A.wk = K;
+      A.wmax_used = hs[1];
+      if (c->tune.verbose)
+        fprintf(stderr, "[bf_setup]   window: n %d nnz %lld rpt %d K %d: %d super-tiles, max window %d, %.3f entries/nnz\n",
+                A.n, (long long)A.nnz, A.rpt, K, nsuper, hs[1], (double)tot / (double)A.nnz);
+      dfree(c, stat);
+      return;
+    }
+    dfree(c, A.wn);
+    dfree(c, A.wcol);
+    A.wn = nullptr;
+    A.wcol = nullptr;
+    if (K == 1) break;
+  }
+  dfree(c, stat);
+  free_window(c, A);
+}
+
+// windows for the coarse levels of a hierarchy: A_l and the fused restriction Rf_l (window_csr
+// keeps them only where the rows share columns: the renumbered levels)
+void build_windows(bf_ctx *c, Hier &h) {
+  for (int l = 0; l < h.nlev - 1; l++) {
+    Level &L = h.lv[l];
+    if (l >= 1) window_csr(c, L.A);
+    if (l >= 1 && L.Rf.n) window_csr(c, L.Rf);
+  }
+  BF_CUDA(cudaGetLastError());
+}
+
 // DIA form of a finest-level matrix whose nonzeros all sit on a few grid-stencil offsets
 void setup_dia(bf_ctx *c, DCsr &A) {
   if (!c->tune.dia || A.n == 0 || A.n != A.m || c->nx <= 0) return;

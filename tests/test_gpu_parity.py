@@ -347,6 +347,11 @@ VARIANTS = {
     "plain": {"BF_NO_DTAIL": "1", "BF_NO_RFUSE": "1", "BF_NO_TAIL": "1", "BF_NO_DIA": "1", "BF_NO_TMA": "1"},
     "coop-tail-big": {"BF_NO_DTAIL": "1", "BF_TAIL_NNZ": "200000"},
     "no-reorder": {"BF_NO_REORDER": "1"},
+    # shared-memory x windows (k_csr_win.cuh) forced onto these small hierarchies: every CSR level,
+    # accepted whatever their reuse; super-tiles of 64 and 512 rows; and switched off
+    "win-all-64": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_ROWS": "64"},
+    "win-all-512": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_ROWS": "512", "BF_NO_DTAIL": "1"},
+    "no-win": {"BF_NO_WIN": "1"},
 }
 
 

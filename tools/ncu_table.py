@@ -9,6 +9,9 @@ M = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "rdMB"), ("dram_
      ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2%"),
      ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%"),
      ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "lsb"),
+     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "bar"),
+     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "ssb"),
+     ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "mio"),
      ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%"),
      ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid")]
 
@@ -26,7 +29,10 @@ def main(path, n=60):
             except (ValueError, IndexError):
                 v = float("nan")
             vals.append(v)
-        print("%-28s" % r[h.index("Kernel Name")][:28] + "".join("%9.1f" % v for v in vals))
+        name = r[h.index("Kernel Name")]
+        # keep the template arguments visible: k_csr_tma<3, 16, 2, 256>(...) -> k_csr_tma<3,16,2,256>
+        name = name.replace("void ", "").replace("bf::", "").split("(")[0].replace(", ", ",")
+        print("%-28s" % name[:28] + "".join("%9.1f" % v for v in vals))
 
 
 if __name__ == "__main__":
