@@ -147,9 +147,7 @@ void free_csr(bf_ctx *c, DCsr &A) {
   dfree(c, A.ci);
   dfree(c, A.v);
   dfree(c, A.dia_v);
-  dfree(c, A.lc);
-  dfree(c, A.wn);
-  dfree(c, A.wcol);
+  free_window(c, A);
   A = DCsr();
 }
 
@@ -323,9 +321,11 @@ Tuning tuning_from_env() {
   t.tma_min_nnz = (int64_t)env_num("BF_TMA_MIN_NNZ", (double)t.tma_min_nnz);
   t.spread_small = !env_flag("BF_NO_SPREAD");
   t.win = !env_flag("BF_NO_WIN");
-  t.win_rows = std::max(8, (int)env_num("BF_WIN_ROWS", t.win_rows));
+  t.win_rows = std::max(32, (int)env_num("BF_WIN_ROWS", t.win_rows));
   t.win_nmin = (int64_t)env_num("BF_WIN_NMIN", (double)t.win_nmin);
   t.win_ratio = env_num("BF_WIN_RATIO", t.win_ratio);
+  t.win_minlen = env_num("BF_WIN_MINLEN", t.win_minlen);
+  t.win_stage = std::max(1024, (int)env_num("BF_WIN_STAGE", t.win_stage));
   t.tma_g_p = (int)env_num("BF_TMA_G_P", 0);
   t.tma_g_r = (int)env_num("BF_TMA_G_R", 0);
   t.spgemm = env_flag("BF_SPGEMM_ESC") ? 2 : (env_flag("BF_SPGEMM_HASH") ? 1 : 0);

@@ -23,6 +23,21 @@
 
 namespace bf {
 
+// Windowed jagged-diagonal form of a CSR matrix (k_csr_win.cuh).  Kept behind a pointer: DCsr is a
+// by-value kernel parameter of the setup kernels.
+struct WJds {
+  int32_t wrows = 0;          // rows per block (one CTA of wrows threads; power of two, 32..256)
+  int32_t wmax_used = 0;      // largest window of any block (doubles)
+  int32_t cap_ne = 0;         // largest entry count of any block (its bulk-copy stage; multiple of 8)
+  int4 *meta = nullptr;       // per block: entry offset, entries (padded to 8), window length, longest row
+  uint16_t *jdo = nullptr;    // per block: 256 slots, offset of jagged diagonal e within the block
+  uint32_t *rowinfo = nullptr;// per sorted position: (row length << 16) | row within the block (0xffff: none)
+  double *wv = nullptr;       // values by block and jagged diagonal
+  uint16_t *lc = nullptr;     // per entry: position of its column in the block's window
+  int32_t wstride = 0;        // slots per block in wcol: wmax_used rounded up to 256
+  int32_t *wcol = nullptr;    // per block: wstride slots, the sorted distinct columns (zero padded)
+};
+
 struct DCsr {
   int32_t n = 0, m = 0;  // rows, cols
   int64_t nnz = 0;
@@ -34,12 +49,7 @@ struct DCsr {
   int32_t *dia_off = nullptr;  // host array of dia_k offsets (kept out of the by-value kernel struct)
   int32_t *rp = nullptr, *ci = nullptr;
   double *v = nullptr;
-  // windowed form (k_csr_win.cuh): super-tiles of wk TMA tiles share one shared-memory window of x
-  int32_t wk = 0;            // TMA tiles per super-tile (0: not windowed)
-  int32_t wmax_used = 0;     // largest window of any super-tile (doubles)
-  uint16_t *lc = nullptr;    // per nonzero: position of its column in the super-tile's window
-  int32_t *wn = nullptr;     // per super-tile: window length
-  int32_t *wcol = nullptr;   // per super-tile: WIN_MAX slots, the sorted distinct columns
+  WJds *ws = nullptr;  // windowed jagged-diagonal form (k_csr_win.cuh), host object; null: none
 };
 
 struct Level {
@@ -98,10 +108,12 @@ struct Tuning {
   int tma_ctas = 8;         // TMA kernel CTAs per SM (upper bound; shared memory decides)
   int64_t tma_min_nnz = 0;  // matrices with fewer nonzeros use the warp-staged kernel (no TMA pipeline)
   bool spread_small = true; // small matrices: >= 2 TMA tiles per SM (more lanes per row)
-  bool win = true;          // shared-memory x windows for the renumbered Galerkin levels (k_csr_win.cuh)
-  int win_rows = 512;       // rows per super-tile (rounded to whole TMA tiles)
-  int64_t win_nmin = 16384; // matrices with fewer rows are not windowed
-  double win_ratio = 0.5;   // windows are dropped if they hold more than this many entries per nonzero
+  bool win = true;          // windowed jagged-diagonal form of the coarse-level operators (k_csr_win.cuh)
+  int win_rows = 256;       // rows per block at most
+  int win_stage = 36 * 1024; // block size: mean bytes of a block's matrix stream
+  double win_minlen = 8.0;  // matrices with shorter mean rows (the level transfers) keep the CSR kernels
+  int64_t win_nmin = 16384; // matrices with fewer rows keep the CSR kernels
+  double win_ratio = 0.35;   // the form is dropped if the windows hold more than this many entries per nonzero
   int tma_g_p = 0, tma_g_r = 0;  // forced lanes per row for P / R (0: heuristic)
   int spgemm = 0;           // 0 auto (thread-per-row, hash, ESC fallback), 1 hash, 2 ESC
   int ilu_ctas = 4;         // generic ILU sweep CTAs per SM

@@ -1,202 +1,180 @@
-// k_csr_win.cuh -- windowed TMA CSR kernels for the renumbered Galerkin levels (A_1, A_2, ...,
-// their fused restrictions Rf and the level transfers between renumbered levels).
+// k_csr_win.cuh -- windowed jagged-diagonal ("WJDS") kernels for the coarse (Galerkin) levels: A_l
+// and the fused restrictions Rf_l with at least win_nmin rows.
 //
-// ncu on the TMA CSR kernels of the Galerkin levels (k_csr_tma.cuh): ~40 % of the DRAM bandwidth
-// at ~70 % of the L1 wavefront throughput, the issue slots waiting on the x gathers (a warp-wide
-// gather of fp64 values scattered over a coarse grid costs up to 32 L1 wavefronts and an L2 round
-// trip).  After the coarse levels are renumbered in Morton order (k_amg_setup.cu
-// reorder_levels), a block of a few hundred consecutive rows touches a compact set of columns:
-// K consecutive TMA tiles (a "super-tile", K * rpt rows) reference only ~2-3 distinct columns per
-// row although they hold ~18-26 nonzeros per row.  So, per super-tile, setup stores
-//   wcol[s * wmax + i], i < wn[s] : the sorted distinct columns of the super-tile (the window)
-//   lc[q] (uint16)                : the position of ci[q] in that list
-// and the kernel gathers the window ONCE from global memory into shared memory (sorted, so the
-// gathers coalesce into runs) and then forms the rows from shared memory: a warp-wide gather is
-// a few shared-memory wavefronts instead of up to 32 L1 wavefronts, has shared-memory latency,
-// and the streamed matrix shrinks from 12 to 10 bytes per nonzero.  The TMA pipeline of the
-// matrix stream (tiles of rpt rows, double-buffered bulk copies, fused epilogues, PDL prologue)
-// is the one of k_csr_tma.cuh; the sums are formed by the same lanes in the same order, so the
-// results are bitwise those of the unwindowed kernel.
+// Why: ncu on the TMA CSR kernels of the Galerkin levels (k_csr_tma.cuh, G lanes per row) shows
+// ~40 % of the DRAM bandwidth with NO unit saturated -- about 2 warp instructions are issued per
+// nonzero (per-row bookkeeping, predicated gather slots, shuffles, an epilogue with 1 lane in G
+// active) and every gather is an L2 round trip.  This layout removes both:
 //
-// Work split: the tiles are dealt to the CTAs of one wave in contiguous ranges; a CTA whose range
-// begins or ends inside a super-tile fills that super-tile's window too (a few per cent more
-// window traffic, no imbalance).
+//  * rows are grouped in blocks of `wrows` consecutive rows, one CTA of wrows threads per block.
+//    After the Morton renumbering of the coarse levels (k_amg_setup.cu reorder_levels) a block
+//    touches only ~3-6 distinct columns per row, so setup stores per block the sorted list of its
+//    distinct columns (the WINDOW, wcol[blk * wstride + i], i < cnt) and per nonzero the uint16
+//    position of its column in that list.  The kernel gathers the window once into shared memory
+//    (sorted columns: the gathers coalesce into runs) and every product reads x from shared
+//    memory.
+//  * inside a block the rows are sorted by length (descending, ties by row); thread t owns the
+//    row at position t.  The block's entries are stored by jagged diagonals: entry e of position
+//    t at eo + off[e] + t, where off[e] counts the entries of the diagonals before e (diagonal e
+//    holds the rows longer than e, a prefix of the sorted order).  No padding (a sliced-ELL
+//    variant measured 12-30 % padding at these block sizes), consecutive threads read consecutive
+//    addresses, and a block's values and its local indices are each ONE contiguous 16-B aligned
+//    range: one elected thread fetches the whole block with two bulk copies (cp.async.bulk +
+//    mbarrier, the TMA engine) while the other threads gather the window.
+//  * everything a block needs first sits at an address computable from blockIdx alone (meta,
+//    diagonal offsets, row order, window columns: fixed strides), so a CTA's life is ONE round
+//    trip for that setup data (before griddepcontrol.wait: it overlaps the previous kernel), one
+//    for the matrix stream and the window gathers in parallel, then ~20 instructions per row entry
+//    from shared memory and a coalesced fused epilogue from row sums staged in shared memory.
+//    Throughput = resident CTAs x block bytes / CTA lifetime: blocks are sized to ~24-36 KB so
+//    that 5-7 CTAs per SM keep > 100 KB in flight per SM with no registers tied up (a first
+//    version that streamed slices through registers was latency bound at 3.2 TB/s; a version with
+//    three dependent round trips per CTA at 4 TB/s).
+//
+// A row's products are summed by 256 / wrows thread groups (group g: the entries e = g mod ng in
+// ascending order) whose partial sums are added in group order: deterministic for a given block
+// size; with wrows = 256 it is the sequential order of the CSR row.
+// Bytes per nonzero: 10 (8 value + 2 index) instead of 12, plus 4 per window column from DRAM (x
+// itself is L2 resident) and ~1.6 KB of block metadata.
 #pragma once
 #include "bf_internal.cuh"
 #include "k_csr_tma.cuh"
 
 namespace bf {
 
-constexpr int WIN_MAX = 4096;     // largest window (doubles) a super-tile may need: 32 KB of shared memory
-constexpr int WIN_HASH = 16384;   // setup: per-CTA hash table slots (distinct columns <= WIN_MAX)
+constexpr int WIN_MAX = 4096;     // largest window (doubles) a block may need: 32 KB of shared memory
+constexpr int WIN_HASH = 8192;    // setup: per-CTA hash table slots at most (distinct columns <= WIN_MAX)
+constexpr int WIN_ROWS_MAX = 256; // rows per block at most
+constexpr int WJDS_MAXLEN = 255;  // longest row a block may hold (jdo has WJDS_MAXLEN + 1 slots per block)
+constexpr int WJDS_STAGE_MAX = 80 * 1024;     // hard limit of a block's stream (else smaller blocks)
 
 // local index, range-checked (and clamped) in the checked build
 #define BF_LC(idx, cnt) (BF_CHK((int)(idx) < (cnt)) ? (int)(idx) : 0)
 
-__host__ __device__ inline int win_lc_bytes(int cap) { return ((2 * (cap + 16)) + 15) & ~15; }
-__host__ __device__ inline int win_stage_bytes(int cap, int rpt) {
-  return tma_rp_bytes(rpt) + win_lc_bytes(cap) + (((8 * (cap + 4)) + 15) & ~15);
-}
+// 256 threads per CTA whatever the block's row count: the window is gathered by all of them (<= 8
+// columns each from registers, one round trip), and 256 / wrows thread groups share a row's
+// entries (group g takes the jagged diagonals e = g, g + NG, ...); the groups' partial sums are
+// added in group order in the epilogue (deterministic; not the sequential order of the CSR row).
+constexpr int WJDS_THREADS = 256;
+constexpr int WJDS_WK = 8;  // window columns per thread held in registers (8 x 256 = 2048 of <= WIN_MAX)
 
-template <int MODE, int G, int ST>
-__global__ void __launch_bounds__(TMA_THREADS) k_csr_win(int n, int m, int rpt, int ntiles, int cap, int K, int wmax,
-                                                         const int32_t *__restrict__ rp,
-                                                         const uint16_t *__restrict__ lc,
-                                                         const double *__restrict__ v,
-                                                         const int32_t *__restrict__ wn,
-                                                         const int32_t *__restrict__ wcol,
-                                                         const double *__restrict__ x, const double *__restrict__ b,
-                                                         const double *__restrict__ dinv, double *__restrict__ y,
-                                                         double *__restrict__ aux, double alpha, double beta,
-                                                         const double *__restrict__ dir, int wsm) {
-  constexpr int NT = TMA_THREADS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bars[ST];
-  double *win = reinterpret_cast<double *>(smem_raw);  // wsm doubles
-  unsigned char *stages = smem_raw + 8 * (size_t)wsm;
-  const int stage_bytes = win_stage_bytes(cap, rpt);
-  const int rb = tma_rp_bytes(rpt);
-  const int cb = rb + win_lc_bytes(cap);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int s = 0; s < ST; s++) mbar_init(&bars[s], 1);
+template <int MODE>
+__global__ void __launch_bounds__(WJDS_THREADS) k_wjds(int n, int m, int wrows, const int4 *__restrict__ meta,
+                                              const uint16_t *__restrict__ jdo, const uint32_t *__restrict__ rowinfo,
+                                              const uint16_t *__restrict__ lc, const double *__restrict__ val,
+                                              const int32_t *__restrict__ wcol, const double *__restrict__ x,
+                                              const double *__restrict__ b, const double *__restrict__ dinv,
+                                              double *__restrict__ y, double *__restrict__ aux, double alpha,
+                                              double beta, const double *__restrict__ dir, int wsm, int cap_ne, int wstride) {
+  constexpr int NT = WJDS_THREADS;
+  extern __shared__ __align__(128) unsigned char wjds_sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint16_t offs[WJDS_MAXLEN + 1];
+  double *sval = reinterpret_cast<double *>(wjds_sm);                           // cap_ne values
+  uint16_t *slc = reinterpret_cast<uint16_t *>(wjds_sm + (size_t)cap_ne * 8);   // cap_ne local indices
+  double *win = reinterpret_cast<double *>(wjds_sm + (size_t)cap_ne * 10);      // wsm: window of x (cap_ne % 8 == 0)
+  double *racc = win + wsm;                                                     // NT: partial row sums [group][row]
+  const int blk = blockIdx.x, tid = threadIdx.x;
+  const int t = tid & (wrows - 1), g = tid / wrows, ng = NT / wrows;  // row position, entry group
+  // round trip 1: the block's setup data, all at addresses computable from blk
+  const int4 mt = __ldg(meta + blk);  // entry offset, entries (multiple of 8), window length, longest row
+  const uint32_t ri = __ldg(rowinfo + (size_t)blk * wrows + t);  // (row length << 16) | row within the block
+  const int32_t *wc = wcol + (size_t)blk * wstride;  // wstride: the matrix's largest window rounded up to 256
+  int wi[WJDS_WK];
+#pragma unroll
+  for (int k = 0; k < WJDS_WK; k++) wi[k] = k * NT < wstride ? __ldg(wc + tid + k * NT) : 0;  // (uniform guard)
+  offs[tid] = __ldg(jdo + (size_t)blk * (WJDS_MAXLEN + 1) + tid);       // WJDS_MAXLEN + 1 == NT
+  int ne = mt.y;
+  if (!BF_CHK(ne <= cap_ne)) ne = 0;
+  const int cnt = min(mt.z, wsm);
+  if (tid == 0) {  // the block's whole matrix stream: two bulk copies
+    mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ne > 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      mbar_expect_tx(&bar, (uint32_t)ne * 10u);
+      tma_bulk_g2s(sval, val + mt.x, (uint32_t)ne * 8u, &bar, pol);
+      tma_bulk_g2s(slc, lc + mt.x, (uint32_t)ne * 2u, &bar, pol);
+    }
+  }
+  const int r = blk * wrows + tid;  // the epilogue row of threads tid < wrows
+  const bool own = tid < wrows && r < n;
+  pdl_wait();  // x, b, dinv, dir and the outputs are touched only after this
+  // round trip 2: window gathers and the epilogue's row operands (the stream is in flight)
+  double xw[WJDS_WK];
+#pragma unroll
+  for (int k = 0; k < WJDS_WK; k++) xw[k] = tid + k * NT < cnt ? __ldg(x + BF_COL(wi[k], m)) : 0.0;
+  double eb = 0.0, ed = 0.0, ex = 0.0, edir = 0.0;
+  if (own) {
+    if (MODE == OP_RESID || MODE == OP_SUB_X0 || MODE == OP_SMOOTH) eb = __ldg(b + r);
+    if (MODE == OP_SUB_X0 || MODE == OP_SMOOTH || MODE == OP_SPMV_X0) ed = __ldg(dinv + r);
+    if (MODE == OP_SMOOTH) ex = __ldg(x + r);
+    if (MODE == OP_SMOOTH && dir) edir = dir[r];
+    if (MODE == OP_ADD) ex = y[r];
+  }
+#pragma unroll
+  for (int k = 0; k < WJDS_WK; k++)
+    if (tid + k * NT < cnt) win[tid + k * NT] = xw[k];
+#pragma unroll 4
+  for (int i = tid + WJDS_WK * NT; i < cnt; i += NT) win[i] = __ldg(x + BF_COL(__ldg(wc + i), m));
+  __syncthreads();  // window and offsets complete; the barrier's initialisation visible to every thread
+  if (ne > 0) mbar_wait(&bar, 0);
+  {
+    const int len = ne > 0 ? (int)(ri >> 16) : 0;
+    const int lr = (int)(ri & 0xffffu);
+    const double *vp = sval + t;
+    const uint16_t *ip = slc + t;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int e = g; e < len; e += ng) {
+      const int o = offs[e];
+      acc += vp[o] * win[BF_LC(ip[o], cnt)];
+    }
+    if (lr < wrows) racc[g * wrows + lr] = acc;
   }
   __syncthreads();
-
-  const uint64_t pol = l2_evict_first_policy();
-  auto issue = [&](int t, int s) {
-    int r0 = t * rpt, r1 = min(r0 + rpt, n);
-    int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
-    int c0 = q0 & ~7, c1 = (q1 + 7) & ~7;  // 16-B aligned uint16 range
-    int v0 = q0 & ~1, v1 = (q1 + 1) & ~1;  // 16-B aligned double range
-    unsigned char *base = stages + s * stage_bytes;
-    uint32_t br = 4u * ((r1 - r0 + 1 + 3) & ~3);
-    uint32_t bc = 2u * (c1 - c0), bv = 8u * (v1 - v0);
-    if (!BF_CHK(br <= (uint32_t)rb && rb + bc <= (uint32_t)cb && cb + bv <= (uint32_t)stage_bytes)) bc = bv = 0;
-    mbar_expect_tx(&bars[s], br + bc + bv);
-    tma_bulk_g2s(base, rp + r0, br, &bars[s], pol);
-    if (bc) tma_bulk_g2s(base + rb, lc + c0, bc, &bars[s], pol);
-    if (bv) tma_bulk_g2s(base + cb, v + v0, bv, &bars[s], pol);
-  };
-
-  // this CTA's contiguous tile range
-  const int t_begin = (int)(((int64_t)blockIdx.x * ntiles) / gridDim.x);
-  const int t_end = (int)(((int64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
-  if (t_begin >= t_end) {
-    pdl_wait();
-    return;
-  }
-  if (tid == 0)
-    for (int s = 0; s < ST && t_begin + s < t_end; s++) issue(t_begin + s, s);
-  pdl_wait();  // x, b, dinv, dir and the outputs are touched only after this
-  const int sub = tid % G;
-  int cur = -1, cnt = 0;
-  for (int t = t_begin, it = 0; t < t_end; t++, it++) {
-    const int sp = t / K;
-    if (sp != cur) {  // new super-tile: gather its window (every thread is past the previous tile's rows)
-      cur = sp;
-      cnt = min(__ldg(wn + sp), wsm);
-      const int32_t *wc = wcol + (size_t)sp * wmax;
-#pragma unroll 4
-      for (int i = tid; i < cnt; i += NT) win[i] = __ldg(x + BF_COL(__ldg(wc + i), m));
-      __syncthreads();
+  if (own) {  // fused epilogue in row order (coalesced)
+    double acc = racc[tid];
+    for (int k = 1; k < ng; k++) acc += racc[k * wrows + tid];
+    if (MODE == OP_SPMV) {
+      y[r] = acc;
+    } else if (MODE == OP_SPMV_X0) {
+      y[r] = acc;
+      aux[r] = beta * (acc * ed);
+    } else if (MODE == OP_RESID) {
+      y[r] = eb - acc;
+    } else if (MODE == OP_SUB_X0) {
+      double tt = eb - acc;
+      y[r] = tt;
+      aux[r] = beta * (tt * ed);
+    } else if (MODE == OP_SMOOTH) {
+      double dn = beta * ((eb - acc) * ed);
+      if (dir) dn += alpha * edir;
+      y[r] = ex + dn;
+      if (aux) aux[r] = dn;
+    } else if (MODE == OP_ADD) {
+      y[r] = ex + acc;
     }
-    const int s = it % ST;
-    const int r0 = t * rpt;
-    mbar_wait(&bars[s], (it / ST) & 1);
-    const unsigned char *base = stages + s * stage_bytes;
-    const int32_t *srp = reinterpret_cast<const int32_t *>(base);
-    const int q0 = srp[0];
-    const uint16_t *sc = reinterpret_cast<const uint16_t *>(base + rb) - (q0 & ~7);
-    const double *sv = reinterpret_cast<const double *>(base + cb) - (q0 & ~1);
-    for (int row_in_tile = tid / G; row_in_tile < ((rpt + (NT / G) - 1) / (NT / G)) * (NT / G);
-         row_in_tile += NT / G) {
-      const int r = r0 + row_in_tile;
-      const bool ok = row_in_tile < rpt && r < n;
-      const int lo = ok ? srp[row_in_tile] : 0, hi = ok ? srp[row_in_tile + 1] : 0;
-      const bool own = ok && sub == 0;
-      double eb = 0.0, ed = 0.0, ex = 0.0, edir = 0.0;
-      if (own) {
-        if (MODE == OP_RESID || MODE == OP_SUB_X0 || MODE == OP_SMOOTH) eb = __ldg(b + r);
-        if (MODE == OP_SUB_X0 || MODE == OP_SMOOTH || MODE == OP_SPMV_X0) ed = __ldg(dinv + r);
-        if (MODE == OP_SMOOTH) ex = __ldg(x + r);
-        if (MODE == OP_SMOOTH && dir) edir = dir[r];
-        if (MODE == OP_ADD) ex = y[r];
-      }
-      double acc = 0.0;
-#pragma unroll 4
-      for (int q = lo + sub; q < hi; q += G) acc += sv[q] * win[BF_LC(sc[q], cnt)];
-      if (G > 1) {
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-      }
-      if (!own) continue;
-      if (MODE == OP_SPMV) {
-        y[r] = acc;
-      } else if (MODE == OP_SPMV_X0) {
-        y[r] = acc;
-        aux[r] = beta * (acc * ed);
-      } else if (MODE == OP_RESID) {
-        y[r] = eb - acc;
-      } else if (MODE == OP_SUB_X0) {
-        double tt = eb - acc;
-        y[r] = tt;
-        aux[r] = beta * (tt * ed);
-      } else if (MODE == OP_SMOOTH) {
-        double dn = beta * ((eb - acc) * ed);
-        if (dir) dn += alpha * edir;
-        y[r] = ex + dn;
-        if (aux) aux[r] = dn;
-      } else if (MODE == OP_ADD) {
-        y[r] = ex + acc;
-      }
-    }
-    __syncthreads();  // every thread is done with stage s (and, at a super-tile's end, with the window)
-    if (tid == 0 && t + ST < t_end) issue(t + ST, s);
   }
   pdl_launch_dependents();
 }
 
-template <int MODE, int G>
-void launch_csr_win(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
-                    double *aux, double alpha, double beta, const double *dir) {
-  constexpr int ST = TMA_STAGES;
-  ensure_smem_attr((const void *)k_csr_win<MODE, G, ST>, 200 * 1024);
-  const int wsm = (A.wmax_used + 1) & ~1;
-  int smem = 8 * wsm + ST * win_stage_bytes(A.cap, A.rpt);
-  int ntiles = (A.n + A.rpt - 1) / A.rpt;
-  int per_sm = std::max(1, std::min(c->tune.tma_ctas, (220 * 1024) / (smem + 1024)));
-  int grid = std::min(ntiles, c->num_sms * per_sm);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TMA_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  BF_CUDA(cudaLaunchKernelEx(&cfg, k_csr_win<MODE, G, ST>, A.n, A.m, A.rpt, ntiles, A.cap, A.wk, (int)WIN_MAX,
-                             (const int32_t *)A.rp, (const uint16_t *)A.lc, (const double *)A.v,
-                             (const int32_t *)A.wn, (const int32_t *)A.wcol, x, b, dinv, y, aux, alpha, beta, dir,
-                             wsm));
+inline int wjds_smem_bytes(const WJds &W) {
+  return W.cap_ne * 10 + 8 * (((W.wmax_used + 1) & ~1) + WJDS_THREADS);
 }
 
 template <int MODE>
 bool csr_op_win(bf_ctx *c, const DCsr &A, const double *x, const double *b, const double *dinv, double *y,
                 double *aux, double alpha, double beta, const double *dir) {
-  if (!A.lc || A.cap <= 0) return false;
-  switch (A.g) {
-    case 1: launch_csr_win<MODE, 1>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 2: launch_csr_win<MODE, 2>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 4: launch_csr_win<MODE, 4>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 8: launch_csr_win<MODE, 8>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 16: launch_csr_win<MODE, 16>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    case 32: launch_csr_win<MODE, 32>(c, A, x, b, dinv, y, aux, alpha, beta, dir); break;
-    default: return false;
-  }
+  if (!A.ws || !A.ws->wrows) return false;
+  const WJds &W = *A.ws;
+  ensure_smem_attr((const void *)k_wjds<MODE>, 200 * 1024);
+  const int wsm = (W.wmax_used + 1) & ~1;
+  const int nblocks = (A.n + W.wrows - 1) / W.wrows;
+  launch_pdl(c, k_wjds<MODE>, dim3(nblocks), dim3(WJDS_THREADS), (size_t)wjds_smem_bytes(W), A.n, A.m, W.wrows,
+             (const int4 *)W.meta, (const uint16_t *)W.jdo, (const uint32_t *)W.rowinfo, (const uint16_t *)W.lc,
+             (const double *)W.wv, (const int32_t *)W.wcol, x, b, dinv, y, aux, alpha, beta, dir, wsm, W.cap_ne,
+             W.wstride);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
   return true;

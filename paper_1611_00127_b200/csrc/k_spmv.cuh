@@ -190,6 +190,7 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
   if (A.n == 0) return;
   c->alg_bytes += csr_op_bytes<MODE>(A, dir != nullptr, aux != nullptr);
   if (csr_op_dia<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
+  if (A.ws && csr_op_win<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (A.short_rows) {
     launch_pdl(c, k_csr_short<MODE>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y, aux,
                alpha, beta, dir);
@@ -197,7 +198,6 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
     BF_CUDA(cudaGetLastError());
     return;
   }
-  if (A.wk && c->use_tma && csr_op_win<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (c->use_tma && A.nnz >= c->tune.tma_min_nnz && csr_op_tma<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir))
     return;
   int G = lanes_for(c, A);

@@ -542,53 +542,133 @@ void tile_csr(bf_ctx *c, DCsr &A, bool stencil, int force_g) {
   dfree(c, mx);
 }
 
-// ---- shared-memory x windows (k_csr_win.cuh) ------------------------------------------------
-// one CTA per super-tile: distinct columns by a shared-memory hash table, bitonic sort, then every
-// nonzero's local index by binary search
-static __global__ void __launch_bounds__(256) k_win_build(int n, int rows, const int32_t *__restrict__ rp,
-                                                          const int32_t *__restrict__ ci, int32_t *__restrict__ wn,
-                                                          int32_t *__restrict__ wcol, uint16_t *__restrict__ lc,
+// ---- windowed jagged-diagonal form of the coarse-level operators (k_csr_win.cuh) ---------------
+// plan: one CTA per block of `wrows` rows sorts the block's rows by (length descending, row
+// ascending) and records the order with the lengths (rowinfo), the jagged-diagonal offsets (jdo)
+// and the block's entry count
+static __global__ void __launch_bounds__(256) k_wjds_plan(int n, int wrows, const int32_t *__restrict__ rp,
+                                                          uint32_t *__restrict__ rowinfo,
+                                                          uint16_t *__restrict__ jdo, int32_t *__restrict__ block_ne,
+                                                          int32_t *__restrict__ block_maxlen,
+                                                          int *__restrict__ stat) {
+  __shared__ int key[WIN_ROWS_MAX];
+  __shared__ int cnt_e[WJDS_MAXLEN + 1];
+  const int blk = blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < wrows; i += blockDim.x) {
+    const int r = blk * wrows + i;
+    int k = -1;  // padding row (beyond n)
+    if (r < n) {
+      const int len = rp[r + 1] - rp[r];
+      if (len > WJDS_MAXLEN) stat[5] = 1;  // row too long for the per-block offset table: no WJDS form
+      k = (min(len, WJDS_MAXLEN) << 16) | (0xffff - i);
+    }
+    key[i] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= wrows; k <<= 1)  // bitonic sort, descending
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < wrows; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int a = key[i], b = key[l];
+          const bool down = (i & k) == 0;
+          if ((a < b) == down) {
+            key[i] = b;
+            key[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int p = tid; p < wrows; p += blockDim.x) {
+    const int k = key[p];
+    rowinfo[(size_t)blk * wrows + p] = k < 0 ? 0xffffu : (((uint32_t)(k >> 16) << 16) | (uint32_t)(0xffff - (k & 0xffff)));
+  }
+  // rows longer than e: the sorted order makes them a prefix (binary search for its end)
+  for (int e = tid; e <= WJDS_MAXLEN; e += blockDim.x) {
+    int lo = 0, hi = wrows;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int k = key[mid];
+      if (k >= 0 && (k >> 16) > e) lo = mid + 1;
+      else hi = mid;
+    }
+    cnt_e[e] = lo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int off = 0, maxlen = 0;
+    for (int e = 0; e <= WJDS_MAXLEN; e++) {
+      jdo[(size_t)blk * (WJDS_MAXLEN + 1) + e] = (uint16_t)min(off, 0xffff);
+      if (cnt_e[e] > 0) maxlen = e + 1;
+      off += cnt_e[e];
+    }
+    if (off > 0xffff) stat[5] = 1;
+    block_ne[blk] = (off + 7) & ~7;
+    block_maxlen[blk] = maxlen;
+  }
+}
+
+// fill: one CTA per block: the block's distinct columns by a shared-memory hash table and a
+// bitonic sort (the window), then every entry written to its jagged-diagonal slot with its
+// position in the window (binary search); the padding entries up to a multiple of 8 are (0.0, 0)
+static __global__ void __launch_bounds__(256) k_wjds_fill(int n, int wrows, const int32_t *__restrict__ rp,
+                                                          const int32_t *__restrict__ ci,
+                                                          const double *__restrict__ v,
+                                                          const uint32_t *__restrict__ rowinfo,
+                                                          const uint16_t *__restrict__ jdo,
+                                                          const int32_t *__restrict__ eo,
+                                                          const int32_t *__restrict__ block_ne,
+                                                          const int32_t *__restrict__ block_maxlen,
+                                                          int4 *__restrict__ meta, int32_t *__restrict__ wcol,
+                                                          uint16_t *__restrict__ lc, double *__restrict__ wv,
                                                           int *__restrict__ stat, unsigned long long *total) {
   extern __shared__ int32_t win_sm[];
   int32_t *table = win_sm, *uniq = win_sm + WIN_HASH;
   __shared__ int cnt;
-  const int s = blockIdx.x, tid = threadIdx.x;
-  const int r0 = s * rows, r1 = min(n, r0 + rows);
+  const int blk = blockIdx.x, tid = threadIdx.x;
+  const int r0 = blk * wrows, r1 = min(n, r0 + wrows);
   const int q0 = rp[r0], q1 = rp[r1];
-  for (int i = tid; i < WIN_HASH; i += 256) table[i] = -1;
+  if (stat[5]) return;  // the plan met a row it cannot represent (lengths clamped): no form
+  // hash table sized for this block: at most min(nnz, WIN_MAX) distinct columns at load factor <= 1/2
+  int hbits = 10;
+  while (hbits < 13 && (1 << hbits) < 2 * min(q1 - q0, WIN_MAX)) hbits++;
+  const int hsize = 1 << hbits;
+  for (int i = tid; i < hsize; i += blockDim.x) table[i] = -1;
   if (tid == 0) cnt = 0;
   __syncthreads();
-  for (int q = q0 + tid; q < q1; q += 256) {
+  for (int q = q0 + tid; q < q1; q += blockDim.x) {
     const int col = ci[q];
-    unsigned slot = ((unsigned)col * 2654435761u) >> 18;  // 14 bits
-    for (int probe = 0; probe < WIN_HASH; probe++) {
+    unsigned slot = ((unsigned)col * 2654435761u) >> (32 - hbits);
+    for (int probe = 0; probe < hsize; probe++) {
       int old = atomicCAS(&table[slot], -1, col);
       if (old == -1 || old == col) break;
-      slot = (slot + 1) & (WIN_HASH - 1);
+      slot = (slot + 1) & (hsize - 1);
     }
   }
   __syncthreads();
-  for (int i = tid; i < WIN_HASH; i += 256)
+  for (int i = tid; i < hsize; i += blockDim.x)
     if (table[i] != -1) {
       int pos = atomicAdd(&cnt, 1);
       if (pos < WIN_MAX) uniq[pos] = table[i];
     }
   __syncthreads();
   const int c = cnt;
-  if (c > WIN_MAX) {  // the super-tile needs a larger window than shared memory holds
+  const int ne = block_ne[blk], e0 = eo[blk];
+  if (c > WIN_MAX) {  // the block needs a larger window than shared memory holds
     if (tid == 0) {
       stat[0] = 1;
-      wn[s] = 0;
+      meta[blk] = make_int4(e0, 0, 0, 0);
     }
     return;
   }
   int p2 = 2;
   while (p2 < c) p2 <<= 1;
-  for (int i = c + tid; i < p2; i += 256) uniq[i] = 0x7fffffff;
+  for (int i = c + tid; i < p2; i += blockDim.x) uniq[i] = 0x7fffffff;
   __syncthreads();
   for (int k = 2; k <= p2; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < p2; i += 256) {
+      for (int i = tid; i < p2; i += blockDim.x) {
         int l = i ^ j;
         if (l > i) {
           int a = uniq[i], b = uniq[l];
@@ -601,89 +681,151 @@ static __global__ void __launch_bounds__(256) k_win_build(int n, int rows, const
       }
       __syncthreads();
     }
-  for (int i = tid; i < c; i += 256) wcol[(size_t)s * WIN_MAX + i] = uniq[i];
+  for (int i = tid; i < c; i += blockDim.x) wcol[(size_t)blk * WIN_MAX + i] = uniq[i];
   if (tid == 0) {
-    wn[s] = c;
+    meta[blk] = make_int4(e0, ne, c, block_maxlen[blk]);
     atomicMax(&stat[1], c);
+    atomicMax(&stat[4], ne);
     atomicAdd(total, (unsigned long long)c);
   }
-  for (int q = q0 + tid; q < q1; q += 256) {
-    const int col = ci[q];
-    int lo = 0, hi = c - 1;
+  // entries in jagged-diagonal order, one thread per entry: flat position i -> diagonal e (binary
+  // search in the block's offsets) and sorted row position t = i - off[e]
+  __shared__ uint16_t off[WJDS_MAXLEN + 1];
+  __shared__ int rowq[WIN_ROWS_MAX];
+  for (int e = tid; e <= WJDS_MAXLEN; e += blockDim.x) off[e] = jdo[(size_t)blk * (WJDS_MAXLEN + 1) + e];
+  for (int t = tid; t < wrows; t += blockDim.x) {
+    const int lr = (int)(rowinfo[(size_t)blk * wrows + t] & 0xffffu);
+    rowq[t] = lr == 0xffff ? 0 : rp[r0 + lr];
+  }
+  __syncthreads();
+  const int maxlen = block_maxlen[blk];
+  for (int i = tid; i < q1 - q0; i += blockDim.x) {
+    int lo = 0, hi = maxlen - 1;
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
+      const int mid = (lo + hi + 1) >> 1;
+      if ((int)off[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, t = i - (int)off[e];
+    const int q = rowq[t] + e;
+    const int col = ci[q];
+    lo = 0;
+    hi = c - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
       if (uniq[mid] < col) lo = mid + 1;
       else hi = mid;
     }
-    if (BF_CHK(uniq[lo] == col)) lc[q] = (uint16_t)lo;
+    wv[(size_t)e0 + i] = v[q];
+    lc[(size_t)e0 + i] = BF_CHK(uniq[lo] == col) ? (uint16_t)lo : (uint16_t)0;
   }
+  for (int i = (q1 - q0) + tid; i < ne; i += blockDim.x) {  // padding entries
+    wv[(size_t)e0 + i] = 0.0;
+    lc[(size_t)e0 + i] = 0;
+  }
+}
+
+// wcol with the matrix's own stride instead of WIN_MAX slots per block
+static __global__ void k_wjds_compact(int nblocks, int wstride, const int4 *__restrict__ meta,
+                                      const int32_t *__restrict__ wide, int32_t *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nblocks * wstride) return;
+  const int blk = (int)(i / wstride), k = (int)(i % wstride);
+  out[i] = k < meta[blk].z ? wide[(size_t)blk * WIN_MAX + k] : 0;  // zero padded up to the stride
 }
 
 void free_window(bf_ctx *c, DCsr &A) {
-  dfree(c, A.lc);
-  dfree(c, A.wn);
-  dfree(c, A.wcol);
-  A.lc = nullptr;
-  A.wn = nullptr;
-  A.wcol = nullptr;
-  A.wk = 0;
-  A.wmax_used = 0;
+  if (!A.ws) return;
+  dfree(c, A.ws->meta);
+  dfree(c, A.ws->jdo);
+  dfree(c, A.ws->rowinfo);
+  dfree(c, A.ws->wv);
+  dfree(c, A.ws->lc);
+  dfree(c, A.ws->wcol);
+  delete A.ws;
+  A.ws = nullptr;
 }
 
-// Give a TMA-tiled matrix its shared-memory windows (super-tiles of wk tiles ~ win_rows rows);
-// halves the super-tile while some window exceeds WIN_MAX, gives up (plain TMA kernel) if single
-// tiles do, or if the windows hold too many entries per nonzero (no locality to exploit).
+// Build the windowed jagged-diagonal form of A (k_csr_win.cuh): blocks of wrows rows sized so that a
+// block's stream is ~WJDS_STAGE_TARGET bytes; wrows is halved while some block's window exceeds
+// WIN_MAX or its stream WJDS_STAGE_MAX; the form is dropped (CSR kernels) if no block size fits, if
+// a row is longer than WJDS_MAXLEN, or if the windows hold more than win_ratio entries per nonzero
+// (no column reuse to exploit).
 void window_csr(bf_ctx *c, DCsr &A) {
   free_window(c, A);
-  if (!c->tune.win || !c->use_tma || A.cap <= 0 || A.short_rows || A.dia_v || A.n < c->tune.win_nmin ||
-      A.nnz < c->tune.tma_min_nnz || A.nnz <= 0)
-    return;
-  ensure_smem_attr((const void *)k_win_build, (WIN_HASH + WIN_MAX) * 4 + 1024);
-  int *stat = dalloc_t<int>(c, 4);
+  if (!c->tune.win || A.dia_v || A.n < c->tune.win_nmin || A.nnz <= 0) return;
+  const double mean = (double)A.nnz / A.n;
+  if (mean < c->tune.win_minlen) return;
+  ensure_smem_attr((const void *)k_wjds_fill, (WIN_HASH + WIN_MAX) * 4 + 1024);
+  int *stat = dalloc_t<int>(c, 8);
   unsigned long long *total = reinterpret_cast<unsigned long long *>(stat + 2);
-  A.lc = dalloc_t<uint16_t>(c, (size_t)A.nnz + 8);
-  for (int K = std::max(1, c->tune.win_rows / A.rpt);; K >>= 1) {
-    const int rows = K * A.rpt;
-    const int nsuper = (A.n + rows - 1) / rows;
-    A.wn = dalloc_t<int32_t>(c, nsuper);
-    A.wcol = dalloc_t<int32_t>(c, (size_t)nsuper * WIN_MAX);
-    BF_CUDA(cudaMemsetAsync(stat, 0, 16, c->stream));
-    k_win_build<<<nsuper, 256, (WIN_HASH + WIN_MAX) * 4, c->stream>>>(A.n, rows, A.rp, A.ci, A.wn, A.wcol, A.lc, stat,
-                                                                      total);
+  int wrows = std::min(WIN_ROWS_MAX, std::max(32, c->tune.win_rows));
+  while (wrows & (wrows - 1)) wrows &= wrows - 1;  // power of two
+  while (wrows > 32 && wrows * mean * 10.0 > c->tune.win_stage) wrows >>= 1;
+  for (;; wrows >>= 1) {
+    A.ws = new WJds();
+    WJds &W = *A.ws;
+    const int nblocks = (A.n + wrows - 1) / wrows;
+    W.rowinfo = dalloc_t<uint32_t>(c, (size_t)nblocks * wrows);
+    W.jdo = dalloc_t<uint16_t>(c, (size_t)nblocks * (WJDS_MAXLEN + 1));
+    int32_t *bne = dalloc_t<int32_t>(c, (size_t)nblocks + 1), *bml = dalloc_t<int32_t>(c, nblocks);
+    int32_t *eo = dalloc_t<int32_t>(c, (size_t)nblocks + 1);
+    BF_CUDA(cudaMemsetAsync(stat, 0, 32, c->stream));
+    k_wjds_plan<<<nblocks, 256, 0, c->stream>>>(A.n, wrows, A.rp, W.rowinfo, W.jdo, bne, bml, stat);
     BF_LAUNCH(c);
-    int hs[4] = {0, 0, 0, 0};
-    BF_CUDA(cudaMemcpyAsync(hs, stat, 16, cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
+    const int64_t entries = exclusive_scan_i32(c, bne, eo, nblocks);  // syncs
+    int hs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool ok = entries < (1ll << 31) - 8;  // (a too-long row, stat[0] = 2, is seen after the fill: its length is clamped)
+    if (ok) {
+      W.meta = dalloc_t<int4>(c, nblocks);
+      W.wcol = dalloc_t<int32_t>(c, (size_t)nblocks * WIN_MAX);
+      W.lc = dalloc_t<uint16_t>(c, (size_t)entries + 8);
+      W.wv = dalloc_t<double>(c, (size_t)entries + 2);
+      k_wjds_fill<<<nblocks, 256, (WIN_HASH + WIN_MAX) * 4, c->stream>>>(
+          A.n, wrows, A.rp, A.ci, A.v, W.rowinfo, W.jdo, eo, bne, bml, W.meta, W.wcol, W.lc, W.wv, stat, total);
+      BF_LAUNCH(c);
+      BF_CUDA(cudaMemcpyAsync(hs, stat, 32, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      ok = hs[5] == 0;
+    }
+    dfree(c, bne);
+    dfree(c, bml);
+    dfree(c, eo);
     unsigned long long tot;
     memcpy(&tot, hs + 2, sizeof tot);
-    if (!hs[0]) {
-      if ((double)tot > c->tune.win_ratio * (double)A.nnz) break;  // no reuse: not worth a window
-      A.wk = K;
-      A.wmax_used = hs[1];
+    const bool too_big = ok && (hs[0] == 1 || hs[4] * 10 > WJDS_STAGE_MAX);  // window or stream: smaller blocks
+    if (ok && !too_big && (double)tot <= c->tune.win_ratio * (double)A.nnz) {
+      W.wrows = wrows;
+      W.wmax_used = hs[1];
+      W.cap_ne = hs[4];
+      W.wstride = std::min(WIN_MAX, (hs[1] + 255) & ~255);
+      int32_t *wide = W.wcol;
+      W.wcol = dalloc_t<int32_t>(c, (size_t)nblocks * W.wstride);
+      k_wjds_compact<<<div_up((int64_t)nblocks * W.wstride, 256), 256, 0, c->stream>>>(nblocks, W.wstride, W.meta, wide,
+                                                                                                W.wcol);
+      BF_LAUNCH(c);
+      dfree(c, wide);
       if (c->tune.verbose)
-        fprintf(stderr, "[bf_setup]   window: n %d nnz %lld rpt %d K %d: %d super-tiles, max window %d, %.3f entries/nnz\n",
-                A.n, (long long)A.nnz, A.rpt, K, nsuper, hs[1], (double)tot / (double)A.nnz);
+        fprintf(stderr,
+                "[bf_setup]   wjds: %d x %d, nnz %lld, blocks of %d rows: %d blocks, max window %d, max stream %d B, "
+                "%.3f window entries/nnz\n",
+                A.n, A.m, (long long)A.nnz, wrows, nblocks, hs[1], hs[4] * 10, (double)tot / (double)A.nnz);
       dfree(c, stat);
       return;
     }
-    dfree(c, A.wn);
-    dfree(c, A.wcol);
-    A.wn = nullptr;
-    A.wcol = nullptr;
-    if (K == 1) break;
+    free_window(c, A);
+    if (!(too_big && wrows > 32)) break;
   }
   dfree(c, stat);
-  free_window(c, A);
 }
 
-// windows for the coarse levels of a hierarchy: A_l and the fused restriction Rf_l (window_csr
-// keeps them only where the rows share columns: the renumbered levels)
+// WJDS forms for the coarse levels of a hierarchy: A_l, l >= 1, above the tail.  Measured on C3 and
+// not given a form: the fused restrictions Rf_l (rows of ~100 entries over ~0.4 window columns per
+// nonzero: 48 us against 45 us for the TMA CSR kernel) and the level transfers P_l, R_l (2-6 entries
+// per row, 0.5-0.6 window columns per nonzero: 40 us against 30 us for the thread-per-row kernel).
 void build_windows(bf_ctx *c, Hier &h) {
-  for (int l = 0; l < h.nlev - 1; l++) {
-    Level &L = h.lv[l];
-    if (l >= 1) window_csr(c, L.A);
-    if (l >= 1 && L.Rf.n) window_csr(c, L.Rf);
-  }
+  const int lend = h.dtail >= 0 ? h.dtail : (h.tail >= 0 ? h.tail : h.nlev - 1);
+  for (int l = 1; l < lend; l++) window_csr(c, h.lv[l].A);
   BF_CUDA(cudaGetLastError());
 }
 

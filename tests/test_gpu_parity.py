@@ -347,11 +347,14 @@ VARIANTS = {
     "plain": {"BF_NO_DTAIL": "1", "BF_NO_RFUSE": "1", "BF_NO_TAIL": "1", "BF_NO_DIA": "1", "BF_NO_TMA": "1"},
     "coop-tail-big": {"BF_NO_DTAIL": "1", "BF_TAIL_NNZ": "200000"},
     "no-reorder": {"BF_NO_REORDER": "1"},
-    # shared-memory x windows (k_csr_win.cuh) forced onto these small hierarchies: every CSR level,
-    # accepted whatever their reuse; super-tiles of 64 and 512 rows; and switched off
-    "win-all-64": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_ROWS": "64"},
-    "win-all-512": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_ROWS": "512", "BF_NO_DTAIL": "1"},
-    "no-win": {"BF_NO_WIN": "1"},
+    # windowed jagged-diagonal kernels (k_csr_win.cuh) forced onto these small hierarchies: every CSR
+    # level above the tail, accepted whatever its reuse; blocks of 256 / 64 / 32 rows (1, 4 and 8
+    # thread groups per row); and switched off
+    "wjds-256": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_STAGE": "1000000"},
+    "wjds-64": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_ROWS": "64", "BF_NO_DTAIL": "1"},
+    "wjds-32": {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_WIN_STAGE": "1024", "BF_NO_DTAIL": "1",
+                "BF_NO_TAIL": "1"},
+    "no-wjds": {"BF_NO_WIN": "1"},
 }
 
 
@@ -385,12 +388,18 @@ def test_solve_path_variants(variant, config, dims, monkeypatch):
     g.close()
 
 
-def test_long_rows_hash_overflow_regression():
-    """A hub cell coupled to 700 others through A_ss only makes A_ss rows (and its Galerkin
+@pytest.mark.parametrize("force_wjds", [False, True])
+def test_long_rows_hash_overflow_regression(force_wjds, monkeypatch):
+    """(force_wjds: the windowed jagged-diagonal form is requested for every CSR level, whatever its
+    size or reuse; the levels whose hub row exceeds the form's 255-entry row limit must fall back to
+    the CSR kernels, the others use it.)  A hub cell coupled to 700 others through A_ss only makes A_ss rows (and its Galerkin
     products) longer than the 512-slot shared-memory hash table of the SpGEMM (the C5 setup hang
     of round 1): setup must fall back to the expand-sort-compress product and stay bit-exact
     with the oracle.  (S~ keeps short rows: its row pattern is bounded at 256 entries,
     BF_ERR_LIMIT beyond.)"""
+    if force_wjds:
+        for k, v in {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_NO_DTAIL": "1", "BF_NO_TAIL": "1"}.items():
+            monkeypatch.setenv(k, v)
     n = 1200
     rng = np.random.default_rng(11)
     hub = set(rng.choice(np.arange(1, n), 700, replace=False).tolist())
