@@ -28,7 +28,7 @@ launches)
   python tools/traffic_summary.py $O/launches_step.csv > $O/traffic.json 2> $O/traffic.err;;
 full)
   ncu --set full --clock-control none --import-source on \
-      -k regex:'k_csr|k_dia|k_bsr2|k_dots|k_axpy|k_split|k_merge|k_dense_tail|k_vcycle_tail|k_coarse_inv' \
+      -k regex:'k_csr|k_wjds|k_dia|k_bsr2|k_dots|k_axpy|k_split|k_merge|k_dense_tail|k_vcycle_tail|k_coarse_inv' \
       -s 70 -c 150 -o $O/full_apply python tools/profile_step.py --config 3 --maxit 30 > $O/ncu_full.log 2>&1
   python tools/ncu_table.py $O/full_apply.ncu-rep 150 > $O/full_apply_table.txt 2>&1
   # gpurun_out/ is capped at 64 MiB: keep the report only if it is small
