@@ -386,7 +386,7 @@ def run_ours(args):
     kt = rec["kt"]
     cls = {0: "bsr2_spmv (J SpMV, one DIA-BSR kernel; bytes: SURVEY 8(d) 36 B/block + 36 B/row)",
            1: "gmres_cgs2 (3 fused orthogonalisation passes per Arnoldi step; bytes: 8N(3j+5))",
-           2: "bf_apply (Algorithm 3: two V-cycles + A_ps coupling, ~37 DIA/TMA-CSR kernels + a dense tail operator in one CUDA graph; "
+           2: "bf_apply (Algorithm 3: two V-cycles + A_ps coupling, ~50 DIA / windowed-JDS / TMA-CSR kernels + two dense tail operators in one CUDA graph; "
               "bytes: SURVEY 8(d) per-level V(1,1) model on the actual hierarchies)"}
 
     n_arnoldi = float(sum(rec["iters"]))

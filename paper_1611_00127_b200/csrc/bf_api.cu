@@ -314,6 +314,7 @@ Tuning tuning_from_env() {
   t.merge_fuse = !env_flag("BF_NO_MERGE_FUSE");
   t.short_lim = env_num("BF_SHORT", t.short_lim);
   t.short_nmin = (int64_t)env_num("BF_SHORT_N", (double)t.short_nmin);
+  t.short_k4 = env_num("BF_SHORT_K4", t.short_k4);
   t.stencil_g2 = env_num("BF_STENCIL_G2", t.stencil_g2);
   t.tma_g_div = env_num("BF_TMA_G", t.tma_g_div);
   t.tma_tile = env_num("BF_TMA_TILE", t.tma_tile);

@@ -101,6 +101,7 @@ struct Tuning {
   bool rfuse_l0 = false;    // ... also on the finest level (measured slower)
   bool merge_fuse = true;   // S~ finest post-sweep fused with the merge
   double short_lim = 8.0;   // thread-per-row kernel for P / R with mean row length <= short_lim ...
+  double short_k4 = 3.0;    // ... with 4 register slots per row up to this mean row length, 8 above
   int64_t short_nmin = 65536;  // ... and at least this many rows
   double stencil_g2 = 8.0;  // stencil rows longer than this on average get 2 lanes per row
   double tma_g_div = 4.0;   // Galerkin rows: lanes per row ~ mean row length / tma_g_div

@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(CSR_WARPS * 32) k_csr(int n, int m, const int3
 // loaded into registers BEFORE griddepcontrol.wait (programmatic dependent launch), so only
 // the gathers of x and the epilogue wait for the kernel that produced x; consecutive threads'
 // entries are contiguous, so the streaming loads of a warp coalesce.
-constexpr int SHORT_K = 8;
-template <int MODE>
-__global__ void __launch_bounds__(256) k_csr_short(int n, int m, const int32_t *__restrict__ rp,
+// SHORT_K register slots per row: 4 for the interpolation-like matrices (mean row length <= 3:
+// fewer registers, 8 CTAs per SM), 8 otherwise; longer rows finish in a scalar loop.
+template <int MODE, int SHORT_K>
+__global__ void __launch_bounds__(256, SHORT_K == 4 ? 8 : 6) k_csr_short(int n, int m, const int32_t *__restrict__ rp,
                                                    const int32_t *__restrict__ ci,
                                                    const double *__restrict__ v, const double *__restrict__ x,
                                                    const double *__restrict__ b, const double *__restrict__ dinv,
@@ -192,8 +193,12 @@ void csr_op(bf_ctx *c, const DCsr &A, const double *x, const double *b, const do
   if (csr_op_dia<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (A.ws && csr_op_win<MODE>(c, A, x, b, dinv, y, aux, alpha, beta, dir)) return;
   if (A.short_rows) {
-    launch_pdl(c, k_csr_short<MODE>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y, aux,
-               alpha, beta, dir);
+    if ((double)A.nnz <= c->tune.short_k4 * (double)A.n)
+      launch_pdl(c, k_csr_short<MODE, 4>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y,
+                 aux, alpha, beta, dir);
+    else
+      launch_pdl(c, k_csr_short<MODE, 8>, dim3(div_up(A.n, 256)), dim3(256), 0, A.n, A.m, A.rp, A.ci, A.v, x, b, dinv, y,
+                 aux, alpha, beta, dir);
     BF_LAUNCH(c);
     BF_CUDA(cudaGetLastError());
     return;
