@@ -113,6 +113,11 @@ typedef struct {
                                   -- DESIGN.md R22 */
   int32_t cheb_levels;         /* a Chebyshev hierarchy smooths its levels l < cheb_levels with Chebyshev
                                   and the coarser ones with l1-Jacobi; 0: every level (R22) */
+  int32_t diag_stop;           /* 1 (default): coarsening stops before a level whose Galerkin operator has a
+                                  non-positive diagonal entry; the level above becomes the coarsest one
+                                  (dense LU, or 4 l1-Jacobi sweeps when it has more than max_coarse rows)
+                                  -- DESIGN.md R23.  0: no such stop.  The hierarchy of the coupled AMG
+                                  (precond 3, the paper's failing comparison) never stops this way. */
 } bf_options;
 
 typedef struct bf_ctx *bf_handle;

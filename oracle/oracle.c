@@ -51,6 +51,7 @@ void or_default_options(or_options *o) {
   o->cheb_eig = 0;        /* R21: Gershgorin interval end 1 */
   o->smoother_p = 0;      /* ... and l1-Jacobi for S~ / A_pp / J (R22) */
   o->cheb_levels = 0;     /* R22 */
+  o->diag_stop = 1;       /* R23 */
 }
 
 /* options of one hierarchy: every hierarchy but A_ss (S~, A_pp, J) takes smoother_p (R22) */
@@ -512,6 +513,16 @@ static void csr_copy(const or_csr *A, or_csr *B) {
 /* ------------------------------------------------------------------------ */
 /* AMG setup (c.2 steps 3-4)                                    */
 /* ------------------------------------------------------------------------ */
+/* 1 if every row of A has a stored diagonal entry > 0 (R23) */
+static int or_diag_positive(const or_csr *A) {
+  for (int32_t i = 0; i < A->nrows; i++) {
+    double aii = 0.0;
+    for (int64_t q = A->rp[i]; q < A->rp[i + 1]; q++) if (A->ci[q] == i) aii = A->v[q];
+    if (!(aii > 0.0)) return 0;
+  }
+  return 1;
+}
+
 int or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h) {
   memset(h, 0, sizeof *h);
   h->opt = *o;
@@ -539,6 +550,16 @@ int or_amg_setup(const or_csr *A0, const or_options *o, or_amg *h) {
     or_matmul(A, &h->P[l], &AP);
     or_matmul(&h->R[l], &AP, &h->A[l + 1]);
     or_csr_free(&AP);
+    /* R23: coarsening stops before a level whose Galerkin operator has a non-positive (or
+     * missing) diagonal entry -- the classical strength / interpolation formulas (R4-R8) and the
+     * l1 divisor a_ii + sum |a_ij| presuppose a_ii > 0.  Level l then is the coarsest level
+     * (the stalled-coarsening rule of c.2 3.7 below: 4 l1-Jacobi sweeps if it is too large for
+     * the dense LU). */
+    if (o->diag_stop && !or_diag_positive(&h->A[l + 1])) {
+      or_csr_free(&h->P[l]); or_csr_free(&h->R[l]); or_csr_free(&h->A[l + 1]);
+      free(strong); free(cf);
+      break;
+    }
     h->cf[l] = cf;
     h->strong[l] = strong;
     l++;
@@ -816,7 +837,9 @@ static int build_precond(or_bf *b) {
   const or_options ot = hier_options(o, 0), op = hier_options(o, 1);
   if (o->precond == 3) {
     or_jscalar(b->n, b->brp, b->bci, b->bv, &b->Jsc);
-    return or_amg_setup(&b->Jsc, &op, &b->hJ);
+    or_options oj = op;
+    oj.diag_stop = 0;     /* R23: the paper's coupled AMG comparison stays the classical algorithm */
+    return or_amg_setup(&b->Jsc, &oj, &b->hJ);
   }
   if (o->precond == 0 || o->precond == 2) {
     st = or_amg_setup(&b->Ass, &ot, &b->hss);

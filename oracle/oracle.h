@@ -46,6 +46,9 @@ typedef struct {
                               AMG), default 0 (l1-Jacobi); -1: the same as `smoother` -- R22 */
   int32_t  cheb_levels;    /* Chebyshev hierarchies smooth levels l < cheb_levels with Chebyshev and the
                               coarser ones with l1-Jacobi; 0: every level (R22) */
+  int32_t  diag_stop;      /* 1 (default): coarsening stops before a Galerkin level with a non-positive
+                              diagonal entry (R23); 0: classical, no such stop.  The coupled AMG's
+                              hierarchy (precond 3) never stops this way (R23) */
 } or_options;
 
 #define OR_MAX_LEVELS 64

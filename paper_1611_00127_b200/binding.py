@@ -48,7 +48,7 @@ class bf_options(C.Structure):
                 ("cheb_degree", C.c_int32), ("cheb_lo", C.c_double), ("seed", C.c_uint64),
                 ("orth", C.c_int32), ("schur_as_printed", C.c_int32), ("interp_norm", C.c_int32),
                 ("timing", C.c_int32), ("precond", C.c_int32), ("cheb_eig", C.c_int32),
-                ("smoother_p", C.c_int32), ("cheb_levels", C.c_int32)]
+                ("smoother_p", C.c_int32), ("cheb_levels", C.c_int32), ("diag_stop", C.c_int32)]
 
 
 class bf_twophase(C.Structure):

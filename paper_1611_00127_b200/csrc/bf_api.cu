@@ -425,6 +425,7 @@ bf_status bf_default_options(bf_options *o) {
   o->cheb_eig = 0;
   o->smoother_p = 0;
   o->cheb_levels = 0;
+  o->diag_stop = 1;  // R23
   return BF_OK;
 }
 
@@ -435,6 +436,7 @@ static const char *check_options(const bf_options *o) {
   if (o->smoother != 0 && o->smoother != 1) return "smoother must be 0 or 1";
   if (o->smoother_p < -1 || o->smoother_p > 1) return "smoother_p must be -1, 0 or 1";
   if (o->cheb_levels < 0) return "cheb_levels must be >= 0";
+  if (o->diag_stop != 0 && o->diag_stop != 1) return "diag_stop must be 0 or 1";
   if (o->nu_pre < 0 || o->nu_post < 0 || o->nu_pre > 8 || o->nu_post > 8) return "nu_pre/nu_post in [0, 8]";
   const bool cheb = o->smoother == 1 || o->smoother_p == 1;
   if (cheb && (o->cheb_degree < 1 || o->cheb_degree > 8)) return "cheb_degree in [1, 8]";

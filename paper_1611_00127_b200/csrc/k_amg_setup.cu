@@ -41,6 +41,16 @@ __global__ void k_diag(DCsr A, double *diag) {
   diag[i] = d;
 }
 
+// R23: *flag = 1 if a row of A has no stored diagonal entry > 0
+__global__ void k_diag_nonpos(DCsr A, int *flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  double d = 0.0;
+  for (int q = A.rp[i]; q < A.rp[i + 1]; q++)
+    if (A.ci[q] == i) d = A.v[q];
+  if (!(d > 0.0)) atomicMax(flag, 1);
+}
+
 // l1 diagonal d_i = a_ii + sum_{j != i, ascending} |a_ij|
 __global__ void k_l1diag(DCsr A, const double *__restrict__ diag, double *dl1) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1420,6 +1430,26 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
               "[bf_setup]   h%d L%d n=%d nnz=%lld: strength %.2f pmis %.2f interp %.2f transpose %.2f AP %.2f RAP %.2f ms\n",
               which, l, n, (long long)A.nnz, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, t6));
     free_csr(c, AP);
+    if (o.diag_stop && which != 3) {  // R23: coarsening stops before a Galerkin level with a non-positive (or missing) diagonal entry;
+       // level l then is the coarsest level (stalled-coarsening rule: dense LU or 4 l1-Jacobi sweeps)
+      DCsr &Ac = h.lv[l + 1].A;
+      int *bad_d = nU_d + 3;
+      BF_CUDA(cudaMemsetAsync(bad_d, 0, sizeof(int), c->stream));
+      k_diag_nonpos<<<div_up(Ac.n, 256), 256, 0, c->stream>>>(Ac, bad_d);
+      BF_LAUNCH(c);
+      int bad = 0;
+      BF_CUDA(cudaMemcpyAsync(&bad, bad_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      if (bad) {
+        if (verbose) fprintf(stderr, "[bf_setup]   h%d L%d: Galerkin diagonal not positive, coarsening stops (R23)\n", which, l + 1);
+        free_csr(c, Ac);
+        free_csr(c, L.P);
+        free_csr(c, L.R);
+        dfree(c, L.cf);
+        L.cf = nullptr;
+        break;
+      }
+    }
     l++;
   }
   dfree(c, nU_d);

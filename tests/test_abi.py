@@ -56,6 +56,7 @@ def test_default_options_without_gpu():
     assert o.precond == 0  # BF (Algorithm 3); 1, 2 CPR-AMG(1)/(2), 3 coupled AMG
     # R22: Chebyshev(2) on [0.1, 1] for A_ss, l1-Jacobi for S~ (and A_pp, J); the oracle agrees
     assert (o.smoother, o.smoother_p, o.cheb_degree, o.cheb_lo, o.cheb_levels, o.cheb_eig) == (1, 0, 2, 0.1, 0, 0)
+    assert o.diag_stop == 1  # R23
     import oracle
     oo = oracle.default_options()
     for f, _ in oracle.Options._fields_:

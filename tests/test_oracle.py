@@ -371,13 +371,15 @@ def test_poisson_convergence_factor():
     """BJ oracle check 3: asymptotic V(1,1) l1-Jacobi convergence factor on the 2D 5-point /
     3D 7-point Laplacian, bounded and non-growing under refinement.  Bound calibrated once for
     PMIS + classical interpolation + l1-Jacobi (l1-Jacobi on the Laplacian is Jacobi damped by
-    1/2, smoothing factor 3/4): 2D <= 0.75, 3D <= 0.70, growth <= +0.05 per refinement."""
+    1/2, smoothing factor 3/4): 2D <= 0.75, 3D <= 0.70, growth <= +0.05 per refinement.  The bounds were
+    calibrated at the classical strength threshold 0.25, which the test therefore names (the default
+    moved to 0.18 with reading R23; on the Laplacian the threshold only acts on the Galerkin levels)."""
     for d, sizes, bound in ((2, (32, 64, 128), 0.75), (3, (16, 32), 0.70)):
         f, fc = [], []
         for m in sizes:
             A = lap(m, d)
-            f.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=0)))
-            fc.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=1, cheb_lo=0.1)))
+            f.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=0, theta=0.25)))
+            fc.append(_conv_factor(A, oracle.AMG(CSR.from_scipy(A), smoother=1, cheb_lo=0.1, theta=0.25)))
         assert max(f) <= bound, (d, f)
         assert all(f[i + 1] <= f[i] + 0.05 for i in range(len(f) - 1)), (d, f)
         # Chebyshev(2) on [0.1, 1] (R22) is the stronger smoother at every size (2D: 0.52 / 0.60 / 0.72
@@ -695,3 +697,51 @@ def test_chebyshev_interval_from_power_estimate():
             est = oracle.power_estimate(L["A"], L["dl1"], 12, seed=0x1611, level=l)
             assert L["cheb_hi"] == 1.1 * est
     assert all(oracle.BF(J, smoother=1).level(0, l)["cheb_hi"] == 1.0 for l in range(2))
+
+
+def test_diag_stop_rule():
+    """Reading R23: coarsening stops before a Galerkin level with a non-positive diagonal entry.
+    Pinned against scipy: on the C2 recipe (advection-dominated A_ss) the classical hierarchy
+    (diag_stop=0) has such a level; P^T A P recomputed with scipy from the level above confirms
+    the sign; with the rule on the hierarchy is the classical one cut just above that level, and
+    its last level -- too large for the dense LU -- is solved by 4 l1-Jacobi sweeps from zero
+    (the stalled-coarsening rule).  Where every Galerkin diagonal is positive (S~, Poisson) the
+    rule changes nothing, bit for bit."""
+    prob, J, rhs = tiny_system((12, 12, 12), config=2)
+    b0, b1 = oracle.BF(J, diag_stop=0), oracle.BF(J)
+    mins = [b0.level(0, l)["A"].to_scipy().diagonal().min() for l in range(b0.nlev(0))]
+    bad = next(l for l, m in enumerate(mins) if m <= 0.0)
+    assert bad >= 2                                    # the case keeps one coarse level
+    L = b0.level(0, bad - 1)
+    Ac = (L["P"].to_scipy().T @ L["A"].to_scipy() @ L["P"].to_scipy()).tocsr()
+    assert Ac.diagonal().min() <= 0.0                  # scipy's product agrees about the sign
+    assert b1.nlev(0) == bad                           # levels 0 .. bad-1 kept
+    for l in range(bad):
+        for k in ("A", "dl1") + (("P", "cf") if l < bad - 1 else ()):
+            x0, x1 = b0.level(0, l)[k], b1.level(0, l)[k]
+            if isinstance(x0, CSR):
+                assert np.array_equal(x0.to_dense(), x1.to_dense())
+            else:
+                assert np.array_equal(x0, x1)
+    # S~ has positive Galerkin diagonals: identical hierarchies and V-cycles
+    assert b0.nlev(1) == b1.nlev(1)
+    v = seeded_vector(J.n, 3)
+    assert np.array_equal(b0.vcycle(1, v), b1.vcycle(1, v))
+    # an A_ss hierarchy cut at level 0: the "solve" is 4 l1-Jacobi sweeps from zero
+    prob, J, rhs = tiny_system((8, 8, 8), config=2)
+    b1 = oracle.BF(J)
+    assert b1.nlev(0) == 1 and oracle.BF(J, diag_stop=0).nlev(0) > 1
+    A = b1.level(0, 0)["A"].to_scipy()
+    d = b1.level(0, 0)["dl1"]
+    v = seeded_vector(J.n, 4)
+    x = np.zeros(J.n)
+    for _ in range(4):
+        x = x + (v - A @ x) / d
+    got = b1.vcycle(0, v)
+    assert np.max(np.abs(got - x)) <= 1e-13 * np.max(np.abs(x))
+    # Poisson: no effect
+    Ap = CSR.from_scipy(lap(12, 3))
+    h0, h1 = oracle.AMG(Ap, diag_stop=0), oracle.AMG(Ap)
+    assert h0.nlev == h1.nlev > 1
+    w = seeded_vector(12 ** 3, 5)
+    assert np.array_equal(h0.vcycle(w), h1.vcycle(w))

@@ -49,6 +49,8 @@ MUTANTS = [
     ("PMIS index tie-break reversed", "(key[a] == key[b] && (a) > (b))", "(key[a] == key[b] && (a) < (b))", 1),
     ("V-cycle post-smoother skipped", "for (int s = 0; s < h->opt.nu_post; s++) smooth(h, l, b, x, tmp, dir);", "", 1),
     ("BF apply: A_ps coupling sign flipped", "rp[c] = rp[c] - t[c];", "rp[c] = rp[c] + t[c];", 1),
+    ("R23 stop at a non-positive Galerkin diagonal accepts a zero diagonal", "if (!(aii > 0.0)) return 0;",
+     "if (aii < -1e300) return 0;", 1),
     ("block ILU(0): fill update sign flipped", "lu[4 * t + e] = lu[4 * t + e] - P[e];", "lu[4 * t + e] = lu[4 * t + e] + P[e];", 1),
 ]
 
