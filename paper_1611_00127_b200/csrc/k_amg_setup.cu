@@ -544,12 +544,12 @@ constexpr int HASH_MAX = 320;        // max distinct columns per row (load facto
 
 // per-row table size: the smallest power of two >= 2 * (upper bound of the row's distinct
 // columns), at least 32, at most HASH_CAP -- small rows (most of them) touch few slots
-__device__ __forceinline__ int row_table_mask(const DCsr &A, const DCsr &B, int i, int lane) {
+__device__ __forceinline__ int row_table_mask(const DCsr &A, const DCsr &B, int i, int lane, int cap = HASH_CAP) {
   int ub = 0;
   for (int q = A.rp[i] + lane; q < A.rp[i + 1]; q += 32) ub += B.rp[A.ci[q] + 1] - B.rp[A.ci[q]];
   for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
   int t = 32;
-  while (t < HASH_CAP && t < 2 * ub) t <<= 1;
+  while (t < cap && t < 2 * ub) t <<= 1;
   return t - 1;
 }
 
@@ -590,12 +590,13 @@ __device__ __forceinline__ RowChunk load_chunk(const DCsr &A, const DCsr &B, int
   }
   return c;
 }
-__device__ __forceinline__ int chunk_mask(const DCsr &A, const DCsr &B, int i, int lane, int len, const RowChunk &c) {
-  if (len > 32) return row_table_mask(A, B, i, lane);
+__device__ __forceinline__ int chunk_mask(const DCsr &A, const DCsr &B, int i, int lane, int len, const RowChunk &c,
+                                          int cap = HASH_CAP) {
+  if (len > 32) return row_table_mask(A, B, i, lane, cap);
   int ub = c.be - c.bs;
   for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
   int t = 32;
-  while (t < HASH_CAP && t < 2 * ub) t <<= 1;
+  while (t < cap && t < 2 * ub) t <<= 1;
   return t - 1;
 }
 
@@ -637,24 +638,34 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, D
   if (lane == 0) {
     cnt[i] = count;
     if (count > HASH_MAX) atomicMax(overflow, 1);
+    // overflow[1] = the product's longest row (picks the fill kernel's table size); the plain
+    // read first keeps the atomics to the few rows that raise the maximum
+    if (count > *(volatile int *)(overflow + 1)) atomicMax(overflow + 1, count);
   }
 }
 
 constexpr int HASH_WARP_BYTES = HASH_CAP * 4 + HASH_CAP * 8 + HASH_MAX * 4 + HASH_MAX * 8;
+// the fill kernel with a quarter of the table (products whose longest row has <= HASH_MAX_S
+// columns -- the count kernel reports it): 2.5 KB of shared memory per warp instead of 10 KB,
+// so 64 instead of 20 resident warps per SM for this latency-bound kernel
+constexpr int HASH_CAP_S = 128, HASH_MAX_S = 80;
+constexpr int HASH_WARP_BYTES_S = HASH_CAP_S * 4 + HASH_CAP_S * 8 + HASH_MAX_S * 4 + HASH_MAX_S * 8;
 
+template <int CAP, int MAXD>
 __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DCsr B, DCsr C) {
   extern __shared__ __align__(16) unsigned char hsm[];
+  constexpr int WARP_BYTES = CAP * 4 + CAP * 8 + MAXD * 4 + MAXD * 8;
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int i = blockIdx.x * HASH_WARPS + warp;
   if (i >= A.n) return;
-  unsigned char *wb = hsm + (size_t)warp * HASH_WARP_BYTES;
+  unsigned char *wb = hsm + (size_t)warp * WARP_BYTES;
   double *vals = reinterpret_cast<double *>(wb);
-  double *cvals = reinterpret_cast<double *>(wb + HASH_CAP * 8);
-  int *keys = reinterpret_cast<int *>(wb + HASH_CAP * 8 + HASH_MAX * 8);
-  int *ckeys = keys + HASH_CAP;
+  double *cvals = reinterpret_cast<double *>(wb + CAP * 8);
+  int *keys = reinterpret_cast<int *>(wb + CAP * 8 + MAXD * 8);
+  int *ckeys = keys + CAP;
   const int r0 = A.rp[i], r1 = A.rp[i + 1];
   RowChunk ch = load_chunk(A, B, r0 + lane, r1, true);
-  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch);
+  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch, CAP);
   for (int s = lane; s <= mask; s += 32) keys[s] = -1;
   __syncwarp();
   for (int q0 = r0; q0 < r1; q0 += 32) {  // k ascending
@@ -785,6 +796,142 @@ __global__ void k_spgemm_tpr_fill(DCsr A, DCsr B, DCsr C) {
   }
 }
 
+// ---- warp-per-row SpGEMM with one lane per entry of the A row, for A P on the first coarse
+// levels (A rows of 15-30 entries, P rows of 1-6): the warp-hash kernels above walk one B row
+// at a time and so keep 2-3 lanes busy on these products, and the thread-per-row kernels search
+// their column list linearly (O(len^2) local-memory accesses for ~60 products per row).  Here
+// lane q takes A(i, k_q), inserts the columns of B(k_q, :) into the warp's shared-memory key
+// table and stages its products a * b (in the row's ascending (q, t) order, at the offset given
+// by a warp scan of the B row lengths); then each output column is owned by one lane, which
+// sums the staged products of its column in that order -- the same rounding sequence as the
+// other SpGEMM kernels (acc starts at +0.0; products rounded, then added, k ascending).
+constexpr int WK_WARPS = 8;
+constexpr int WK_CAP = 256;   // key slots per warp
+constexpr int WK_MAX = 192;   // distinct columns per row at most (else the product falls back)
+constexpr int WK_PROD = 256;  // staged products per row; longer rows re-read A and B per column
+
+__device__ __forceinline__ int wk_mask(int ub) {
+  int t = 32;
+  while (t < WK_CAP && t < 2 * ub) t <<= 1;
+  return t - 1;
+}
+
+// inserts the columns of the row's products; returns the number of distinct columns, or -1
+template <bool STAGE>
+__device__ __forceinline__ int wk_insert_row(const DCsr &A, const DCsr &B, int r0, int r1, int lane, int *keys,
+                                             int *pcol, double *pval, int &nprod) {
+  // upper bound on the distinct columns = number of products
+  int ub = 0;
+  for (int q = r0 + lane; q < r1; q += 32) {
+    int k = A.ci[q];
+    ub += B.rp[k + 1] - B.rp[k];
+  }
+  for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+  nprod = ub;
+  const int mask = wk_mask(ub);
+  for (int s = lane; s <= mask; s += 32) keys[s] = -1;
+  __syncwarp();
+  int count = 0, base = 0;
+  bool spill = false;
+  const bool stage = STAGE && ub <= WK_PROD;
+  for (int q0 = r0; q0 < r1; q0 += 32) {
+    int q = q0 + lane, bs = 0, be = 0;
+    double a = 0.0;
+    if (q < r1) {
+      int k = A.ci[q];
+      bs = B.rp[k];
+      be = B.rp[k + 1];
+      if (STAGE) a = A.v[q];
+    }
+    int off = 0;
+    if (STAGE) {  // exclusive scan of the B row lengths: this lane's first product slot
+      int len = be - bs, inc = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      off = base + inc - len;
+      base += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    for (int t = bs; t < be; t++) {
+      int col = B.ci[t];
+      bool ins;
+      if (hash_insert(keys, col, mask, ins) < 0) {
+        spill = true;
+        break;
+      }
+      count += ins;
+      if (stage) {
+        pcol[off + (t - bs)] = col;
+        pval[off + (t - bs)] = __dmul_rn(a, B.v[t]);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+  if (__any_sync(0xffffffffu, spill) || count > WK_MAX) return -1;
+  return count;
+}
+
+__global__ void __launch_bounds__(WK_WARPS * 32) k_spgemm_wk_count(DCsr A, DCsr B, int32_t *cnt, int *overflow) {
+  __shared__ int skeys[WK_WARPS][WK_CAP];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i = blockIdx.x * WK_WARPS + warp;
+  if (i >= A.n) return;
+  int nprod;
+  int count = wk_insert_row<false>(A, B, A.rp[i], A.rp[i + 1], lane, skeys[warp], nullptr, nullptr, nprod);
+  if (lane == 0) {
+    cnt[i] = count < 0 ? 0 : count;
+    if (count < 0) atomicMax(overflow, 1);
+  }
+}
+
+__global__ void __launch_bounds__(WK_WARPS * 32) k_spgemm_wk_fill(DCsr A, DCsr B, DCsr C) {
+  __shared__ int skeys[WK_WARPS][WK_CAP];
+  __shared__ int sckeys[WK_WARPS][WK_MAX];
+  __shared__ int spcol[WK_WARPS][WK_PROD];
+  __shared__ double spval[WK_WARPS][WK_PROD];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i = blockIdx.x * WK_WARPS + warp;
+  if (i >= A.n) return;
+  int *keys = skeys[warp], *ckeys = sckeys[warp], *pcol = spcol[warp];
+  double *pval = spval[warp];
+  const int r0 = A.rp[i], r1 = A.rp[i + 1];
+  int nprod;
+  int count = wk_insert_row<true>(A, B, r0, r1, lane, keys, pcol, pval, nprod);
+  if (!BF_CHK(count >= 0)) return;  // the count kernel admitted every row of this product
+  __syncwarp();
+  const int mask = wk_mask(nprod);
+  int n = 0;
+  for (int s0 = 0; s0 <= mask; s0 += 32) {
+    int key = keys[s0 + lane];
+    unsigned m = __ballot_sync(0xffffffffu, key >= 0);
+    if (key >= 0) ckeys[n + __popc(m & ((1u << lane) - 1))] = key;
+    n += __popc(m);
+  }
+  __syncwarp();
+  const int base = C.rp[i];
+  const bool staged = nprod <= WK_PROD;
+  for (int e = lane; e < n; e += 32) {
+    int key = ckeys[e], rank = 0;
+    for (int u = 0; u < n; u++) rank += ckeys[u] < key;
+    double acc = 0.0;
+    if (staged) {
+      for (int p = 0; p < nprod; p++)
+        if (pcol[p] == key) acc = __dadd_rn(acc, pval[p]);
+    } else {
+      for (int q = r0; q < r1; q++) {  // k ascending
+        int k = A.ci[q];
+        double a = A.v[q];
+        for (int t = B.rp[k]; t < B.rp[k + 1]; t++)
+          if (B.ci[t] == key) acc = __dadd_rn(acc, __dmul_rn(a, B.v[t]));
+      }
+    }
+    if (!BF_CHK(base + rank < C.rp[i + 1])) continue;
+    C.ci[base + rank] = key;
+    C.v[base + rank] = acc;
+  }
+}
+
 static void spgemm_esc(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
 static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C);
 
@@ -793,13 +940,15 @@ static void spgemm(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
     spgemm_esc(c, A, B, C);
     return;
   }
-  if (B.n > 0 && (double)B.nnz / B.n <= 6.0 && A.n > 0 && (double)A.nnz / A.n <= 30.0 && c->tune.spgemm != 1) {
+  if (B.n > 0 && (double)B.nnz / B.n <= c->tune.tpr_bmax && A.n > 0 && (double)A.nnz / A.n <= c->tune.tpr_amax && c->tune.spgemm != 1) {
     C.n = A.n;
     C.m = B.m;
     int32_t *cnt = dalloc_t<int32_t>(c, A.n);
     int *ovf = dalloc_t<int>(c, 1);
     BF_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), c->stream));
-    k_spgemm_tpr_count<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, cnt, ovf);
+    const bool wk = (double)A.nnz / A.n > c->tune.wk_amin;  // lane-per-entry warp kernels for the longer A rows
+    if (wk) k_spgemm_wk_count<<<div_up(A.n, WK_WARPS), WK_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
+    else k_spgemm_tpr_count<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, cnt, ovf);
     BF_LAUNCH(c);
     int h_ovf = 0;
     BF_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -811,7 +960,8 @@ static void spgemm(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
       dfree(c, cnt);
       C.ci = dalloc_t<int32_t>(c, C.nnz);
       C.v = dalloc_t<double>(c, C.nnz);
-      k_spgemm_tpr_fill<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, C);
+      if (wk) k_spgemm_wk_fill<<<div_up(A.n, WK_WARPS), WK_WARPS * 32, 0, c->stream>>>(A, B, C);
+      else k_spgemm_tpr_fill<<<div_up(A.n, 128), 128, 0, c->stream>>>(A, B, C);
       BF_LAUNCH(c);
       BF_CUDA(cudaGetLastError());
       return;
@@ -826,16 +976,17 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   C.n = A.n;
   C.m = B.m;
   int32_t *cnt = dalloc_t<int32_t>(c, A.n);
-  int *ovf = dalloc_t<int>(c, 1);
-  BF_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), c->stream));
+  int *ovf = dalloc_t<int>(c, 2);
+  BF_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), c->stream));
   int blocks = div_up(A.n, HASH_WARPS);
   k_spgemm_hash_count<<<blocks, HASH_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
-  int h_ovf = 0;
-  BF_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  int h_ovf2[2] = {0, 0};
+  BF_CUDA(cudaMemcpyAsync(h_ovf2, ovf, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   dfree(c, ovf);
+  const int h_ovf = h_ovf2[0], h_max = h_ovf2[1];
   if (h_ovf) {
     dfree(c, cnt);
     spgemm_esc(c, A, B, C);
@@ -846,8 +997,14 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   dfree(c, cnt);
   C.ci = dalloc_t<int32_t>(c, C.nnz);
   C.v = dalloc_t<double>(c, C.nnz);
-  ensure_smem_attr((const void *)k_spgemm_hash_fill, HASH_WARPS * HASH_WARP_BYTES);
-  k_spgemm_hash_fill<<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES, c->stream>>>(A, B, C);
+  if (h_max <= HASH_MAX_S && c->tune.hash_small) {
+    k_spgemm_hash_fill<HASH_CAP_S, HASH_MAX_S>
+        <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES_S, c->stream>>>(A, B, C);
+  } else {
+    ensure_smem_attr((const void *)k_spgemm_hash_fill<HASH_CAP, HASH_MAX>, HASH_WARPS * HASH_WARP_BYTES);
+    k_spgemm_hash_fill<HASH_CAP, HASH_MAX>
+        <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES, c->stream>>>(A, B, C);
+  }
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());
 }
