@@ -616,23 +616,33 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, D
   for (int q0 = r0; q0 < r1 && !full; q0 += 32) {
     if (q0 != r0) ch = load_chunk(A, B, q0 + lane, r1, false);
     int nq = min(32, r1 - q0);
-    for (int u = 0; u < nq && !full; u++) {
-      int bs = __shfl_sync(0xffffffffu, ch.bs, u), be = __shfl_sync(0xffffffffu, ch.be, u);
-      bool spill = false;
-      for (int t = bs + lane; t < be; t += 32) {
-        bool ins;
-        if (hash_insert(keys, B.ci[t], mask, ins) < 0) {
-          spill = true;
-          break;
-        }
-        count += ins;
+    // as in the fill kernel, the first 32 columns of the next B row are fetched while this one is hashed
+    int bs = __shfl_sync(0xffffffffu, ch.bs, 0), be = __shfl_sync(0xffffffffu, ch.be, 0);
+    int nc = bs + lane < be ? B.ci[bs + lane] : -1;
+    bool spill = false;
+    for (int u = 0; u < nq; u++) {
+      int cbs = bs, cbe = be, cc = nc;
+      if (u + 1 < nq) {
+        bs = __shfl_sync(0xffffffffu, ch.bs, u + 1);
+        be = __shfl_sync(0xffffffffu, ch.be, u + 1);
+        nc = bs + lane < be ? B.ci[bs + lane] : -1;
       }
-      // stop early once the row cannot fit (the product then falls back to the ESC path)
-      int tot = count;
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      full = tot > HASH_MAX || __any_sync(0xffffffffu, spill);
-      if (full && lane == 0) count = HASH_MAX + 1;  // forces the overflow flag below
+      bool ins;
+      if (cc >= 0 && !spill) {  // a lane that found the table full stops inserting
+        if (hash_insert(keys, cc, mask, ins) < 0) spill = true;
+        else count += ins;
+      }
+      for (int t = cbs + 32 + lane; t < cbe && !spill; t += 32) {
+        if (hash_insert(keys, B.ci[t], mask, ins) < 0) spill = true;
+        else count += ins;
+      }
     }
+    // once per 32 entries of the A row: stop once the row cannot fit (a full table makes
+    // hash_insert return -1; the product then falls back to the ESC path)
+    int tot = count;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    full = tot > HASH_MAX || __any_sync(0xffffffffu, spill);
+    if (full && lane == 0) count = HASH_MAX + 1;  // forces the overflow flag below
   }
   for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
   if (lane == 0) {
@@ -650,6 +660,8 @@ constexpr int HASH_WARP_BYTES = HASH_CAP * 4 + HASH_CAP * 8 + HASH_MAX * 4 + HAS
 // so 64 instead of 20 resident warps per SM for this latency-bound kernel
 constexpr int HASH_CAP_S = 128, HASH_MAX_S = 80;
 constexpr int HASH_WARP_BYTES_S = HASH_CAP_S * 4 + HASH_CAP_S * 8 + HASH_MAX_S * 4 + HASH_MAX_S * 8;
+constexpr int HASH_CAP_M = 256, HASH_MAX_M = 160;  // ... and with half of it: 5 KB, 40 warps per SM
+constexpr int HASH_WARP_BYTES_M = HASH_CAP_M * 4 + HASH_CAP_M * 8 + HASH_MAX_M * 4 + HASH_MAX_M * 8;
 
 template <int CAP, int MAXD>
 __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_fill(DCsr A, DCsr B, DCsr C) {
@@ -987,6 +999,7 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   sync(c);
   dfree(c, ovf);
   const int h_ovf = h_ovf2[0], h_max = h_ovf2[1];
+  if (c->tune.verbose) fprintf(stderr, "[bf] spgemm_hash: %d x %d rows, longest row %d%s\n", A.n, B.n, h_max, h_ovf ? " (overflow)" : "");
   if (h_ovf) {
     dfree(c, cnt);
     spgemm_esc(c, A, B, C);
@@ -1000,6 +1013,9 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   if (h_max <= HASH_MAX_S && c->tune.hash_small) {
     k_spgemm_hash_fill<HASH_CAP_S, HASH_MAX_S>
         <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES_S, c->stream>>>(A, B, C);
+  } else if (h_max <= HASH_MAX_M && c->tune.hash_small) {
+    k_spgemm_hash_fill<HASH_CAP_M, HASH_MAX_M>
+        <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES_M, c->stream>>>(A, B, C);
   } else {
     ensure_smem_attr((const void *)k_spgemm_hash_fill<HASH_CAP, HASH_MAX>, HASH_WARPS * HASH_WARP_BYTES);
     k_spgemm_hash_fill<HASH_CAP, HASH_MAX>
