@@ -103,52 +103,30 @@ __device__ __forceinline__ bool greater_key(const uint64_t *key, int a, int b) {
   return ka > kb || (ka == kb && a > b);
 }
 
-// every strong edge (i, j in S_i) with both ends undecided marks its smaller end "not max";
-// this covers U cap (S_i cup S_i^T) for every i
-__global__ void k_pmis_edges(DCsr A, const uint8_t *__restrict__ strong, const uint64_t *__restrict__ key,
-                             const int8_t *__restrict__ state, uint8_t *notmax) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= A.n || state[i] >= 0) return;
-  for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
-    int j = A.ci[q];
-    if (!strong[q] || state[j] >= 0) continue;
-    if (greater_key(key, i, j)) notmax[j] = 1;
-    else notmax[i] = 1;
-  }
-}
-
-__global__ void k_pmis_cnew(int n, const int8_t *__restrict__ state, const uint8_t *__restrict__ notmax,
-                            uint8_t *cnew) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  cnew[i] = (uint8_t)(state[i] < 0 && !notmax[i]);
-}
-
-__global__ void k_pmis_update(DCsr A, const uint8_t *__restrict__ strong, const uint8_t *__restrict__ cnew,
-                              int8_t *state, int *nU) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= A.n || state[i] >= 0) return;
-  if (cnew[i]) { state[i] = 1; return; }
-  for (int q = A.rp[i]; q < A.rp[i + 1]; q++)
-    if (strong[q] && cnew[A.ci[q]]) { state[i] = 0; return; }
-  atomicAdd(nU, 1);
-}
-
-// All PMIS rounds in one cooperative kernel (grid-wide barriers between the synchronous
-// phases of a round) -- a round costs ~4 grid barriers instead of 3 launches + a host sync;
-// chains of strictly ordered keys can need hundreds of rounds (measured: 500 on a S~ level).
+// All PMIS rounds in one cooperative kernel, two grid-wide barriers per round:
+//   phase 1: every strong edge with both ends undecided marks its smaller end in notmax[p];
+//   phase 2: an undecided i with no mark becomes C; otherwise it becomes F if some j in S_i is a
+//            new C point, else it stays undecided.
+// "j is a new C point of this round" is evaluated from state[j] and notmax[p][j] without a
+// separate flag array: an undecided i never has an OLDER C point in S_i (it would have become
+// F in that round), so state[j] == 1 can only have been written in this phase, and for a j
+// still read as undecided the mark decides -- the same value whichever way the race between
+// i's read and j's write goes (state[j] is read once).  The marks alternate between two
+// buffers, the idle one is cleared in phase 2.  Chains of strictly ordered keys can need
+// hundreds of rounds (measured: 500 on a S~ level), so the barriers are what a round costs.
 __global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const uint64_t *__restrict__ key,
-                            int8_t *state, uint8_t *notmax, uint8_t *cnew, int *nU, int max_rounds, int *rounds) {
+                            int8_t *state, uint8_t *notmax0, uint8_t *notmax1, int *nU, int max_rounds, int *rounds) {
   cg::grid_group grid = cg::this_grid();
   const int n = A.n;
   const int stride = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = t0; i < n; i += stride) notmax0[i] = 0, notmax1[i] = 0;
+  grid.sync();
   int round = 0;
   for (; round < max_rounds; round++) {
     int *cnt = nU + (round & 1);
-    for (int i = t0; i < n; i += stride) notmax[i] = 0;
+    uint8_t *notmax = (round & 1) ? notmax1 : notmax0, *idle = (round & 1) ? notmax0 : notmax1;
     if (t0 == 0) *cnt = 0;
-    grid.sync();
     for (int i = t0; i < n; i += stride) {
       if (state[i] >= 0) continue;
       for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
@@ -159,15 +137,19 @@ __global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const ui
       }
     }
     grid.sync();
-    for (int i = t0; i < n; i += stride) cnew[i] = (uint8_t)(state[i] < 0 && !notmax[i]);
-    grid.sync();
     int local = 0;
     for (int i = t0; i < n; i += stride) {
+      idle[i] = 0;
       if (state[i] >= 0) continue;
-      if (cnew[i]) { state[i] = 1; continue; }
+      if (!notmax[i]) { state[i] = 1; continue; }
       bool f = false;
-      for (int q = A.rp[i]; q < A.rp[i + 1] && !f; q++) f = strong[q] && cnew[A.ci[q]];
-      if (f) state[i] = 0;
+      for (int q = A.rp[i]; q < A.rp[i + 1] && !f; q++) {
+        if (!strong[q]) continue;
+        int j = A.ci[q];
+        int8_t sj = *(volatile const int8_t *)(state + j);
+        f = sj == 1 || (sj < 0 && !notmax[j]);
+      }
+      if (f) *(volatile int8_t *)(state + i) = 0;
       else local++;
     }
     if (local) atomicAdd(cnt, local);
@@ -338,62 +320,93 @@ __global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uin
       fa[nf + __popc(mf & below)] = a;
     }
     // dg = dg + a_in over the weak entries, ascending (lane 0 walks the chunk in order)
-    for (int l = 0; l < 32; l++) {
-      double al = __shfl_sync(0xffffffffu, a, l);
-      if ((mw >> l) & 1u) dg = __dadd_rn(dg, al);
-    }
+    for (unsigned w = mw; w; w &= w - 1)  // set bits in ascending lane order
+      dg = __dadd_rn(dg, __shfl_sync(0xffffffffu, a, __ffs(w) - 1));
     nc += __popc(mc);
     nf += __popc(mf);
   }
   __syncwarp();
   // pass 2: strong F neighbours k ascending
+  // row k of the NEXT strong F neighbour (bounds, sign of a_kk, first 32 entries) is fetched
+  // while the current one is processed: the per-k chain fk -> row_ptr -> entries is two
+  // dependent global round trips
+  int nk0 = 0, nk1 = 0, nm = -1;
+  double na = 0.0, ndk = 1.0;
+  if (nf > 0) {
+    int k = fk[0];
+    nk0 = A.rp[k];
+    nk1 = A.rp[k + 1];
+    ndk = diag[k];
+    if (nk0 + lane < nk1) {
+      nm = A.ci[nk0 + lane];
+      na = A.v[nk0 + lane];
+    }
+  }
   for (int f = 0; f < nf; f++) {
-    const int k = fk[f];
     const double aik = fa[f];
-    const double sk = diag[k] < 0.0 ? -1.0 : 1.0;
-    const int k0 = A.rp[k], k1 = A.rp[k + 1];
+    const double sk = ndk < 0.0 ? -1.0 : 1.0;
+    const int k0 = nk0, k1 = nk1, cm = nm;
+    const double ca = na;
+    if (f + 1 < nf) {
+      int k = fk[f + 1];
+      nk0 = A.rp[k];
+      nk1 = A.rp[k + 1];
+      ndk = diag[k];
+      nm = -1;
+      if (nk0 + lane < nk1) {
+        nm = A.ci[nk0 + lane];
+        na = A.v[nk0 + lane];
+      }
+    }
     double Dk = 0.0;
+    int pos1 = -1;        // single-chunk rows (<= 32 entries): this lane's entry of row k, found once
+    double abar1 = 0.0;
     for (int q0 = k0; q0 < k1; q0 += 32) {  // D_k = sum over row k cap C_i of abar, ascending
       int q = q0 + lane;
       double abar = 0.0;
       bool mem = false;
+      int lo = 0;
       if (q < k1) {
-        int m = A.ci[q];
-        int lo = 0, hi = nc;  // binary search of m in C_i
+        int m = q0 == k0 ? cm : A.ci[q];
+        int hi = nc;  // binary search of m in C_i
         while (lo < hi) {
           int mid = (lo + hi) >> 1;
           if (ccol[mid] < m) lo = mid + 1;
           else hi = mid;
         }
         mem = lo < nc && ccol[lo] == m;
-        double a = A.v[q];
+        double a = q0 == k0 ? ca : A.v[q];
         abar = (sk * a < 0.0) ? a : 0.0;
       }
+      pos1 = mem ? lo : -1;
+      abar1 = abar;
       unsigned mm = __ballot_sync(0xffffffffu, mem);
-      for (int l = 0; l < 32; l++) {
-        double al = __shfl_sync(0xffffffffu, abar, l);
-        if ((mm >> l) & 1u) Dk = __dadd_rn(Dk, al);
-      }
+      for (unsigned w = mm; w; w &= w - 1)  // members of C_i in ascending lane (= column) order
+        Dk = __dadd_rn(Dk, __shfl_sync(0xffffffffu, abar, __ffs(w) - 1));
     }
     if (Dk == 0.0) {
       dg = __dadd_rn(dg, aik);  // lumped into the diagonal
       continue;
     }
     const double cc = __ddiv_rn(aik, Dk);
-    for (int q0 = k0; q0 < k1; q0 += 32) {  // num_m += cc * abar_km (each m owned by one lane)
-      int q = q0 + lane;
-      if (q < k1) {
-        int m = A.ci[q];
-        int lo = 0, hi = nc;
-        while (lo < hi) {
-          int mid = (lo + hi) >> 1;
-          if (ccol[mid] < m) lo = mid + 1;
-          else hi = mid;
-        }
-        if (lo < nc && ccol[lo] == m) {
-          double a = A.v[q];
-          double abar = (sk * a < 0.0) ? a : 0.0;
-          num[lo] = __dadd_rn(num[lo], __dmul_rn(cc, abar));
+    if (k1 - k0 <= 32) {  // num_m += cc * abar_km (each m owned by one lane)
+      if (pos1 >= 0) num[pos1] = __dadd_rn(num[pos1], __dmul_rn(cc, abar1));
+    } else {
+      for (int q0 = k0; q0 < k1; q0 += 32) {
+        int q = q0 + lane;
+        if (q < k1) {
+          int m = A.ci[q];
+          int lo = 0, hi = nc;
+          while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (ccol[mid] < m) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo < nc && ccol[lo] == m) {
+            double a = A.v[q];
+            double abar = (sk * a < 0.0) ? a : 0.0;
+            num[lo] = __dadd_rn(num[lo], __dmul_rn(cc, abar));
+          }
         }
       }
     }
@@ -1516,13 +1529,13 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
     k_pmis_init<<<div_up(n, 256), 256, 0, c->stream>>>(n, lam, o.seed, l, key, state);
     BF_LAUNCH(c);
     uint8_t *notmax = dalloc_t<uint8_t>(c, n);
-    uint8_t *cnew = dalloc_t<uint8_t>(c, n);
+    uint8_t *notmax1 = dalloc_t<uint8_t>(c, n);
     {
       const int coop_blocks = std::max(1, occupancy(c, (const void *)k_pmis_coop, 256, 0)) * c->num_sms;
       int grid = std::max(1, std::min(coop_blocks, div_up(n, 256)));
       int max_rounds = n + 1;  // each round decides at least the undecided point of largest key
       int *rounds_d = nU_d + 2;
-      void *args[] = {(void *)&A, (void *)&strong, (void *)&key, (void *)&state, (void *)&notmax, (void *)&cnew,
+      void *args[] = {(void *)&A, (void *)&strong, (void *)&key, (void *)&state, (void *)&notmax, (void *)&notmax1,
                       (void *)&nU_d, (void *)&max_rounds, (void *)&rounds_d};
       BF_CUDA(cudaLaunchCooperativeKernel((void *)k_pmis_coop, grid, 256, args, 0, c->stream));
       BF_LAUNCH(c);
@@ -1532,7 +1545,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
       if (hr[2] > max_rounds) throw Error(BF_ERR_LIMIT, "PMIS did not terminate");
     }
     dfree(c, notmax);
-    dfree(c, cnew);
+    dfree(c, notmax1);
     dfree(c, key);
     dfree(c, lam);
     // coarse numbering
@@ -1566,7 +1579,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
       uint8_t *long_rows = dalloc_t<uint8_t>(c, n);
       int *any_long = dalloc_t<int>(c, 1);
       int h_long = 1;
-      if ((double)A.nnz / n > 22.0) {  // long (Galerkin) rows: warp per row; short rows: thread per row
+      if ((double)A.nnz / n > c->tune.interp_warp_min) {  // long (Galerkin) rows: warp per row; short rows: thread per row
         BF_CUDA(cudaMemsetAsync(long_rows, 0, n, c->stream));
         BF_CUDA(cudaMemsetAsync(any_long, 0, sizeof(int), c->stream));
         k_interp_warp<<<div_up(n, IW_WARPS), IW_WARPS * 32, 0, c->stream>>>(A, strong, state, cmap, diag,
