@@ -333,6 +333,8 @@ Tuning tuning_from_env() {
   t.tpr_amax = env_num("BF_TPR_AMAX", t.tpr_amax);
   t.wk_amin = env_num("BF_WK_AMIN", t.wk_amin);
   t.hash_small = !env_flag("BF_NO_HASH_SMALL");
+  t.hash_large = !env_flag("BF_NO_HASH_LARGE");
+  t.hash_large_min = env_num("BF_HASH_LARGE_MIN", t.hash_large_min);
   t.interp_warp_min = env_num("BF_INTERP_WARP_MIN", t.interp_warp_min);
   t.tpr_bmax = env_num("BF_TPR_BMAX", t.tpr_bmax);
   t.ilu_ctas = std::max(1, (int)env_num("BF_ILU_CTAS", t.ilu_ctas));

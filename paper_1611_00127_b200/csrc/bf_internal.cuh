@@ -117,7 +117,9 @@ struct Tuning {
   double win_ratio = 0.35;   // the form is dropped if the windows hold more than this many entries per nonzero
   int tma_g_p = 0, tma_g_r = 0;  // forced lanes per row for P / R (0: heuristic)
   int spgemm = 0;           // 0 auto (thread-per-row, hash, ESC fallback), 1 hash, 2 ESC
-  double interp_warp_min = 22.0;  // interpolation: warp per row above this mean row length of A, thread per row below
+  double interp_warp_min = 16.0;  // interpolation: warp per row above this mean row length of A, thread per row below
+  bool hash_large = true;   // ... and with the 1024-slot table for rows of up to 640 columns before falling back to ESC
+  double hash_large_min = 500.0;  // mean products per row from which the count starts with the large table
   bool hash_small = true;   // warp-hash fill kernel with the small table when the product's longest row allows
   double wk_amin = 14.0;    // ... and the lane-per-entry warp kernels (k_spgemm_wk_*) above this mean row length of A
   double tpr_bmax = 6.0;    // thread-per-row / lane-per-entry SpGEMM only for B with at most this mean row length

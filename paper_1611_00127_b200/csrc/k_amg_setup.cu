@@ -613,15 +613,16 @@ __device__ __forceinline__ int chunk_mask(const DCsr &A, const DCsr &B, int i, i
   return t - 1;
 }
 
+template <int CAP, int MAXD>
 __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, DCsr B, int32_t *cnt, int *overflow) {
-  __shared__ int skeys[HASH_WARPS][HASH_CAP];
+  __shared__ int skeys[HASH_WARPS][CAP];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int i = blockIdx.x * HASH_WARPS + warp;
   if (i >= A.n) return;
   int *keys = skeys[warp];
   const int r0 = A.rp[i], r1 = A.rp[i + 1];
   RowChunk ch = load_chunk(A, B, r0 + lane, r1, false);
-  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch);
+  int mask = chunk_mask(A, B, i, lane, r1 - r0, ch, CAP);
   for (int s = lane; s <= mask; s += 32) keys[s] = -1;
   __syncwarp();
   int count = 0;
@@ -654,13 +655,13 @@ __global__ void __launch_bounds__(HASH_WARPS * 32) k_spgemm_hash_count(DCsr A, D
     // hash_insert return -1; the product then falls back to the ESC path)
     int tot = count;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    full = tot > HASH_MAX || __any_sync(0xffffffffu, spill);
-    if (full && lane == 0) count = HASH_MAX + 1;  // forces the overflow flag below
+    full = tot > MAXD || __any_sync(0xffffffffu, spill);
+    if (full && lane == 0) count = MAXD + 1;  // forces the overflow flag below
   }
   for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
   if (lane == 0) {
     cnt[i] = count;
-    if (count > HASH_MAX) atomicMax(overflow, 1);
+    if (count > MAXD) atomicMax(overflow, 1);
     // overflow[1] = the product's longest row (picks the fill kernel's table size); the plain
     // read first keeps the atomics to the few rows that raise the maximum
     if (count > *(volatile int *)(overflow + 1)) atomicMax(overflow + 1, count);
@@ -673,6 +674,8 @@ constexpr int HASH_WARP_BYTES = HASH_CAP * 4 + HASH_CAP * 8 + HASH_MAX * 4 + HAS
 // so 64 instead of 20 resident warps per SM for this latency-bound kernel
 constexpr int HASH_CAP_S = 128, HASH_MAX_S = 80;
 constexpr int HASH_WARP_BYTES_S = HASH_CAP_S * 4 + HASH_CAP_S * 8 + HASH_MAX_S * 4 + HASH_MAX_S * 8;
+constexpr int HASH_CAP_L = 1024, HASH_MAX_L = 640;  // long rows (the fused restrictions Rf of levels >= 2): 20 KB per warp
+constexpr int HASH_WARP_BYTES_L = HASH_CAP_L * 4 + HASH_CAP_L * 8 + HASH_MAX_L * 4 + HASH_MAX_L * 8;
 constexpr int HASH_CAP_M = 256, HASH_MAX_M = 160;  // ... and with half of it: 5 KB, 40 warps per SM
 constexpr int HASH_WARP_BYTES_M = HASH_CAP_M * 4 + HASH_CAP_M * 8 + HASH_MAX_M * 4 + HASH_MAX_M * 8;
 
@@ -1002,17 +1005,32 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   C.m = B.m;
   int32_t *cnt = dalloc_t<int32_t>(c, A.n);
   int *ovf = dalloc_t<int>(c, 2);
-  BF_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), c->stream));
   int blocks = div_up(A.n, HASH_WARPS);
-  k_spgemm_hash_count<<<blocks, HASH_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
-  BF_LAUNCH(c);
-  BF_CUDA(cudaGetLastError());
-  int h_ovf2[2] = {0, 0};
-  BF_CUDA(cudaMemcpyAsync(h_ovf2, ovf, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
+  // products with many products per row (mean over the rows) start with the 1024-slot table
+  const double mean_products = A.n && B.n ? ((double)A.nnz / A.n) * ((double)B.nnz / B.n) : 0.0;
+  bool large = c->tune.hash_large && mean_products > c->tune.hash_large_min;
+  int h_ovf = 0, h_max = 0;
+  for (;;) {
+    BF_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), c->stream));
+    if (large) k_spgemm_hash_count<HASH_CAP_L, HASH_MAX_L><<<blocks, HASH_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
+    else k_spgemm_hash_count<HASH_CAP, HASH_MAX><<<blocks, HASH_WARPS * 32, 0, c->stream>>>(A, B, cnt, ovf);
+    BF_LAUNCH(c);
+    BF_CUDA(cudaGetLastError());
+    int h_ovf2[2] = {0, 0};
+    BF_CUDA(cudaMemcpyAsync(h_ovf2, ovf, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    h_ovf = h_ovf2[0];
+    h_max = h_ovf2[1];
+    if (c->tune.verbose)
+      fprintf(stderr, "[bf] spgemm_hash: %d x %d rows, longest row %d%s%s\n", A.n, B.n, h_max, large ? " (1024-slot table)" : "",
+              h_ovf ? " (overflow)" : "");
+    if (h_ovf && !large && c->tune.hash_large) {
+      large = true;  // second attempt with the large table before the expand-sort-compress path
+      continue;
+    }
+    break;
+  }
   dfree(c, ovf);
-  const int h_ovf = h_ovf2[0], h_max = h_ovf2[1];
-  if (c->tune.verbose) fprintf(stderr, "[bf] spgemm_hash: %d x %d rows, longest row %d%s\n", A.n, B.n, h_max, h_ovf ? " (overflow)" : "");
   if (h_ovf) {
     dfree(c, cnt);
     spgemm_esc(c, A, B, C);
@@ -1029,10 +1047,14 @@ static void spgemm_hash(bf_ctx *c, const DCsr &A, const DCsr &B, DCsr &C) {
   } else if (h_max <= HASH_MAX_M && c->tune.hash_small) {
     k_spgemm_hash_fill<HASH_CAP_M, HASH_MAX_M>
         <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES_M, c->stream>>>(A, B, C);
-  } else {
+  } else if (h_max <= HASH_MAX) {
     ensure_smem_attr((const void *)k_spgemm_hash_fill<HASH_CAP, HASH_MAX>, HASH_WARPS * HASH_WARP_BYTES);
     k_spgemm_hash_fill<HASH_CAP, HASH_MAX>
         <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES, c->stream>>>(A, B, C);
+  } else {
+    ensure_smem_attr((const void *)k_spgemm_hash_fill<HASH_CAP_L, HASH_MAX_L>, HASH_WARPS * HASH_WARP_BYTES_L);
+    k_spgemm_hash_fill<HASH_CAP_L, HASH_MAX_L>
+        <<<blocks, HASH_WARPS * 32, HASH_WARPS * HASH_WARP_BYTES_L, c->stream>>>(A, B, C);
   }
   BF_LAUNCH(c);
   BF_CUDA(cudaGetLastError());

@@ -388,15 +388,19 @@ def test_solve_path_variants(variant, config, dims, monkeypatch):
     g.close()
 
 
-@pytest.mark.parametrize("force_wjds", [False, True])
-def test_long_rows_hash_overflow_regression(force_wjds, monkeypatch):
-    """(force_wjds: the windowed jagged-diagonal form is requested for every CSR level, whatever its
+@pytest.mark.parametrize("force_wjds,esc", [(False, False), (True, False), (False, True)], ids=["default", "wjds", "no-large-table"])
+def test_long_rows_hash_overflow_regression(force_wjds, esc, monkeypatch):
+    """(esc: the 1024-slot table of the warp-hash SpGEMM is switched off, so the count is not
+    repeated with it before the expand-sort-compress fallback.
+    force_wjds: the windowed jagged-diagonal form is requested for every CSR level, whatever its
     size or reuse; the levels whose hub row exceeds the form's 255-entry row limit must fall back to
     the CSR kernels, the others use it.)  A hub cell coupled to 700 others through A_ss only makes A_ss rows (and its Galerkin
     products) longer than the 512-slot shared-memory hash table of the SpGEMM (the C5 setup hang
     of round 1): setup must fall back to the expand-sort-compress product and stay bit-exact
     with the oracle.  (S~ keeps short rows: its row pattern is bounded at 256 entries,
     BF_ERR_LIMIT beyond.)"""
+    if esc:
+        monkeypatch.setenv("BF_NO_HASH_LARGE", "1")
     if force_wjds:
         for k, v in {"BF_WIN_NMIN": "0", "BF_WIN_RATIO": "100", "BF_NO_DTAIL": "1", "BF_NO_TAIL": "1"}.items():
             monkeypatch.setenv(k, v)
