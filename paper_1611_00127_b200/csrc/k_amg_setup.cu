@@ -113,7 +113,8 @@ __device__ __forceinline__ bool greater_key(const uint64_t *key, int a, int b) {
 // still read as undecided the mark decides -- the same value whichever way the race between
 // i's read and j's write goes (state[j] is read once).  The marks alternate between two
 // buffers, the idle one is cleared in phase 2.  Chains of strictly ordered keys can need
-// hundreds of rounds (measured: 500 on a S~ level), so the barriers are what a round costs.
+// hundreds of rounds (measured: 500 on a S~ level).
+constexpr int PM_CH = 4;
 __global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const uint64_t *__restrict__ key,
                             int8_t *state, uint8_t *notmax0, uint8_t *notmax1, int *nU, int max_rounds, int *rounds) {
   cg::grid_group grid = cg::this_grid();
@@ -127,14 +128,36 @@ __global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const ui
     int *cnt = nU + (round & 1);
     uint8_t *notmax = (round & 1) ? notmax1 : notmax0, *idle = (round & 1) ? notmax0 : notmax1;
     if (t0 == 0) *cnt = 0;
+    // Both phases walk a row in chunks of PM_CH entries with the loads of a chunk issued
+    // together (columns and strength flags, then the neighbours' states, then their keys /
+    // marks): a grid-stride thread is bound by its chain of dependent gathers otherwise.
     for (int i = t0; i < n; i += stride) {
       if (state[i] >= 0) continue;
-      for (int q = A.rp[i]; q < A.rp[i + 1]; q++) {
-        int j = A.ci[q];
-        if (!strong[q] || state[j] >= 0) continue;
-        if (greater_key(key, i, j)) notmax[j] = 1;
-        else notmax[i] = 1;
+      const int r0 = A.rp[i], r1 = A.rp[i + 1];
+      const uint64_t ki = key[i];
+      bool mark_i = false;
+      for (int q0 = r0; q0 < r1; q0 += PM_CH) {
+        int j[PM_CH];
+        bool und[PM_CH];
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) {
+          int q = q0 + u;
+          j[u] = q < r1 ? A.ci[q] : -1;
+          und[u] = q < r1 && strong[q];
+        }
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) und[u] = und[u] && state[j[u]] < 0;
+        uint64_t kj[PM_CH];
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) kj[u] = und[u] ? key[j[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) {
+          if (!und[u]) continue;
+          if (ki > kj[u] || (ki == kj[u] && i > j[u])) notmax[j[u]] = 1;
+          else mark_i = true;
+        }
       }
+      if (mark_i) notmax[i] = 1;
     }
     grid.sync();
     int local = 0;
@@ -143,11 +166,25 @@ __global__ void k_pmis_coop(DCsr A, const uint8_t *__restrict__ strong, const ui
       if (state[i] >= 0) continue;
       if (!notmax[i]) { state[i] = 1; continue; }
       bool f = false;
-      for (int q = A.rp[i]; q < A.rp[i + 1] && !f; q++) {
-        if (!strong[q]) continue;
-        int j = A.ci[q];
-        int8_t sj = *(volatile const int8_t *)(state + j);
-        f = sj == 1 || (sj < 0 && !notmax[j]);
+      const int r0 = A.rp[i], r1 = A.rp[i + 1];
+      for (int q0 = r0; q0 < r1 && !f; q0 += PM_CH) {
+        int j[PM_CH];
+        bool st[PM_CH];
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) {
+          int q = q0 + u;
+          j[u] = q < r1 ? A.ci[q] : -1;
+          st[u] = q < r1 && strong[q];
+        }
+        int8_t sj[PM_CH];
+        uint8_t nm[PM_CH];
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) {
+          sj[u] = st[u] ? *(volatile const int8_t *)(state + j[u]) : (int8_t)0;
+          nm[u] = st[u] ? notmax[j[u]] : (uint8_t)1;
+        }
+#pragma unroll
+        for (int u = 0; u < PM_CH; u++) f = f || (st[u] && (sj[u] == 1 || (sj[u] < 0 && !nm[u])));
       }
       if (f) *(volatile int8_t *)(state + i) = 0;
       else local++;
@@ -1565,6 +1602,7 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
       BF_CUDA(cudaMemcpyAsync(hr, nU_d, sizeof(hr), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
       if (hr[2] > max_rounds) throw Error(BF_ERR_LIMIT, "PMIS did not terminate");
+      if (c->tune.verbose) fprintf(stderr, "[bf_setup]   PMIS n=%d: %d rounds, grid %d x 256\n", n, hr[2], grid);
     }
     dfree(c, notmax);
     dfree(c, notmax1);
