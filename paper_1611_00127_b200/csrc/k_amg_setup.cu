@@ -586,8 +586,12 @@ static int bits_for(int64_t x) {
 // apply acc[J] = acc[J] + A(i,k) * B(k,J) (separately rounded); a __syncwarp between
 // consecutive k keeps every entry's sum in ascending-k order -- the same sequence of
 // roundings as the oracle and as the expand-sort-compress path.  Rows are emitted sorted
-// (rank of each key among the row's keys).  If any row holds more than HASH_MAX distinct
-// columns the product falls back to expand-sort-compress.
+// (rank of each key among the row's keys).  The count kernel reports the product's longest
+// row; the fill kernel is instantiated for 128 / 256 / 512 / 1024 slots (80 / 160 / 320 / 640
+// columns per row at most) and the smallest table that holds the longest row is used -- the
+// kernel is latency bound and its residency follows the table size.  If a row holds more than
+// HASH_MAX distinct columns the count is repeated with the 1024-slot table, and beyond
+// HASH_MAX_L columns the product falls back to expand-sort-compress.
 constexpr int HASH_WARPS = 4;
 constexpr int HASH_CAP = 512;        // max slots per warp (power of two)
 constexpr int HASH_MAX = 320;        // max distinct columns per row (load factor 0.625)
@@ -1451,6 +1455,56 @@ static __global__ void __launch_bounds__(256) k_perm_fill_warp(int n, const int3
   }
 }
 
+// thread per row for the interpolation-like matrices (mean row length <= 4; a warp per row leaves
+// 30 lanes idle there): rows of up to 8 entries are ranked in registers, longer ones are
+// insertion-sorted in place like k_perm_fill
+static __global__ void __launch_bounds__(256) k_perm_fill_short(int n, const int32_t *__restrict__ rp,
+                                                                const int32_t *__restrict__ ci,
+                                                                const double *__restrict__ v,
+                                                                const int32_t *__restrict__ rperm,
+                                                                const int32_t *__restrict__ cinv,
+                                                                const int32_t *__restrict__ brp, int32_t *bci,
+                                                                double *bv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = rperm ? rperm[i] : i;
+  const int q0 = rp[r], len = rp[r + 1] - q0, o = brp[i];
+  if (len <= 8) {
+    int col[8];
+    double val[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++)
+      if (e < len) {
+        int cc = ci[q0 + e];
+        col[e] = cinv ? cinv[cc] : cc;
+        val[e] = v[q0 + e];
+      }
+#pragma unroll
+    for (int e = 0; e < 8; e++)
+      if (e < len) {
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) rank += (k < len && col[k] < col[e]);
+        if (!BF_CHK(rank < len)) continue;
+        bci[o + rank] = col[e];
+        bv[o + rank] = val[e];
+      }
+    return;
+  }
+  for (int e = 0; e < len; e++) {  // insertion sort by the new column index
+    int col = cinv ? cinv[ci[q0 + e]] : ci[q0 + e];
+    double val = v[q0 + e];
+    int k = e;
+    while (k > 0 && bci[o + k - 1] > col) {
+      bci[o + k] = bci[o + k - 1];
+      bv[o + k] = bv[o + k - 1];
+      k--;
+    }
+    bci[o + k] = col;
+    bv[o + k] = val;
+  }
+}
+
 static void permute_csr(bf_ctx *c, const DCsr &A, const int32_t *rperm, const int32_t *cinv, DCsr &B) {
   B = DCsr();
   B.n = A.n;
@@ -1462,6 +1516,12 @@ static void permute_csr(bf_ctx *c, const DCsr &A, const int32_t *rperm, const in
   dfree(c, cnt);
   B.ci = dalloc_t<int32_t>(c, B.nnz);
   B.v = dalloc_t<double>(c, B.nnz);
+  if ((double)A.nnz <= 4.0 * (double)A.n) {
+    k_perm_fill_short<<<div_up(A.n, 256), 256, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, rperm, cinv, B.rp, B.ci, B.v);
+    c->launches += 2;
+    BF_CUDA(cudaGetLastError());
+    return;
+  }
   int *longrow = dalloc_t<int>(c, 1);
   BF_CUDA(cudaMemsetAsync(longrow, 0, sizeof(int), c->stream));
   k_perm_fill_warp<<<div_up(A.n, 8), 256, 0, c->stream>>>(A.n, A.rp, A.ci, A.v, rperm, cinv, B.rp, B.ci, B.v,
