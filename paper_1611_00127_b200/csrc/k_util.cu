@@ -3,45 +3,52 @@
 // setup path: a scan and a sort are library steps, the method's arithmetic is ours).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "bf_internal.cuh"
 BF_CHECK_TU("k_util.cu")
 
 namespace bf {
 
+// input of the scans: counts[0..n) followed by one zero, without a padded copy
+template <typename T>
+struct PaddedCounts {
+  const T *p;
+  int64_t n;
+  __host__ __device__ T operator()(int64_t i) const { return i < n ? p[i] : T(0); }
+};
+template <typename T>
+static auto padded_input(const T *counts, int64_t n) {
+  return thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), PaddedCounts<T>{counts, n});
+}
+
 int64_t exclusive_scan_i32(bf_ctx *c, const int32_t *counts, int32_t *out, int32_t n) {
   // out[0..n] with out[n] = total; the total must fit int32 (checked by the caller's allocator)
   size_t tmp = 0;
-  BF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, out, n + 1, c->stream));
+  auto in = padded_input(counts, n);
+  BF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, c->stream));
   void *t = dalloc(c, tmp + 16);
-  // counts has n entries; make the (n+1)-th element 0 by scanning a padded copy
-  int32_t *padded = dalloc_t<int32_t>(c, (size_t)n + 1);
-  BF_CUDA(cudaMemcpyAsync(padded, counts, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
-  BF_CUDA(cudaMemsetAsync(padded + n, 0, sizeof(int32_t), c->stream));
-  BF_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, padded, out, n + 1, c->stream));
+  BF_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n + 1, c->stream));
   c->launches += 2;
   int32_t total = 0;
   BF_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   dfree(c, t);
-  dfree(c, padded);
   return total;
 }
 
 int64_t exclusive_scan_i64(bf_ctx *c, const int64_t *counts, int64_t *out, int64_t n) {
   size_t tmp = 0;
-  int64_t *padded = dalloc_t<int64_t>(c, (size_t)n + 1);
-  BF_CUDA(cudaMemcpyAsync(padded, counts, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
-  BF_CUDA(cudaMemsetAsync(padded + n, 0, sizeof(int64_t), c->stream));
-  BF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, padded, out, n + 1, c->stream));
+  auto in = padded_input(counts, n);
+  BF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, c->stream));
   void *t = dalloc(c, tmp + 16);
-  BF_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, padded, out, n + 1, c->stream));
+  BF_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n + 1, c->stream));
   c->launches += 2;
   int64_t total = 0;
   BF_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   dfree(c, t);
-  dfree(c, padded);
   return total;
 }
 
