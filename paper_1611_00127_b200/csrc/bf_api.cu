@@ -330,13 +330,9 @@ Tuning tuning_from_env() {
   t.tma_g_p = (int)env_num("BF_TMA_G_P", 0);
   t.tma_g_r = (int)env_num("BF_TMA_G_R", 0);
   t.spgemm = env_flag("BF_SPGEMM_ESC") ? 2 : (env_flag("BF_SPGEMM_HASH") ? 1 : 0);
-  t.tpr_amax = env_num("BF_TPR_AMAX", t.tpr_amax);
   t.wk_amin = env_num("BF_WK_AMIN", t.wk_amin);
   t.hash_small = !env_flag("BF_NO_HASH_SMALL");
   t.hash_large = !env_flag("BF_NO_HASH_LARGE");
-  t.hash_large_min = env_num("BF_HASH_LARGE_MIN", t.hash_large_min);
-  t.interp_warp_min = env_num("BF_INTERP_WARP_MIN", t.interp_warp_min);
-  t.tpr_bmax = env_num("BF_TPR_BMAX", t.tpr_bmax);
   t.ilu_ctas = std::max(1, (int)env_num("BF_ILU_CTAS", t.ilu_ctas));
   t.ilu_pencil = env_num("BF_ILU_PENCIL", 1.0) != 0.0;
   t.ilu_flags = env_flag("BF_ILU_FLAGS");
