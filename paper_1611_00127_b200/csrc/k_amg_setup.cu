@@ -303,18 +303,11 @@ __global__ void k_interp_fill(DCsr A, const uint8_t *__restrict__ strong, const 
 constexpr int IW_WARPS = 8;
 constexpr int IW_CAP = 128;
 
-__global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uint8_t *__restrict__ strong,
-                                                               const int8_t *__restrict__ cf,
-                                                               const int32_t *__restrict__ cmap,
-                                                               const double *__restrict__ diag, int norm, DCsr P,
-                                                               uint8_t *long_rows, int *any_long) {
-  __shared__ int s_ccol[IW_WARPS][IW_CAP];
-  __shared__ double s_num[IW_WARPS][IW_CAP];
-  __shared__ int s_fk[IW_WARPS][IW_CAP];
-  __shared__ double s_fa[IW_WARPS][IW_CAP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * IW_WARPS + warp;
-  if (i >= A.n) return;
+__device__ __forceinline__ void interp_warp_row(const DCsr &A, const uint8_t *__restrict__ strong,
+                                                const int8_t *__restrict__ cf, const int32_t *__restrict__ cmap,
+                                                const double *__restrict__ diag, int norm, const DCsr &P,
+                                                uint8_t *long_rows, int *any_long, int i, int lane, int *ccol,
+                                                double *num, int *fk, double *fa) {
   const int base = P.rp[i], end = P.rp[i + 1];
   if (cf[i] == 1) {
     if (lane == 0) {
@@ -324,8 +317,6 @@ __global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uin
     return;
   }
   if (end == base) return;
-  int *ccol = s_ccol[warp], *fk = s_fk[warp];
-  double *num = s_num[warp], *fa = s_fa[warp];
   const int r0 = A.rp[i], r1 = A.rp[i + 1];
   // pass 1: C_i (ascending) with num = a_ij; F_i^s (ascending) with a_ik; dg over the weak set
   int nc = 0, nf = 0;
@@ -458,6 +449,25 @@ __global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uin
     double w = den == 0.0 ? 0.0 : (norm ? __ddiv_rn(num[u], den) : -__ddiv_rn(num[u], den));
     P.v[base + u] = w;
     P.ci[base + u] = cmap[ccol[u]];
+  }
+}
+
+// each warp walks rows i, i + (warps in the grid), ...: about a third of the rows are C points
+// and finish at once, so with one row per warp the resident warps idle (ncu: 30 % occupancy)
+__global__ void __launch_bounds__(IW_WARPS * 32) k_interp_warp(DCsr A, const uint8_t *__restrict__ strong,
+                                                               const int8_t *__restrict__ cf,
+                                                               const int32_t *__restrict__ cmap,
+                                                               const double *__restrict__ diag, int norm, DCsr P,
+                                                               uint8_t *long_rows, int *any_long) {
+  __shared__ int s_ccol[IW_WARPS][IW_CAP];
+  __shared__ double s_num[IW_WARPS][IW_CAP];
+  __shared__ int s_fk[IW_WARPS][IW_CAP];
+  __shared__ double s_fa[IW_WARPS][IW_CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * IW_WARPS + warp; i < A.n; i += gridDim.x * IW_WARPS) {
+    interp_warp_row(A, strong, cf, cmap, diag, norm, P, long_rows, any_long, i, lane, s_ccol[warp], s_num[warp],
+                    s_fk[warp], s_fa[warp]);
+    __syncwarp();  // the next row reuses the warp's shared-memory lists
   }
 }
 
@@ -1702,7 +1712,8 @@ void build_hierarchy(bf_ctx *c, int which, const DCsr &A0) {
       if ((double)A.nnz / n > c->tune.interp_warp_min) {  // long (Galerkin) rows: warp per row; short rows: thread per row
         BF_CUDA(cudaMemsetAsync(long_rows, 0, n, c->stream));
         BF_CUDA(cudaMemsetAsync(any_long, 0, sizeof(int), c->stream));
-        k_interp_warp<<<div_up(n, IW_WARPS), IW_WARPS * 32, 0, c->stream>>>(A, strong, state, cmap, diag,
+        const int iw_grid = std::max(1, std::min(div_up(n, IW_WARPS), 4 * c->num_sms * std::max(1, occupancy(c, (const void *)k_interp_warp, IW_WARPS * 32, 0))));
+        k_interp_warp<<<iw_grid, IW_WARPS * 32, 0, c->stream>>>(A, strong, state, cmap, diag,
                                                                            o.interp_norm, L.P, long_rows, any_long);
         BF_LAUNCH(c);
         BF_CUDA(cudaMemcpyAsync(&h_long, any_long, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
